@@ -1,0 +1,93 @@
+"""Gen-CFR with RM / RM+ and the CFR(RM), CFR(RM+), CFR+ variants (oracle side).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md:1-106: Algorithm Gen-CFR (alternating updates), RM (Algorithm RM),
+RM+ (Algorithm RM+), stepsizes alpha^t = 1/t (CFR(RM), CFR(RM+)) and
+alpha^t = 2t/(t^2+t) (CFR+).  Strategies are kept per simplex in behavioural
+form z^j (the regret minimiser's output), so Gen-CFR's ratio
+x^{j,t-1} / x^{t-1}_{p_j} is z^{j,t-1} (reading R3 for zero parent weight).
+"""
+import numpy as np
+
+VARIANTS = {
+    "cfr_rm": ("rm", "uniform"),
+    "cfr_rmp": ("rmp", "uniform"),
+    "cfr_plus": ("rmp", "linear"),
+}
+
+
+def alpha(scheme, t):
+    """1/t, or 2t/(t^2+t)."""
+    return 1.0 / t if scheme == "uniform" else 2.0 * t / (t * t + t)
+
+
+def regret_update(kind, r, z, g):
+    """One call of RM or RM+  on one simplex.
+    g is the gain (utility) vector; returns (r^t, z^t)."""
+    r_new = r + g - np.dot(z, g)
+    if kind == "rmp":
+        r_new = np.maximum(r_new, 0.0)
+    pos = np.maximum(r_new, 0.0)
+    tot = pos.sum()
+    z_new = pos / tot if tot > 0 else np.full(len(r), 1.0 / len(r))
+    return r_new, z_new
+
+
+class CFRState:
+    def __init__(self, sf, variant):
+        self.kind, self.scheme = VARIANTS[variant]
+        self.sf = sf
+        self.zx = sf.X.uniform_behavioral()     # x^0 uniform
+        self.zy = sf.Y.uniform_behavioral()
+        self.rx = np.zeros(sf.X.n_seq)
+        self.ry = np.zeros(sf.Y.n_seq)
+        self.x = sf.X.behavioral_to_sequence(self.zx)
+        self.y = sf.Y.behavioral_to_sequence(self.zy)
+        self.xbar = np.zeros(sf.X.n_seq)
+        self.ybar = np.zeros(sf.Y.n_seq)
+        self.t = 1
+        self.grads = 0
+
+
+def _pass(tp, g, z, r, kind):
+    """Bottom-up pass of Gen-CFR lines 30-33 / 36-39: fold <g^j, z^{j,t-1}> into
+    g_{p_j}, then z^{j,t} = R(g^j)."""
+    g = np.array(g, dtype=float)
+    z = z.copy()
+    r = r.copy()
+    for j in tp.bottom_up():
+        s, n, p = tp.start[j], tp.size[j], tp.parent[j]
+        gj = g[s:s + n]
+        g[p] += np.dot(gj, z[s:s + n])
+        r[s:s + n], z[s:s + n] = regret_update(kind, r[s:s + n], z[s:s + n], gj)
+    return z, r
+
+
+def cfr_iteration(st):
+    sf = st.sf
+    g = -sf.Ay(st.y)                                   # line 29: g = -A y^{t-1}
+    st.grads += 1
+    st.zx, st.rx = _pass(sf.X, g, st.zx, st.rx, st.kind)
+    st.x = sf.X.behavioral_to_sequence(st.zx)
+    a = alpha(st.scheme, st.t)
+    st.xbar = a * st.x + (1 - a) * st.xbar            # line 34
+    g = sf.ATx(st.x)                                   # line 35: g = A^T x^t (alternating)
+    st.grads += 1
+    st.zy, st.ry = _pass(sf.Y, g, st.zy, st.ry, st.kind)
+    st.y = sf.Y.behavioral_to_sequence(st.zy)
+    st.ybar = a * st.y + (1 - a) * st.ybar            # line 41, same alpha^t (reading R9)
+    st.t += 1
+    return st
+
+
+def run(sf, variant, iters):
+    st = CFRState(sf, variant)
+    for _ in range(iters):
+        cfr_iteration(st)
+    return st
+
+
+def cfr_plus_regret_bound(sf, T, L):
+    """2 |S_X| L sqrt(max_j |Delta_j|) / sqrt(T)."""
+    return 2.0 * sf.X.n_simplex * L * np.sqrt(sf.X.size.max()) / np.sqrt(T)

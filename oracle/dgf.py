@@ -1,0 +1,98 @@
+"""Dilated entropy DGF, smoothed best response and prox mapping (oracle side).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md:448-537 (Section "Smoothed Best Responses") and the appendix
+"Prox shift".  Vectors follow oracle/treeplex.py: entry 0 is
+the empty sequence (value 1); a gradient's entry 0 carries the terms that do
+not depend on the player's own sequences (leaves reached before the player's
+first move), so after the bottom-up pass it holds the objective value.
+"""
+import math
+
+import numpy as np
+
+
+def d_simplex(xbar):
+    """d_j(x) = sum_i x_i log x_i + log n, with 0 log 0 = 0."""
+    xbar = np.asarray(xbar, dtype=float)
+    nz = xbar > 0
+    return float(np.sum(xbar[nz] * np.log(xbar[nz])) + math.log(len(xbar)))
+
+
+def dgf_value(tp, q):
+    """d(q) = sum_j beta_j q_{p_j} d_j(q^j / q_{p_j}).
+    Simplexes with zero parent weight contribute 0."""
+    total = 0.0
+    for j in range(tp.n_simplex):
+        s, n, p = tp.start[j], tp.size[j], tp.parent[j]
+        qp = q[p]
+        if qp > 0:
+            total += tp.beta[j] * qp * d_simplex(q[s:s + n] / qp)
+    return total
+
+
+def dgf_gradient(tp, q):
+    """Appendix formula, for interior q:
+    grad_{ji} d(q) = beta_j (log(q_i / q_{p_j}) + 1) + sum_{k in D_j^i} beta_k (log n_k - 1).
+    Entry 0 (the empty sequence, not a variable) is 0."""
+    q = np.asarray(q, dtype=float)
+    if (q[1:] <= 0).any():
+        raise ValueError("dgf_gradient requires an interior point (all q_i > 0)")
+    g = np.zeros(tp.n_seq)
+    for j in range(tp.n_simplex):
+        s, n, p = tp.start[j], tp.size[j], tp.parent[j]
+        g[s:s + n] = tp.beta[j] * (np.log(q[s:s + n] / q[p]) + 1.0)
+    for j in range(tp.n_simplex):
+        p = tp.parent[j]
+        if p != 0:
+            g[p] += tp.beta[j] * (math.log(tp.size[j]) - 1.0)
+    return g
+
+
+def prox_shift_closed_form(tp):
+    """-d(q) + <grad d(q), q> = -sum_{j: b_Q^j = 0} beta_j q_{p_j} (log n_j - 1)
+    (PAPER.md:876), with q_{p_j} = 1 at root simplexes."""
+    return -sum(tp.beta[j] * (math.log(tp.size[j]) - 1.0) for j in tp.roots)
+
+
+def smoothed_best_response(tp, g, mu):
+    """argmin_{q in Q} <q, g> + mu d(q) and its value, by the paper's closed form.
+
+    PAPER.md:467-512.  Bottom-up over the simplexes; at simplex j (after the
+    values of the simplexes below have been added to g):
+      qbar_i  proportional to  exp(-g_i / (mu beta_j))
+    computed with the smallest g_i subtracted (overflow safety), then the value
+      g_{i*} + mu beta_j log qbar_{i*} + mu beta_j log n,  i* = argmax qbar_i
+     is added to the parent entry g_{p_j}.  mu scales every
+    beta_j (mu d(q) in Eq. (4)).  Returns (q, value): q in
+    sequence form, value = final g[0] = <q, g> + mu d(q) at the minimiser.
+    """
+    G = np.array(g, dtype=float)
+    b = np.zeros(tp.n_seq)
+    b[0] = 1.0
+    for j in tp.bottom_up():
+        s, n, p = tp.start[j], tp.size[j], tp.parent[j]
+        w = mu * tp.beta[j]
+        Gj = G[s:s + n]
+        e = np.exp(-(Gj - Gj.min()) / w)
+        qbar = e / e.sum()
+        i_star = int(np.argmax(qbar))
+        G[p] += Gj[i_star] + w * math.log(qbar[i_star]) + w * math.log(n)
+        b[s:s + n] = qbar
+    return tp.behavioral_to_sequence(b), float(G[0])
+
+
+def conjugate_gradient(tp, g, mu=1.0):
+    """grad d*(g) = argmax_q <g, q> - mu d(q)."""
+    q, _ = smoothed_best_response(tp, -np.asarray(g, dtype=float), mu)
+    return q
+
+
+def prox_mapping(tp, g, q_prev):
+    """argmin_{q in Q} <q, g> + D(q || q_prev), D the Bregman divergence of d
+    (PAPER.md:514-528): solved as a smoothed best response (mu = 1) on the
+    shifted gradient g - grad d(q_prev)."""
+    shifted = np.asarray(g, dtype=float) - dgf_gradient(tp, q_prev)
+    q, _ = smoothed_best_response(tp, shifted, 1.0)
+    return q
