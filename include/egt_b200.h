@@ -1,0 +1,199 @@
+/*
+ * egt_b200.h — C ABI of the B200-native EGT / CFR solver for poker endgames.
+ *
+ * Method: arXiv:1810.03063 (reference text at PAPER.md, cited as PAPER.md:<line>).
+ * The library solves  min_{x in X} max_{y in Y} <x, A y>
+ * over the players' sequence-form treeplexes, for a BATCH of independent games
+ * that share one public betting tree (same pot/stack/abstraction; each game has
+ * its own board and hand priors).  x is player 1 (moves first, "Libratus",
+ * minimises), y is player 2.  A is player 2's payoff.  A is never materialised.
+ *
+ * Vector layout (device, fp64): for player p, a vector holds, per game g, a
+ * row-major [n_pub[p]][H_pad] block; row 0 is the empty sequence (value 1 in a
+ * strategy, the value/constant term in a gradient; R1), row s >= 1 is
+ * public sequence s (a decision node of p and one of its actions) for every
+ * private hand h < H (columns H..H_pad-1 are padding, kept 0).  Game g's block
+ * starts at g * vec_stride[p] doubles.  Hands are in the library's internal
+ * order (for river games: ascending showdown strength on that game's board);
+ * egt_hand_cards() gives each internal hand's cards.
+ *
+ * Ownership: the library allocates and frees all of its device memory; pointers
+ * passed in (host or device, as stated per call) stay owned by the caller and are
+ * only read/written during the call (device writes are stream-ordered: complete
+ * when the stream set by egt_set_stream, default the legacy default stream, syncs).
+ *
+ * Errors: every int-returning call returns 0 on success and a negative EGT_E_*
+ * code on failure; egt_last_error() returns a message for the calling thread.
+ * No call falls back to a CPU implementation: without a usable CUDA device every
+ * call that touches the device fails with EGT_E_CUDA.
+ */
+#ifndef EGT_B200_H
+#define EGT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EGT_OK 0
+#define EGT_E_ARG (-1)     /* invalid argument */
+#define EGT_E_CUDA (-2)    /* CUDA runtime error (or no device) */
+#define EGT_E_STATE (-3)   /* call out of order (e.g. egt_step before egt_init) */
+#define EGT_E_NUMERIC (-4) /* numerical failure (e.g. EGT/as tau underflow) */
+
+/* Game kinds */
+#define EGT_GAME_KUHN 1  /* 3-card Kuhn poker, ante 1, bet 1 */
+#define EGT_GAME_LEDUC 2 /* Leduc hold'em: 6 cards, bets 2/4, 2 bets per round */
+#define EGT_GAME_RIVER 3 /* NLHE river endgame */
+
+/* River bet-size contexts (R10), index into the spec arrays */
+#define EGT_CTX_P1_OPEN 0
+#define EGT_CTX_P1_VS_BET 1
+#define EGT_CTX_P1_VS_RAISE 2
+#define EGT_CTX_P1_SUBSEQ 3
+#define EGT_CTX_P2_VS_CHECK 4
+#define EGT_CTX_P2_VS_BET 5
+#define EGT_CTX_P2_SUBSEQ 6
+#define EGT_N_CTX 7
+#define EGT_MAX_FRACS 16
+
+typedef struct {
+    int32_t kind;    /* EGT_GAME_* */
+    int32_t n_games; /* batch size B >= 1 */
+    /* --- river only (ignored for Kuhn/Leduc) --- */
+    int32_t pot;       /* chips in the pot at the start of the river; each player put pot/2 */
+    int32_t stack;     /* chips behind per player at the start of the river */
+    int32_t raise_cap; /* max bets+raises in the street (<= 0: unlimited) */
+    int32_t open_fold; /* 1: fold is offered facing no bet */
+    int32_t n_fracs[EGT_N_CTX];                 /* pot multipliers per context ...  */
+    int32_t frac_num[EGT_N_CTX][EGT_MAX_FRACS]; /* ... as exact rationals num/den  */
+    int32_t frac_den[EGT_N_CTX][EGT_MAX_FRACS];
+    int32_t allin[EGT_N_CTX]; /* 1: all-in offered in the context */
+    int32_t n_ranks;          /* deck: top n_ranks ranks (13 = standard) */
+    int32_t n_suits;          /* deck: suits (4 = standard) */
+    const int32_t* boards;    /* HOST [n_games][5] card ids (rank_pos*n_suits + suit) */
+    const double* prior1;     /* HOST [n_games][n_combos] canonical combos (c1<c2 lexicographic), >= 0; NULL = uniform */
+    const double* prior2;     /* as prior1, for player 2 */
+} egt_game_spec;
+
+typedef struct egt_game egt_game; /* opaque */
+
+typedef struct {
+    int32_t n_games;
+    int32_t H;          /* private hands per game (river: combos avoiding the board) */
+    int32_t H_pad;      /* row length in doubles (H rounded up to 32) */
+    int32_t n_combos;   /* canonical hole-card combos of the deck (river) / cards (Kuhn, Leduc) */
+    int32_t n_pub[2];   /* public sequences per player, including row 0 (empty sequence) */
+    int32_t n_nodes[2]; /* public decision nodes per player */
+    int32_t n_terminals;
+    int32_t depth[2];   /* levels of decision nodes per player */
+    int64_t vec_stride[2]; /* doubles per game in a player's vector (= n_pub * H_pad) */
+    double max_abs_A[1];   /* reserved: ||A|| of game 0 (max |A_ij|, R7) */
+} egt_game_info;
+
+/* ---- game ---------------------------------------------------------------- */
+
+/* Build the public tree, the per-player treeplex layout, the
+ * per-board hand-strength order and card-removal tables, and upload them.
+ * spec: host struct, read only during the call.  *out receives the handle.
+ * Errors: EGT_E_ARG on an invalid spec (bad kind/deck/board/fractions), EGT_E_CUDA. */
+int egt_load_game(const egt_game_spec* spec, egt_game** out);
+
+/* Free everything owned by the handle (NULL is a no-op). */
+void egt_free_game(egt_game* game);
+
+/* Stream for every subsequent call on this game (cudaStream_t as void*; NULL = legacy default). */
+int egt_set_stream(egt_game* game, void* stream);
+
+int egt_game_info_get(const egt_game* game, egt_game_info* out);
+
+/* Internal hand h of game g -> its cards: HOST out[2*h+0], out[2*h+1] (second -1 for
+ * one-card hands), for h < H.  out: int32 [2*H]. */
+int egt_hand_cards(const egt_game* game, int32_t g, int32_t* out);
+
+/* Public history string of public sequence s >= 1 of `player` (tokens joined by
+ * '/': k check, c call, f fold, b<n> bet/raise to n chips this round, d<card> a
+ * public card), NUL-terminated into buf[buflen].  s = 0 gives "" (empty sequence). */
+int egt_pub_history(const egt_game* game, int32_t player, int32_t s, char* buf, int32_t buflen);
+
+/* ---- kernel-level calls (device pointers, all games of the batch) ------------ */
+
+/* Gradient of the bilinear form (Gen-CFR lines 29/35):
+ *   player 0: out = A y   (in: y, player-1 layout; out: player-0 layout)
+ *   player 1: out = A^T x (in: x, player-0 layout; out: player-1 layout)
+ * evaluated per terminal without materialising A: fold payoffs by inclusion-exclusion
+ * over blocked cards, showdowns by strength-sorted prefix sums with card-removal
+ * correction.  Row 0 of `in` is ignored (the empty sequence is 1); row 0 of `out`
+ * receives the terms of leaves where `player` has not acted yet.
+ * dev_in/dev_out: DEVICE fp64, n_games * vec_stride[.] each. */
+int egt_gradient(egt_game* game, int32_t player, const double* dev_in, double* dev_out);
+
+/* Smoothed best response: per game, q = argmin_{q in Q_player}
+ * <q, gsign*g> + mu_g d(q) with d the dilated entropy.
+ * dev_g: DEVICE gradient (player layout); dev_mu: DEVICE [n_games];
+ * dev_q: DEVICE out, sequence form (may be NULL); dev_b: DEVICE out, behavioural
+ * (row 0 = 1; may be NULL); dev_value: DEVICE out [n_games], min value (may be NULL). */
+int egt_smoothed_br(egt_game* game, int32_t player, const double* dev_g, double gsign,
+                    const double* dev_mu, double* dev_q, double* dev_b, double* dev_value);
+
+/* Prox mapping: q = argmin_q <q, s_g * gsign * g> + D(q || z), z given
+ * by its behavioural form dev_center_b (DEVICE, player layout), s_g = dev_step[g].
+ * dev_q: DEVICE out, sequence form. */
+int egt_prox(egt_game* game, int32_t player, const double* dev_g, double gsign,
+             const double* dev_step, const double* dev_center_b, double* dev_q);
+
+/* Best response value per game: min_{q in Q} <q, gsign*g>  (dev_value DEVICE [n_games]). */
+int egt_best_response(egt_game* game, int32_t player, const double* dev_g, double gsign,
+                      double* dev_value);
+
+/* ---- solvers --------------------------------------------------------------- */
+
+#define EGT_THEORY 0   /* Alg. 1: tau_t = 2/(t+3), alternate x/y, theory mu */
+#define EGT_BALANCED 1 /* "EGT": mu balancing, tau_t = 2/(t+3) */
+#define EGT_AS 2       /* "EGT/as": Alg. 3-4, aggressive mu reduction with EGC check */
+
+/* Initialise EGT (Alg. 1/3 lines 1-2, R4) for every game.  mu_x, mu_y > 0:
+ * initial smoothing; <= 0: EGT_THEORY uses ||A||/sqrt(phi_X phi_Y); the others search
+ * the smallest mu = mu_theory * 2^-k (k = 30..0) whose initial point satisfies the EGC
+ * (R14), per game. */
+int egt_init(egt_game* game, int32_t variant, double mu_x, double mu_y);
+
+/* Run n_iters iterations for every game.  For EGT_AS one iteration is one Step
+ * attempt (+ EGC check): a failed attempt halves tau and leaves the iterate
+ * unchanged, so Alg. 4's inner loop unrolls into consecutive iterations. */
+int egt_step(egt_game* game, int32_t n_iters);
+
+#define CFR_RM 0   /* CFR(RM):  RM,  alpha_t = 1/t */
+#define CFR_RMP 1  /* CFR(RM+): RM+, alpha_t = 1/t */
+#define CFR_PLUS 2 /* CFR+:     RM+, alpha_t = 2t/(t^2+t) */
+
+int cfr_init(egt_game* game, int32_t variant);
+int cfr_step(egt_game* game, int32_t n_iters);
+
+/* Saddle-point residual eps_sad per game, written to HOST out[n_games].
+ * which = 0: the solver's current iterate (EGT x^t, y^t; CFR x^t, y^t);
+ * which = 1: the CFR averages (xbar, ybar); for EGT the same as 0. */
+int saddle_gap(egt_game* game, int32_t which, double* host_out);
+
+/* Strategy of `player` in sequence form, HOST out [n_games][n_pub][n_combos]: the EGT
+ * iterate, or the CFR average; canonical combo/card order; hands blocked by the
+ * board are 0; row 0 = 1. */
+int get_avg_strategy(egt_game* game, int32_t player, double* host_out);
+
+/* Solver vectors in the internal DEVICE layout (copies into dev_out, vec_stride doubles/game):
+ * which = 0 current iterate (sequence form), 1 CFR average (EGT: current),
+ * 2 CFR cumulative regrets, 3 CFR current behavioural strategy. */
+int get_strategy_device(egt_game* game, int32_t player, int32_t which, double* dev_out);
+
+/* Per-game solver scalars to HOST out[n_games][8]:
+ * mu_x, mu_y, tau, t (accepted steps / CFR iterations), attempts, backtracks,
+ * last EGV, gradient evaluations (A y or A^T x, per game). */
+int egt_scalars(egt_game* game, double* host_out);
+
+const char* egt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EGT_B200_H */

@@ -22,13 +22,22 @@ def alpha(scheme, t):
     return 1.0 / t if scheme == "uniform" else 2.0 * t / (t * t + t)
 
 
+SNAP = 1e-13
+
+
 def regret_update(kind, r, z, g):
     """One call of RM or RM+  on one simplex.
-    g is the gain (utility) vector; returns (r^t, z^t)."""
-    r_new = r + g - np.dot(z, g)
+    g is the gain (utility) vector; returns (r^t, z^t).
+
+    Reading R15: "if r^t = 0 use uniform strategy" is decided robustly -- a regret
+    entry no larger than SNAP * (|r^{t-1}_a| + |g_a| + |<z^{t-1}, g>|) (the rounding
+    noise of its own update) counts as 0 in [r^t]^+."""
+    val = float(np.dot(z, g))
+    r_new = r + g - val
     if kind == "rmp":
         r_new = np.maximum(r_new, 0.0)
-    pos = np.maximum(r_new, 0.0)
+    tol = SNAP * (np.abs(r) + np.abs(g) + abs(val))
+    pos = np.where(r_new > tol, r_new, 0.0)
     tot = pos.sum()
     z_new = pos / tot if tot > 0 else np.full(len(r), 1.0 / len(r))
     return r_new, z_new

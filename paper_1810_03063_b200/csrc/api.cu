@@ -1,0 +1,812 @@
+// C ABI (include/egt_b200.h): device layout upload, solver drivers, graphs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/egt_b200.h"
+#include "game.h"
+#include "kernels.cuh"
+
+using namespace egt;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                                 \
+    do {                                                                                         \
+        cudaError_t _e = (call);                                                                 \
+        if (_e != cudaSuccess) return fail(EGT_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+enum SolverKind { SOLVER_NONE = 0, SOLVER_EGT = 1, SOLVER_CFR = 2 };
+
+struct egt_game {
+    HostGame host;
+    DevGame dg{};
+    DevPlayer dp[2]{};
+    std::vector<void*> allocs;
+    cudaStream_t st = nullptr;      // internal stream (graphs are captured here)
+    cudaStream_t user = nullptr;    // caller's stream (nullptr = legacy default)
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    long long V[2] = {0, 0};        // doubles per game per player vector
+    // scratch
+    double* partial = nullptr;
+    unsigned* counter = nullptr;
+    // solver state
+    int solver = SOLVER_NONE;
+    int variant = 0;
+    DevScalars sc{};
+    double* mu_base = nullptr;      // [2][G] for the mu search
+    int* search_mask = nullptr;     // [G]
+    double* gapval = nullptr;       // [2][G]
+    double* S[2] = {nullptr, nullptr};   // EGT state, 2 slots
+    double* C[2] = {nullptr, nullptr};   // EGT cache (behavioural smoothed BR), 2 slots
+    double* HAT[2] = {nullptr, nullptr};
+    double* RESP[2] = {nullptr, nullptr};
+    double* GR[2] = {nullptr, nullptr};
+    double* R[2] = {nullptr, nullptr};   // CFR regrets
+    double* Z[2] = {nullptr, nullptr};   // CFR behavioural strategy
+    double* Q[2] = {nullptr, nullptr};   // CFR sequence-form strategy
+    double* AVG[2] = {nullptr, nullptr}; // CFR average
+    cudaGraphExec_t graph = nullptr;
+    long long grads = 0;            // gradient evaluations per game
+    int grads_per_iter = 0;
+};
+
+const char* egt_last_error(void) { return g_err.c_str(); }
+
+template <class T>
+static int dalloc(egt_game* G, T** p, size_t n) {
+    void* q = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+    if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    G->allocs.push_back(q);
+    *p = (T*)q;
+    return 0;
+}
+
+template <class T>
+static int upload(egt_game* G, T** p, const std::vector<T>& v) {
+    int r = dalloc(G, p, v.size());
+    if (r) return r;
+    if (!v.empty()) CK(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return 0;
+}
+
+static VecRef vec(double* base, long long stride) {
+    VecRef r;
+    r.base = base;
+    r.game_stride = stride;
+    return r;
+}
+
+// 2-slot buffers are laid out [slot][G][V]; the slot of game g is cur[g] ^ x
+static VecRef slot2(egt_game* G, double* base, int p, int x) {
+    VecRef r;
+    r.base = base;
+    r.game_stride = G->V[p];
+    r.slot_stride = (long long)G->host.n_games * G->V[p];
+    r.slot_sel = G->sc.cur;
+    r.slot_xor = x;
+    return r;
+}
+
+static int begin(egt_game* G) {
+    CK(cudaEventRecord(G->ev_in, G->user));
+    CK(cudaStreamWaitEvent(G->st, G->ev_in, 0));
+    return 0;
+}
+
+static int end(egt_game* G) {
+    CK(cudaEventRecord(G->ev_out, G->st));
+    CK(cudaStreamWaitEvent(G->user, G->ev_out, 0));
+    return 0;
+}
+
+// ----------------------------------------------------------------------------- load
+extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
+    if (!spec || !out) return fail(EGT_E_ARG, "null argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EGT_E_CUDA, "no CUDA device");
+    egt_game* G = new egt_game();
+    std::string err = build_host_game(*spec, G->host);
+    if (!err.empty()) {
+        delete G;
+        return fail(EGT_E_ARG, err);
+    }
+    HostGame& H = G->host;
+    const int Gn = H.n_games, Hp = H.H_pad, nbs = H.tree.n_board_states;
+    int r = 0;
+#define TRY(x)                    \
+    do {                          \
+        r = (x);                  \
+        if (r) {                  \
+            egt_free_game(G);     \
+            return r;             \
+        }                         \
+    } while (0)
+    {
+        cudaError_t e = cudaStreamCreateWithFlags(&G->st, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_in, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_out, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = tree_prepare(0);
+        if (e != cudaSuccess) {
+            egt_free_game(G);
+            return fail(EGT_E_CUDA, std::string("stream/event: ") + cudaGetErrorString(e));
+        }
+    }
+    // tables
+    std::vector<int> nvalid;
+    std::vector<int16_t> order, lo, hi, src, pos4;
+    std::vector<uint8_t> valid;
+    for (const BoardTable& tb : H.tables) {
+        nvalid.push_back(tb.nvalid);
+        order.insert(order.end(), tb.order.begin(), tb.order.end());
+        lo.insert(lo.end(), tb.lo.begin(), tb.lo.end());
+        hi.insert(hi.end(), tb.hi.begin(), tb.hi.end());
+        src.insert(src.end(), tb.src.begin(), tb.src.end());
+        pos4.insert(pos4.end(), tb.pos4.begin(), tb.pos4.end());
+        valid.insert(valid.end(), tb.valid.begin(), tb.valid.end());
+    }
+    int *d_nvalid;
+    int16_t *d_order, *d_lo, *d_hi, *d_src, *d_pos;
+    uint8_t* d_valid;
+    TRY(upload(G, &d_nvalid, nvalid));
+    TRY(upload(G, &d_order, order));
+    TRY(upload(G, &d_lo, lo));
+    TRY(upload(G, &d_hi, hi));
+    TRY(upload(G, &d_src, src));
+    TRY(upload(G, &d_pos, pos4));
+    TRY(upload(G, &d_valid, valid));
+    double *d_p0, *d_p1, *d_kg;
+    TRY(upload(G, &d_p0, H.prior[0]));
+    TRY(upload(G, &d_p1, H.prior[1]));
+    TRY(upload(G, &d_kg, H.kappa_game));
+    std::vector<DevTerm> terms;
+    for (const Terminal& t : H.terms) {
+        DevTerm d;
+        d.amount = t.amount;
+        d.kappa = t.kappa;
+        d.kind = t.kind;
+        d.bs = t.board_state;
+        d.seq[0] = t.last_seq[0];
+        d.seq[1] = t.last_seq[1];
+        terms.push_back(d);
+    }
+    DevTerm* d_terms;
+    TRY(upload(G, &d_terms, terms));
+    G->dg.n_games = Gn;
+    G->dg.H = H.H;
+    G->dg.H_pad = Hp;
+    G->dg.hand_size = H.hand_size;
+    G->dg.n_bs = nbs;
+    G->dg.tab_nvalid = d_nvalid;
+    G->dg.tab_order = d_order;
+    G->dg.tab_lo = d_lo;
+    G->dg.tab_hi = d_hi;
+    G->dg.tab_pos = reinterpret_cast<const int4*>(d_pos);
+    G->dg.tab_src = d_src;
+    G->dg.tab_valid = d_valid;
+    G->dg.prior[0] = d_p0;
+    G->dg.prior[1] = d_p1;
+    G->dg.kappa_game = d_kg;
+    G->dg.terms = d_terms;
+    for (int p = 0; p < 2; ++p) {
+        const PlayerLayout& L = H.pl[p];
+        DevPlayer& P = G->dp[p];
+        P.n_pub = L.n_pub;
+        P.n_nodes = (int)L.first.size();
+        int *a, *b, *c, *d, *e, *f;
+        double* be;
+        TRY(upload(G, &a, L.first));
+        TRY(upload(G, &b, L.nact));
+        TRY(upload(G, &c, L.parent_seq));
+        TRY(upload(G, &d, L.board_state));
+        TRY(upload(G, &be, H.beta[p]));
+        TRY(upload(G, &e, L.term_off));
+        TRY(upload(G, &f, L.term_idx));
+        P.node_first = a;
+        P.node_nact = b;
+        P.node_parent = c;
+        P.node_bs = d;
+        P.beta = be;
+        P.term_off = e;
+        P.term_idx = f;
+        G->V[p] = (long long)L.n_pub * Hp;
+    }
+    const int max_tiles = (H.H + 31) / 32;
+    TRY(dalloc(G, &G->partial, (size_t)Gn * max_tiles));
+    TRY(dalloc(G, &G->counter, (size_t)Gn));
+    if (cudaMemset(G->counter, 0, sizeof(unsigned) * Gn) != cudaSuccess) {
+        egt_free_game(G);
+        return fail(EGT_E_CUDA, "memset");
+    }
+    // scalars
+    DevScalars& S = G->sc;
+    TRY(dalloc(G, &S.mu, 2 * (size_t)Gn));
+    TRY(dalloc(G, &S.mu_cand, 2 * (size_t)Gn));
+    TRY(dalloc(G, &S.tau, (size_t)Gn));
+    TRY(dalloc(G, &S.step, (size_t)Gn));
+    TRY(dalloc(G, &S.val, 2 * (size_t)Gn));
+    TRY(dalloc(G, &S.egv, (size_t)Gn));
+    TRY(dalloc(G, &S.focus, (size_t)Gn));
+    TRY(dalloc(G, &S.cur, (size_t)Gn));
+    TRY(dalloc(G, &S.t, (size_t)Gn));
+    TRY(dalloc(G, &S.attempts, (size_t)Gn));
+    TRY(dalloc(G, &S.backtracks, (size_t)Gn));
+    TRY(dalloc(G, &S.fail, (size_t)Gn));
+    TRY(dalloc(G, &G->mu_base, 2 * (size_t)Gn));
+    TRY(dalloc(G, &G->search_mask, (size_t)Gn));
+    TRY(dalloc(G, &G->gapval, 2 * (size_t)Gn));
+    for (int p = 0; p < 2; ++p) {
+        const size_t n = (size_t)Gn * G->V[p];
+        TRY(dalloc(G, &G->GR[p], n));
+        TRY(dalloc(G, &G->HAT[p], n));
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        egt_free_game(G);
+        return fail(EGT_E_CUDA, "sync after load");
+    }
+#undef TRY
+    *out = G;
+    return 0;
+}
+
+extern "C" void egt_free_game(egt_game* G) {
+    if (!G) return;
+    if (G->graph) cudaGraphExecDestroy(G->graph);
+    if (G->st) cudaStreamSynchronize(G->st);
+    for (void* p : G->allocs) cudaFree(p);
+    if (G->ev_in) cudaEventDestroy(G->ev_in);
+    if (G->ev_out) cudaEventDestroy(G->ev_out);
+    if (G->st) cudaStreamDestroy(G->st);
+    delete G;
+}
+
+extern "C" int egt_set_stream(egt_game* G, void* stream) {
+    if (!G) return fail(EGT_E_ARG, "null game");
+    G->user = (cudaStream_t)stream;
+    return 0;
+}
+
+extern "C" int egt_game_info_get(const egt_game* G, egt_game_info* o) {
+    if (!G || !o) return fail(EGT_E_ARG, "null argument");
+    const HostGame& H = G->host;
+    memset(o, 0, sizeof(*o));
+    o->n_games = H.n_games;
+    o->H = H.H;
+    o->H_pad = H.H_pad;
+    o->n_combos = H.n_combos;
+    for (int p = 0; p < 2; ++p) {
+        o->n_pub[p] = H.pl[p].n_pub;
+        o->n_nodes[p] = (int)H.pl[p].first.size();
+        o->depth[p] = H.pl[p].depth;
+        o->vec_stride[p] = G->V[p];
+    }
+    o->n_terminals = (int)H.terms.size();
+    o->max_abs_A[0] = 0.0;
+    return 0;
+}
+
+extern "C" int egt_hand_cards(const egt_game* G, int32_t g, int32_t* out) {
+    if (!G || !out || g < 0 || g >= G->host.n_games) return fail(EGT_E_ARG, "bad argument");
+    const HostGame& H = G->host;
+    for (int h = 0; h < H.H; ++h) {
+        out[2 * h] = H.hand_cards[((size_t)g * H.H + h) * 2];
+        out[2 * h + 1] = H.hand_size == 2 ? H.hand_cards[((size_t)g * H.H + h) * 2 + 1] : -1;
+    }
+    return 0;
+}
+
+extern "C" int egt_pub_history(const egt_game* G, int32_t player, int32_t s, char* buf, int32_t buflen) {
+    if (!G || !buf || buflen < 1 || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+    const PlayerLayout& L = G->host.pl[player];
+    if (s < 0 || s >= L.n_pub) return fail(EGT_E_ARG, "sequence out of range");
+    const std::string& h = L.seq_hist[s];
+    if ((int)h.size() + 1 > buflen) return fail(EGT_E_ARG, "buffer too small");
+    memcpy(buf, h.c_str(), h.size() + 1);
+    return 0;
+}
+
+// ----------------------------------------------------------------------------- kernel-level
+extern "C" int egt_gradient(egt_game* G, int32_t player, const double* din, double* dout) {
+    if (!G || !din || !dout || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+    if (begin(G)) return EGT_E_CUDA;
+    CK(launch_gradient(G->dg, G->dp[player], player, vec(const_cast<double*>(din), G->V[1 - player]),
+                       vec(dout, G->V[player]), nullptr, 0, G->st));
+    return end(G);
+}
+
+static TreeArgs base_args() { return TreeArgs(); }
+
+extern "C" int egt_smoothed_br(egt_game* G, int32_t player, const double* dg, double gsign, const double* dmu,
+                               double* dq, double* db, double* dval) {
+    if (!G || !dg || !dmu || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+    TreeArgs A = base_args();
+    A.mode = TM_SBR;
+    A.g = vec(const_cast<double*>(dg), G->V[player]);
+    A.gsign = gsign;
+    A.mu = dmu;
+    if (dq) A.out_q = vec(dq, G->V[player]);
+    if (db) A.out_b = vec(db, G->V[player]);
+    A.value = dval;
+    A.partial = G->partial;
+    A.counter = G->counter;
+    if (begin(G)) return EGT_E_CUDA;
+    CK(launch_tree(G->dg, G->dp[player], player, A, G->st));
+    return end(G);
+}
+
+extern "C" int egt_prox(egt_game* G, int32_t player, const double* dg, double gsign, const double* dstep,
+                        const double* dcenter_b, double* dq) {
+    if (!G || !dg || !dstep || !dcenter_b || !dq || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+    TreeArgs A = base_args();
+    A.mode = TM_PROX;
+    A.g = vec(const_cast<double*>(dg), G->V[player]);
+    A.gsign = gsign;
+    A.mu = dstep;
+    A.center = vec(const_cast<double*>(dcenter_b), G->V[player]);
+    A.out_q = vec(dq, G->V[player]);
+    if (begin(G)) return EGT_E_CUDA;
+    CK(launch_tree(G->dg, G->dp[player], player, A, G->st));
+    return end(G);
+}
+
+extern "C" int egt_best_response(egt_game* G, int32_t player, const double* dg, double gsign, double* dval) {
+    if (!G || !dg || !dval || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+    TreeArgs A = base_args();
+    A.mode = TM_BR;
+    A.g = vec(const_cast<double*>(dg), G->V[player]);
+    A.gsign = gsign;
+    A.value = dval;
+    A.partial = G->partial;
+    A.counter = G->counter;
+    if (begin(G)) return EGT_E_CUDA;
+    CK(launch_tree(G->dg, G->dp[player], player, A, G->st));
+    return end(G);
+}
+
+// ----------------------------------------------------------------------------- EGT
+static const double GSIGN[2] = {+1.0, -1.0};  // min-form objective of each player (R5)
+
+static int ensure_egt_buffers(egt_game* G) {
+    const int Gn = G->host.n_games;
+    for (int p = 0; p < 2; ++p) {
+        const size_t n = (size_t)Gn * G->V[p];
+        if (!G->S[p] && dalloc(G, &G->S[p], 2 * n)) return EGT_E_CUDA;
+        if (!G->C[p] && dalloc(G, &G->C[p], 2 * n)) return EGT_E_CUDA;
+        if (!G->RESP[p] && dalloc(G, &G->RESP[p], n)) return EGT_E_CUDA;
+    }
+    return 0;
+}
+
+static cudaError_t tree(egt_game* G, int p, const TreeArgs& A) { return launch_tree(G->dg, G->dp[p], p, A, G->st); }
+static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0) {
+    return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, G->st);
+}
+
+// EGT initial point (Alg. 1/3 lines 1-2, R4) at the current per-game mu;
+// leaves val[0] = phi_{mu_x}(y0), val[1] = -f_{mu_y}(x0) and the caches C[.][cur].
+static int egt_initial_point(egt_game* G) {
+    const int Gn = G->host.n_games;
+    DevScalars& S = G->sc;
+    // x_omega: the uniform behavioural strategy in sequence form
+    TreeArgs U = base_args();
+    U.mode = TM_UNIFORM;
+    U.out_q = vec(G->HAT[0], G->V[0]);
+    CK(tree(G, 0, U));
+    // y0 = y_{mu_y}(x_omega)
+    CK(grad(G, 1, vec(G->HAT[0], G->V[0]), vec(G->GR[1], G->V[1])));
+    TreeArgs A = base_args();
+    A.mode = TM_SBR;
+    A.g = vec(G->GR[1], G->V[1]);
+    A.gsign = GSIGN[1];
+    A.mu = S.mu + Gn;
+    A.out_q = slot2(G, G->S[1], 1, 0);
+    CK(tree(G, 1, A));
+    // x0 = x_{mu_x}(y0) (also the cache C[0]); phi_{mu_x}(y0)
+    CK(grad(G, 0, slot2(G, G->S[1], 1, 0), vec(G->GR[0], G->V[0])));
+    A = base_args();
+    A.mode = TM_SBR;
+    A.g = vec(G->GR[0], G->V[0]);
+    A.gsign = GSIGN[0];
+    A.mu = S.mu;
+    A.out_q = slot2(G, G->S[0], 0, 0);
+    A.out_b = slot2(G, G->C[0], 0, 0);
+    A.value = S.val;
+    A.partial = G->partial;
+    A.counter = G->counter;
+    CK(tree(G, 0, A));
+    // y_{mu_y}(x0) (cache C[1]) and -f_{mu_y}(x0)
+    CK(grad(G, 1, slot2(G, G->S[0], 0, 0), vec(G->GR[1], G->V[1])));
+    A = base_args();
+    A.mode = TM_SBR;
+    A.g = vec(G->GR[1], G->V[1]);
+    A.gsign = GSIGN[1];
+    A.mu = S.mu + Gn;
+    A.out_b = slot2(G, G->C[1], 1, 0);
+    A.value = S.val + Gn;
+    A.partial = G->partial;
+    A.counter = G->counter;
+    CK(tree(G, 1, A));
+    return 0;
+}
+
+static int record_egt_iteration(egt_game* G) {
+    const int Gn = G->host.n_games;
+    DevScalars& S = G->sc;
+    const int var = G->variant;
+    CK(launch_egt_prepare(var, Gn, S, G->st));
+    for (int p = 0; p < 2; ++p) {
+        const int o = 1 - p;
+        if (var != EGT_AS) {
+            // x_{mu_x}(y) for the focused player (not cached without the EGC check)
+            CK(grad(G, p, slot2(G, G->S[o], o, 0), vec(G->GR[p], G->V[p]), S.focus, p));
+            TreeArgs A = base_args();
+            A.mode = TM_SBR;
+            A.g = vec(G->GR[p], G->V[p]);
+            A.gsign = GSIGN[p];
+            A.mu = S.mu + (size_t)p * Gn;
+            A.out_b = slot2(G, G->C[p], p, 0);
+            A.mask = S.focus;
+            A.want = p;
+            CK(tree(G, p, A));
+        }
+        // Alg. 2 line 1: p_hat = (1 - tau) p + tau p_mu(o)
+        TreeArgs A = base_args();
+        A.mode = TM_COMBINE;
+        A.center = slot2(G, G->C[p], p, 0);
+        A.comb_in = slot2(G, G->S[p], p, 0);
+        A.comb_out = vec(G->HAT[p], G->V[p]);
+        A.tau = S.tau;
+        A.mask = S.focus;
+        A.want = p;
+        CK(tree(G, p, A));
+        // line 2: o_plus = (1 - tau) o + tau o_mu(p_hat)
+        CK(grad(G, o, vec(G->HAT[p], G->V[p]), vec(G->GR[o], G->V[o]), S.focus, p));
+        A = base_args();
+        A.mode = TM_SBR;
+        A.g = vec(G->GR[o], G->V[o]);
+        A.gsign = GSIGN[o];
+        A.mu = S.mu + (size_t)o * Gn;
+        A.out_q = vec(G->RESP[o], G->V[o]);
+        A.comb_in = slot2(G, G->S[o], o, 0);
+        A.comb_out = slot2(G, G->S[o], o, 1);
+        A.tau = S.tau;
+        A.mask = S.focus;
+        A.want = p;
+        CK(tree(G, o, A));
+        // line 3-4: p_til = prox_{p_mu(o)}(s grad f(p_hat)), p_plus = (1 - tau) p + tau p_til
+        CK(grad(G, p, vec(G->RESP[o], G->V[o]), vec(G->GR[p], G->V[p]), S.focus, p));
+        A = base_args();
+        A.mode = TM_PROX;
+        A.g = vec(G->GR[p], G->V[p]);
+        A.gsign = GSIGN[p];
+        A.mu = S.step;
+        A.center = slot2(G, G->C[p], p, 0);
+        A.comb_in = slot2(G, G->S[p], p, 0);
+        A.comb_out = slot2(G, G->S[p], p, 1);
+        A.tau = S.tau;
+        A.mask = S.focus;
+        A.want = p;
+        CK(tree(G, p, A));
+    }
+    if (var == EGT_AS) {
+        // excessive gap at the candidate: phi_{mu_x+}(y+) and -f_{mu_y+}(x+); refreshes the caches
+        for (int p = 0; p < 2; ++p) {
+            const int o = 1 - p;
+            CK(grad(G, p, slot2(G, G->S[o], o, 1), vec(G->GR[p], G->V[p])));
+            TreeArgs A = base_args();
+            A.mode = TM_SBR;
+            A.g = vec(G->GR[p], G->V[p]);
+            A.gsign = GSIGN[p];
+            A.mu = S.mu_cand + (size_t)p * Gn;
+            A.out_b = slot2(G, G->C[p], p, 1);
+            A.value = S.val + (size_t)p * Gn;
+            A.partial = G->partial;
+            A.counter = G->counter;
+            CK(tree(G, p, A));
+        }
+    }
+    CK(launch_egt_accept(var, Gn, S, G->st));
+    return 0;
+}
+
+static int build_graph(egt_game* G, int (*rec)(egt_game*)) {
+    if (G->graph) {
+        cudaGraphExecDestroy(G->graph);
+        G->graph = nullptr;
+    }
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(G->st, cudaStreamCaptureModeThreadLocal));
+    int r = rec(G);
+    cudaError_t e = cudaStreamEndCapture(G->st, &graph);
+    if (r) return r;
+    if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&G->graph, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+static int zero_scalars(egt_game* G) {
+    const int Gn = G->host.n_games;
+    DevScalars& S = G->sc;
+    CK(cudaMemsetAsync(S.cur, 0, sizeof(int) * Gn, G->st));
+    CK(cudaMemsetAsync(S.t, 0, sizeof(int) * Gn, G->st));
+    CK(cudaMemsetAsync(S.attempts, 0, sizeof(int) * Gn, G->st));
+    CK(cudaMemsetAsync(S.backtracks, 0, sizeof(int) * Gn, G->st));
+    CK(cudaMemsetAsync(S.fail, 0, sizeof(int) * Gn, G->st));
+    CK(cudaMemsetAsync(S.egv, 0, sizeof(double) * Gn, G->st));
+    std::vector<double> half(Gn, 0.5);
+    CK(cudaMemcpyAsync(S.tau, half.data(), sizeof(double) * Gn, cudaMemcpyHostToDevice, G->st));
+    CK(cudaStreamSynchronize(G->st));
+    return 0;
+}
+
+extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) {
+    if (!G || variant < EGT_THEORY || variant > EGT_AS) return fail(EGT_E_ARG, "bad argument");
+    const HostGame& H = G->host;
+    const int Gn = H.n_games;
+    if (ensure_egt_buffers(G)) return EGT_E_CUDA;
+    if (begin(G)) return EGT_E_CUDA;
+    if (zero_scalars(G)) return EGT_E_CUDA;
+    G->solver = SOLVER_EGT;
+    G->variant = variant;
+    if (G->graph) {
+        cudaGraphExecDestroy(G->graph);
+        G->graph = nullptr;
+    }
+    std::vector<double> mu(2 * (size_t)Gn);
+    const bool given = mu_x > 0 && mu_y > 0;
+    std::vector<double> mth(Gn);
+    if (!given) {
+        // mu_x = mu_y = ||A|| / sqrt(phi_X phi_Y), phi = 1/M
+        for (int g = 0; g < Gn; ++g)
+            mth[g] = compute_max_abs_A(H, g) * std::sqrt(H.M[0][g] * H.M[1][g]);
+    }
+    for (int g = 0; g < Gn; ++g) {
+        mu[g] = given ? mu_x : mth[g];
+        mu[Gn + g] = given ? mu_y : mth[g];
+    }
+    CK(cudaMemcpyAsync(G->sc.mu, mu.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
+    G->grads = 0;
+    if (!given && variant != EGT_THEORY) {
+        // DESIGN.md R14: smallest mu_theory * 2^-k (k = 30..0) whose initial point satisfies the EGC
+        CK(cudaMemcpyAsync(G->mu_base, mu.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
+        std::vector<int> found(Gn, 0);
+        std::vector<double> chosen(mu);
+        std::vector<double> vals(2 * (size_t)Gn);
+        for (int k = 30; k >= 0; --k) {
+            std::vector<int> need(Gn);
+            int any = 0;
+            for (int g = 0; g < Gn; ++g) any += (need[g] = !found[g]);
+            if (!any) break;
+            CK(cudaMemcpyAsync(G->search_mask, need.data(), sizeof(int) * Gn, cudaMemcpyHostToDevice, G->st));
+            CK(launch_set_mu_scale(Gn, G->sc, G->mu_base, std::ldexp(1.0, -k), G->search_mask, G->st));
+            if (egt_initial_point(G)) return EGT_E_CUDA;
+            G->grads += 3;
+            CK(cudaMemcpyAsync(vals.data(), G->sc.val, sizeof(double) * 2 * Gn, cudaMemcpyDeviceToHost, G->st));
+            CK(cudaStreamSynchronize(G->st));
+            for (int g = 0; g < Gn; ++g)
+                if (need[g] && vals[g] + vals[Gn + g] >= 0.0) {
+                    found[g] = 1;
+                    chosen[g] = mu[g] * std::ldexp(1.0, -k);
+                    chosen[Gn + g] = mu[Gn + g] * std::ldexp(1.0, -k);
+                }
+        }
+        CK(cudaMemcpyAsync(G->sc.mu, chosen.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
+    }
+    if (egt_initial_point(G)) return EGT_E_CUDA;
+    G->grads += 3;
+    G->grads_per_iter = variant == EGT_AS ? 4 : 3;
+    return end(G);
+}
+
+extern "C" int egt_step(egt_game* G, int32_t n_iters) {
+    if (!G) return fail(EGT_E_ARG, "null game");
+    if (G->solver != SOLVER_EGT) return fail(EGT_E_STATE, "egt_step before egt_init");
+    if (n_iters <= 0) return 0;
+    if (!G->graph && build_graph(G, record_egt_iteration)) return EGT_E_CUDA;
+    if (begin(G)) return EGT_E_CUDA;
+    for (int i = 0; i < n_iters; ++i) CK(cudaGraphLaunch(G->graph, G->st));
+    G->grads += (long long)G->grads_per_iter * n_iters;
+    return end(G);
+}
+
+// ----------------------------------------------------------------------------- CFR
+static int record_cfr_iteration(egt_game* G) {
+    const int Gn = G->host.n_games;
+    for (int p = 0; p < 2; ++p) {
+        const int o = 1 - p;
+        // Gen-CFR line 29 / 35: g = -A y^{t-1} (x), g = A^T x^t (y, alternating)
+        CK(grad(G, p, vec(G->Q[o], G->V[o]), vec(G->GR[p], G->V[p])));
+        TreeArgs A = base_args();
+        A.mode = TM_CFR;
+        A.g = vec(G->GR[p], G->V[p]);
+        A.gsign = p == 0 ? -1.0 : 1.0;
+        A.center = vec(G->Z[p], G->V[p]);
+        A.regret = vec(G->R[p], G->V[p]);
+        A.out_q = vec(G->Q[p], G->V[p]);
+        A.avg = vec(G->AVG[p], G->V[p]);
+        A.iter = G->sc.t;
+        A.cfr_plus = G->variant != CFR_RM;
+        A.avg_linear = G->variant == CFR_PLUS;
+        CK(tree(G, p, A));
+    }
+    CK(launch_tick(Gn, G->sc.t, G->st));
+    return 0;
+}
+
+extern "C" int cfr_init(egt_game* G, int32_t variant) {
+    if (!G || variant < CFR_RM || variant > CFR_PLUS) return fail(EGT_E_ARG, "bad argument");
+    const int Gn = G->host.n_games;
+    for (int p = 0; p < 2; ++p) {
+        const size_t n = (size_t)Gn * G->V[p];
+        if (!G->R[p] && dalloc(G, &G->R[p], n)) return EGT_E_CUDA;
+        if (!G->Z[p] && dalloc(G, &G->Z[p], n)) return EGT_E_CUDA;
+        if (!G->Q[p] && dalloc(G, &G->Q[p], n)) return EGT_E_CUDA;
+        if (!G->AVG[p] && dalloc(G, &G->AVG[p], n)) return EGT_E_CUDA;
+    }
+    if (begin(G)) return EGT_E_CUDA;
+    if (zero_scalars(G)) return EGT_E_CUDA;
+    if (G->graph) {
+        cudaGraphExecDestroy(G->graph);
+        G->graph = nullptr;
+    }
+    G->solver = SOLVER_CFR;
+    G->variant = variant;
+    G->grads = 0;
+    G->grads_per_iter = 2;
+    std::vector<int> one(Gn, 1);
+    CK(cudaMemcpyAsync(G->sc.t, one.data(), sizeof(int) * Gn, cudaMemcpyHostToDevice, G->st));
+    for (int p = 0; p < 2; ++p) {
+        const size_t n = (size_t)Gn * G->V[p];
+        CK(cudaMemsetAsync(G->R[p], 0, n * sizeof(double), G->st));
+        CK(cudaMemsetAsync(G->AVG[p], 0, n * sizeof(double), G->st));
+        TreeArgs U = base_args();
+        U.mode = TM_UNIFORM;  // x^0 uniform at every simplex (Gen-CFR line 1)
+        U.out_b = vec(G->Z[p], G->V[p]);
+        U.out_q = vec(G->Q[p], G->V[p]);
+        CK(tree(G, p, U));
+    }
+    CK(cudaStreamSynchronize(G->st));
+    return end(G);
+}
+
+extern "C" int cfr_step(egt_game* G, int32_t n_iters) {
+    if (!G) return fail(EGT_E_ARG, "null game");
+    if (G->solver != SOLVER_CFR) return fail(EGT_E_STATE, "cfr_step before cfr_init");
+    if (n_iters <= 0) return 0;
+    if (!G->graph && build_graph(G, record_cfr_iteration)) return EGT_E_CUDA;
+    if (begin(G)) return EGT_E_CUDA;
+    for (int i = 0; i < n_iters; ++i) CK(cudaGraphLaunch(G->graph, G->st));
+    G->grads += 2LL * n_iters;
+    return end(G);
+}
+
+// ----------------------------------------------------------------------------- gap / strategies
+static int strategy_refs(egt_game* G, int which, VecRef out[2]) {
+    if (G->solver == SOLVER_EGT) {
+        out[0] = slot2(G, G->S[0], 0, 0);
+        out[1] = slot2(G, G->S[1], 1, 0);
+    } else if (G->solver == SOLVER_CFR) {
+        for (int p = 0; p < 2; ++p) {
+            double* b = which == 1 ? G->AVG[p] : which == 2 ? G->R[p] : which == 3 ? G->Z[p] : G->Q[p];
+            out[p] = vec(b, G->V[p]);
+        }
+    } else {
+        return fail(EGT_E_STATE, "no solver initialised");
+    }
+    return 0;
+}
+
+extern "C" int saddle_gap(egt_game* G, int32_t which, double* host_out) {
+    if (!G || !host_out) return fail(EGT_E_ARG, "bad argument");
+    VecRef s[2];
+    if (strategy_refs(G, which, s)) return EGT_E_STATE;
+    const int Gn = G->host.n_games;
+    if (begin(G)) return EGT_E_CUDA;
+    // eps_sad = max_y <x, A y> - min_x <x, A y>
+    for (int p = 0; p < 2; ++p) {
+        CK(grad(G, p, s[1 - p], vec(G->GR[p], G->V[p])));
+        TreeArgs A = base_args();
+        A.mode = TM_BR;
+        A.g = vec(G->GR[p], G->V[p]);
+        A.gsign = GSIGN[p];
+        A.value = G->gapval + (size_t)p * Gn;
+        A.partial = G->partial;
+        A.counter = G->counter;
+        CK(tree(G, p, A));
+    }
+    std::vector<double> v(2 * (size_t)Gn);
+    CK(cudaMemcpyAsync(v.data(), G->gapval, sizeof(double) * 2 * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaStreamSynchronize(G->st));
+    for (int g = 0; g < Gn; ++g) host_out[g] = -v[Gn + g] - v[g];
+    G->grads += 2;
+    return end(G);
+}
+
+extern "C" int get_strategy_device(egt_game* G, int32_t player, int32_t which, double* dev_out) {
+    if (!G || !dev_out || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+    VecRef s[2];
+    if (strategy_refs(G, which, s)) return EGT_E_STATE;
+    const int Gn = G->host.n_games;
+    std::vector<int> cur(Gn, 0);
+    if (begin(G)) return EGT_E_CUDA;
+    if (s[player].slot_sel) {
+        CK(cudaMemcpyAsync(cur.data(), G->sc.cur, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
+        CK(cudaStreamSynchronize(G->st));
+    }
+    for (int g = 0; g < Gn; ++g) {
+        const double* src = s[player].base + (size_t)g * G->V[player] +
+                            (s[player].slot_sel ? (size_t)(cur[g] & 1) * s[player].slot_stride : 0);
+        CK(cudaMemcpyAsync(dev_out + (size_t)g * G->V[player], src, sizeof(double) * G->V[player],
+                           cudaMemcpyDeviceToDevice, G->st));
+    }
+    return end(G);
+}
+
+extern "C" int get_avg_strategy(egt_game* G, int32_t player, double* host_out) {
+    if (!G || !host_out || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+    const HostGame& H = G->host;
+    const int Gn = H.n_games, Hp = H.H_pad, np = H.pl[player].n_pub;
+    double* tmp = nullptr;
+    CK(cudaMalloc(&tmp, sizeof(double) * (size_t)Gn * G->V[player]));
+    int r = get_strategy_device(G, player, 1, tmp);
+    std::vector<double> h((size_t)Gn * G->V[player]);
+    if (!r) {
+        cudaError_t e = cudaMemcpyAsync(h.data(), tmp, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, G->user);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(G->user);
+        if (e != cudaSuccess) r = fail(EGT_E_CUDA, cudaGetErrorString(e));
+    }
+    cudaFree(tmp);
+    if (r) return r;
+    const int nc = H.n_combos;
+    for (int g = 0; g < Gn; ++g)
+        for (int s = 0; s < np; ++s) {
+            double* o = host_out + ((size_t)g * np + s) * nc;
+            for (int c = 0; c < nc; ++c) o[c] = 0.0;
+            for (int hh = 0; hh < H.H; ++hh)
+                o[H.hand_combo[(size_t)g * H.H + hh]] = h[(size_t)g * G->V[player] + (size_t)s * Hp + hh];
+        }
+    return 0;
+}
+
+extern "C" int egt_scalars(egt_game* G, double* host_out) {
+    if (!G || !host_out) return fail(EGT_E_ARG, "bad argument");
+    const int Gn = G->host.n_games;
+    std::vector<double> mu(2 * Gn), tau(Gn), egv(Gn);
+    std::vector<int> t(Gn), att(Gn), bt(Gn);
+    if (begin(G)) return EGT_E_CUDA;
+    CK(cudaMemcpyAsync(mu.data(), G->sc.mu, sizeof(double) * 2 * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaMemcpyAsync(tau.data(), G->sc.tau, sizeof(double) * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaMemcpyAsync(egv.data(), G->sc.egv, sizeof(double) * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaMemcpyAsync(t.data(), G->sc.t, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaMemcpyAsync(att.data(), G->sc.attempts, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaMemcpyAsync(bt.data(), G->sc.backtracks, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaStreamSynchronize(G->st));
+    for (int g = 0; g < Gn; ++g) {
+        double* o = host_out + (size_t)g * 8;
+        o[0] = mu[g];
+        o[1] = mu[Gn + g];
+        o[2] = tau[g];
+        o[3] = t[g];
+        o[4] = att[g];
+        o[5] = bt[g];
+        o[6] = egv[g];
+        o[7] = (double)G->grads;
+    }
+    return end(G);
+}

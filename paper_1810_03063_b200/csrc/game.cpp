@@ -1,0 +1,592 @@
+// Host-side game construction: public trees (Kuhn, Leduc, river endgame), the
+// per-player treeplex layout, hand strength order and card-removal tables.
+// Independent of the oracle (separate implementation of the same game rules).
+#include "game.h"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <numeric>
+#include <set>
+
+namespace egt {
+
+static std::string join(const std::string& h, const std::string& t) { return h.empty() ? t : h + "/" + t; }
+
+// ------------------------------------------------------------------ hand strength
+// Standard poker ranking; ranks 0..12 (12 = ace), suits any ints.
+static int64_t eval5(const int* r, const int* s) {
+    int cnt[13] = {0};
+    for (int i = 0; i < 5; ++i) cnt[r[i]]++;
+    bool flush = true;
+    for (int i = 1; i < 5; ++i) flush = flush && (s[i] == s[0]);
+    int top = -1;
+    for (int hi = 12; hi >= 4 && top < 0; --hi) {
+        bool ok = true;
+        for (int k = 0; k < 5; ++k) ok = ok && cnt[hi - k] > 0;
+        if (ok) top = hi;
+    }
+    if (top < 0 && cnt[12] && cnt[0] && cnt[1] && cnt[2] && cnt[3]) top = 3;  // wheel
+    // groups ordered by (count desc, rank desc)
+    int grp[5], ng = 0;
+    for (int c = 4; c >= 1; --c)
+        for (int rk = 12; rk >= 0; --rk)
+            if (cnt[rk] == c) grp[ng++] = rk;
+    int c0 = cnt[grp[0]], c1 = ng > 1 ? cnt[grp[1]] : 0;
+    int cat;
+    if (top >= 0 && flush) cat = 8;
+    else if (c0 == 4) cat = 7;
+    else if (c0 == 3 && c1 == 2) cat = 6;
+    else if (flush) cat = 5;
+    else if (top >= 0) cat = 4;
+    else if (c0 == 3) cat = 3;
+    else if (c0 == 2 && c1 == 2) cat = 2;
+    else if (c0 == 2) cat = 1;
+    else cat = 0;
+    int64_t key = cat;
+    if (cat == 8 || cat == 4) {
+        key = key * 13 + top;
+        for (int i = 1; i < 5; ++i) key *= 13;
+    } else {
+        for (int i = 0; i < 5; ++i) key = key * 13 + (i < ng ? grp[i] : 0);
+    }
+    return key;
+}
+
+int64_t hand_strength(const int* ranks, const int* suits, int n) {
+    int64_t best = -1;
+    int idx[5];
+    // all 5-subsets of n <= 7 cards
+    for (idx[0] = 0; idx[0] < n; ++idx[0])
+        for (idx[1] = idx[0] + 1; idx[1] < n; ++idx[1])
+            for (idx[2] = idx[1] + 1; idx[2] < n; ++idx[2])
+                for (idx[3] = idx[2] + 1; idx[3] < n; ++idx[3])
+                    for (idx[4] = idx[3] + 1; idx[4] < n; ++idx[4]) {
+                        int r[5], s[5];
+                        for (int k = 0; k < 5; ++k) { r[k] = ranks[idx[k]]; s[k] = suits[idx[k]]; }
+                        best = std::max(best, eval5(r, s));
+                    }
+    return best;
+}
+
+// ------------------------------------------------------------------ public trees
+static int add_node(PublicTree& T, PNode n) {
+    T.nodes.push_back(std::move(n));
+    return (int)T.nodes.size() - 1;
+}
+
+static int terminal(PublicTree& T, int kind, double amount, double kappa, int bs, const std::string& hist) {
+    PNode n;
+    n.kind = ND_TERMINAL;
+    n.term_kind = kind;
+    n.amount = amount;
+    n.kappa = kappa;
+    n.board_state = bs;
+    n.hist = hist;
+    return add_node(T, n);
+}
+
+static int decision(PublicTree& T, int player, int bs, const std::string& hist) {
+    PNode n;
+    n.kind = ND_DECISION;
+    n.player = player;
+    n.board_state = bs;
+    n.hist = hist;
+    return add_node(T, n);
+}
+
+static void link(PublicTree& T, int parent, const std::string& tok, int child) {
+    T.nodes[parent].tok.push_back(tok);
+    T.nodes[parent].child.push_back(child);
+}
+
+// Kuhn: cards J<Q<K, ante 1, bet 1; every deal (c1,c2) has probability 1/6.
+static void build_kuhn(PublicTree& T) {
+    const double k = 1.0 / 6.0;
+    T.n_board_states = 1;
+    T.board_cards = {{}};
+    int root = decision(T, 0, 0, "");
+    int p2k = decision(T, 1, 0, "k");
+    link(T, root, "k", p2k);
+    link(T, p2k, "k", terminal(T, T_SHOWDOWN, 1, k, 0, "k/k"));
+    int p1kb = decision(T, 0, 0, "k/b1");
+    link(T, p2k, "b1", p1kb);
+    link(T, p1kb, "f", terminal(T, T_FOLD_P1, +1, k, 0, "k/b1/f"));
+    link(T, p1kb, "c", terminal(T, T_SHOWDOWN, 2, k, 0, "k/b1/c"));
+    int p2b = decision(T, 1, 0, "b1");
+    link(T, root, "b1", p2b);
+    link(T, p2b, "f", terminal(T, T_FOLD_P2, -1, k, 0, "b1/f"));
+    link(T, p2b, "c", terminal(T, T_SHOWDOWN, 2, k, 0, "b1/c"));
+}
+
+// Leduc: 6 cards (id = rank*2 + suit), ante 1, bets 2 then 4, at most 2 bets per round,
+// board card dealt between the rounds (board state 1 + card).  Deal probability of an
+// ordered (c1, c2) is 1/30; with the board card 1/120.
+static void build_leduc(PublicTree& T) {
+    const int bets[2] = {2, 4};
+    T.n_board_states = 7;
+    T.board_cards.assign(7, {});
+    for (int b = 0; b < 6; ++b) T.board_cards[1 + b] = {b};
+    std::function<int(int, int, int, int, int, int, int, int, const std::string&)> rec;
+    std::function<int(int, int, int, int, const std::string&)> end_round;
+    end_round = [&](int rnd, int c0, int c1, int bs, const std::string& hist) -> int {
+        if (rnd == 0) {
+            PNode ch;
+            ch.kind = ND_CHANCE;
+            ch.hist = hist;
+            int cn = add_node(T, ch);
+            for (int b = 0; b < 6; ++b) {
+                std::string h = join(hist, "d" + std::to_string(b));
+                int child = rec(1, c0, c1, 0, 0, 0, 0, 1 + b, h);
+                link(T, cn, "d" + std::to_string(b), child);
+            }
+            return cn;
+        }
+        return terminal(T, T_SHOWDOWN, (double)c1, 1.0 / 120.0, bs, hist);
+    };
+    rec = [&](int rnd, int c0, int c1, int rc0, int rc1, int p, int nb, int bs, const std::string& hist) -> int {
+        int n = decision(T, p, bs, hist);
+        int me = p == 0 ? c0 : c1, opp = p == 0 ? c1 : c0;
+        int toc = opp - me;
+        double kap = rnd == 0 ? 1.0 / 30.0 : 1.0 / 120.0;
+        if (toc > 0) {
+            int t = p == 0 ? terminal(T, T_FOLD_P1, +(double)c0, kap, bs, join(hist, "f"))
+                           : terminal(T, T_FOLD_P2, -(double)c1, kap, bs, join(hist, "f"));
+            link(T, n, "f", t);
+            int child = end_round(rnd, opp, opp, bs, join(hist, "c"));
+            link(T, n, "c", child);
+        } else {
+            int child = p == 0 ? rec(rnd, c0, c1, rc0, rc1, 1, nb, bs, join(hist, "k"))
+                               : end_round(rnd, c0, c1, bs, join(hist, "k"));
+            link(T, n, "k", child);
+        }
+        if (nb < 2) {
+            int add = toc + bets[rnd];
+            int nc0 = c0, nc1 = c1, nrc0 = rc0, nrc1 = rc1;
+            std::string tok;
+            if (p == 0) { nc0 += add; nrc0 += add; tok = "b" + std::to_string(nrc0); }
+            else { nc1 += add; nrc1 += add; tok = "b" + std::to_string(nrc1); }
+            int child = rec(rnd, nc0, nc1, nrc0, nrc1, 1 - p, nb + 1, bs, join(hist, tok));
+            link(T, n, tok, child);
+        }
+        return n;
+    };
+    rec(0, 1, 1, 0, 0, 0, 0, 0, "");
+}
+
+// River endgame, PAPER.md:670-688 with DESIGN.md readings R10-R13.
+struct RiverRules {
+    int pot, stack, cap;
+    bool open_fold;
+    std::vector<std::pair<int64_t, int64_t>> fr[EGT_N_CTX];
+    bool allin[EGT_N_CTX];
+};
+
+static int river_ctx(int p, int nb) {
+    if (p == 0) return nb < 3 ? nb : 3;
+    return 4 + (nb < 2 ? nb : 2);
+}
+
+static int build_river_rec(PublicTree& T, const RiverRules& R, int p, int64_t c0, int64_t c1, int nb,
+                           const std::string& hist) {
+    const double half = R.pot / 2.0;
+    int n = decision(T, p, 0, hist);
+    int64_t me = p == 0 ? c0 : c1, opp = p == 0 ? c1 : c0;
+    int64_t toc = opp - me;
+    int64_t pot = R.pot + c0 + c1;
+    if (toc > 0 || R.open_fold) {
+        int t = p == 0 ? terminal(T, T_FOLD_P1, +(half + (double)c0), 1.0, 0, join(hist, "f"))
+                       : terminal(T, T_FOLD_P2, -(half + (double)c1), 1.0, 0, join(hist, "f"));
+        link(T, n, "f", t);
+    }
+    if (toc > 0) {
+        link(T, n, "c", terminal(T, T_SHOWDOWN, half + (double)opp, 1.0, 0, join(hist, "c")));
+    } else if (p == 0) {
+        link(T, n, "k", build_river_rec(T, R, 1, c0, c1, nb, join(hist, "k")));
+    } else {
+        link(T, n, "k", terminal(T, T_SHOWDOWN, half + (double)c0, 1.0, 0, join(hist, "k")));
+    }
+    if ((R.cap <= 0 || nb < R.cap) && opp < R.stack) {
+        int ctx = river_ctx(p, nb);
+        std::set<int64_t> totals;
+        for (auto& f : R.fr[ctx]) {
+            int64_t X = pot + toc;
+            int64_t inc = (2 * f.first * X + f.second) / (2 * f.second);  // round half up, exact
+            int64_t tot = me + toc + inc;
+            if (inc >= 1 && tot < R.stack) totals.insert(tot);
+        }
+        if (R.allin[ctx]) totals.insert(R.stack);
+        for (int64_t tot : totals) {
+            std::string tok = "b" + std::to_string(tot);
+            int child = p == 0 ? build_river_rec(T, R, 1, tot, c1, nb + 1, join(hist, tok))
+                               : build_river_rec(T, R, 0, c0, tot, nb + 1, join(hist, tok));
+            link(T, n, tok, child);
+        }
+    }
+    return n;
+}
+
+// ------------------------------------------------------------------ layout
+static void build_layout(HostGame& G) {
+    PublicTree& T = G.tree;
+    for (int p = 0; p < 2; ++p) {
+        G.pl[p] = PlayerLayout();
+        G.pl[p].seq_hist = {""};
+        G.pl[p].seq_owner = {-1};
+    }
+    G.terms.clear();
+    std::function<void(int, int, int, int, int)> visit = [&](int n, int s0, int s1, int l0, int l1) {
+        const PNode& N = T.nodes[n];
+        if (N.kind == ND_TERMINAL) {
+            Terminal t;
+            t.kind = N.term_kind;
+            t.amount = N.amount;
+            t.kappa = N.kappa;
+            t.board_state = N.board_state;
+            t.last_seq[0] = s0;
+            t.last_seq[1] = s1;
+            G.terms.push_back(t);
+            return;
+        }
+        if (N.kind == ND_CHANCE) {
+            for (int c : N.child) visit(c, s0, s1, l0, l1);
+            return;
+        }
+        int p = N.player;
+        PlayerLayout& L = G.pl[p];
+        int m = (int)L.node_pub.size();
+        int first = L.n_pub;
+        L.node_pub.push_back(n);
+        L.first.push_back(first);
+        L.nact.push_back((int)N.child.size());
+        L.parent_seq.push_back(p == 0 ? s0 : s1);
+        L.board_state.push_back(N.board_state);
+        L.level.push_back(p == 0 ? l0 : l1);
+        for (size_t a = 0; a < N.child.size(); ++a) {
+            L.seq_hist.push_back(join(N.hist, N.tok[a]));
+            L.seq_owner.push_back(m);
+        }
+        L.n_pub += (int)N.child.size();
+        for (size_t a = 0; a < N.child.size(); ++a) {
+            int s = first + (int)a;
+            if (p == 0) visit(N.child[a], s, s1, l0 + 1, l1);
+            else visit(N.child[a], s0, s, l0, l1 + 1);
+        }
+    };
+    visit(0, 0, 0, 0, 0);
+    for (int p = 0; p < 2; ++p) {
+        PlayerLayout& L = G.pl[p];
+        L.depth = 0;
+        for (int l : L.level) L.depth = std::max(L.depth, l + 1);
+        std::vector<std::vector<int>> by(L.n_pub);
+        for (size_t t = 0; t < G.terms.size(); ++t) by[G.terms[t].last_seq[p]].push_back((int)t);
+        L.term_off.assign(L.n_pub + 1, 0);
+        L.term_idx.clear();
+        for (int s = 0; s < L.n_pub; ++s) {
+            L.term_off[s] = (int)L.term_idx.size();
+            for (int t : by[s]) L.term_idx.push_back(t);
+        }
+        L.term_off[L.n_pub] = (int)L.term_idx.size();
+    }
+}
+
+static int combo_index(int c1, int c2, int n) {
+    // canonical order of (c1 < c2) pairs, lexicographic
+    return c1 * (2 * n - c1 - 1) / 2 + (c2 - c1 - 1);
+}
+
+// strength key of internal hand h for board state bs of game g (only for valid hands)
+static int64_t strength_of(const HostGame& G, int g, int bs, int h, const std::vector<int>& board) {
+    const int* hc = &G.hand_cards[((size_t)g * G.H + h) * 2];
+    if (G.kind == EGT_GAME_KUHN) return hc[0];
+    if (G.kind == EGT_GAME_LEDUC) {
+        if (board.empty()) return hc[0] / 2;
+        int r = hc[0] / 2, b = board[0] / 2;
+        return r == b ? 10 + r : r;
+    }
+    int ranks[7], suits[7], n = 0;
+    for (int k = 0; k < 2; ++k) { ranks[n] = 13 - G.n_ranks + hc[k] / G.n_suits; suits[n++] = hc[k] % G.n_suits; }
+    for (int c : board) { ranks[n] = 13 - G.n_ranks + c / G.n_suits; suits[n++] = c % G.n_suits; }
+    return hand_strength(ranks, suits, n);
+}
+
+static std::vector<int> board_of(const HostGame& G, const std::vector<std::vector<int>>& game_boards, int g, int bs) {
+    if (G.kind == EGT_GAME_RIVER) return game_boards[g];
+    return G.tree.board_cards[bs];
+}
+
+static void build_table(const HostGame& G, int g, int bs, const std::vector<int>& board, BoardTable& tb) {
+    const int H = G.H, Hp = G.H_pad, hs = G.hand_size;
+    tb.valid.assign(Hp, 0);
+    std::vector<std::pair<int64_t, int>> v;
+    for (int h = 0; h < H; ++h) {
+        const int* hc = &G.hand_cards[((size_t)g * H + h) * 2];
+        bool ok = true;
+        for (int k = 0; k < hs; ++k)
+            for (int c : board) ok = ok && hc[k] != c;
+        if (!ok) continue;
+        tb.valid[h] = 1;
+        v.push_back({strength_of(G, g, bs, h, board), h});
+    }
+    std::sort(v.begin(), v.end());  // (strength, hand) ascending: ties by hand index
+    int nv = (int)v.size();
+    tb.nvalid = nv;
+    tb.order.assign(Hp, 0);
+    tb.lo.assign(Hp, 0);
+    tb.hi.assign(Hp, 0);
+    for (int i = 0; i < nv; ++i) tb.order[i] = (int16_t)v[i].second;
+    for (int i = 0; i < nv;) {
+        int j = i;
+        while (j < nv && v[j].first == v[i].first) ++j;
+        for (int k = i; k < j; ++k) { tb.lo[k] = (int16_t)i; tb.hi[k] = (int16_t)j; }
+        i = j;
+    }
+    // expanded card array: for each card, the sorted positions of the valid hands holding it
+    std::vector<std::vector<int>> by_card(G.n_cards);
+    for (int i = 0; i < nv; ++i) {
+        const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
+        for (int k = 0; k < hs; ++k) by_card[hc[k]].push_back(i);
+    }
+    std::vector<int> seg_start(G.n_cards + 1, 0);
+    tb.src.assign(2 * (size_t)Hp + 2, 0);
+    int ne = 0;
+    for (int c = 0; c < G.n_cards; ++c) {
+        seg_start[c] = ne;
+        for (int i : by_card[c]) tb.src[ne++] = (int16_t)i;
+    }
+    seg_start[G.n_cards] = ne;
+    tb.pos4.assign((size_t)Hp * 8, 0);
+    for (int i = 0; i < nv; ++i) {
+        const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
+        for (int k = 0; k < hs; ++k) {
+            int c = hc[k];
+            const std::vector<int>& L = by_card[c];
+            int nlo = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.lo[i]) - L.begin());
+            int nhi = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.hi[i]) - L.begin());
+            int16_t* P = &tb.pos4[(size_t)i * 8 + k * 4];
+            P[0] = (int16_t)(seg_start[c] + nlo);   // elo
+            P[1] = (int16_t)(seg_start[c] + nhi);   // ehi
+            P[2] = (int16_t)seg_start[c];           // est
+            P[3] = (int16_t)seg_start[c + 1];       // een
+        }
+    }
+}
+
+std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
+    G = HostGame();
+    if (spec.n_games < 1) return "n_games must be >= 1";
+    G.kind = spec.kind;
+    G.n_games = spec.n_games;
+    std::vector<std::vector<int>> game_boards;
+    if (spec.kind == EGT_GAME_KUHN) {
+        build_kuhn(G.tree);
+        G.H = 3; G.hand_size = 1; G.n_cards = 3; G.n_combos = 3;
+    } else if (spec.kind == EGT_GAME_LEDUC) {
+        build_leduc(G.tree);
+        G.H = 6; G.hand_size = 1; G.n_cards = 6; G.n_combos = 6;
+    } else if (spec.kind == EGT_GAME_RIVER) {
+        if (spec.n_ranks < 2 || spec.n_ranks > 13 || spec.n_suits < 1 || spec.n_suits > 4)
+            return "invalid deck";
+        G.n_ranks = spec.n_ranks; G.n_suits = spec.n_suits;
+        G.n_cards = spec.n_ranks * spec.n_suits;
+        if (G.n_cards < 9) return "deck too small for a 5-card board and two hands";
+        if (!spec.boards) return "river games need boards";
+        if (spec.pot < 2 || spec.stack < 1) return "invalid pot/stack";
+        RiverRules R;
+        R.pot = spec.pot; R.stack = spec.stack; R.cap = spec.raise_cap; R.open_fold = spec.open_fold != 0;
+        for (int c = 0; c < EGT_N_CTX; ++c) {
+            if (spec.n_fracs[c] < 0 || spec.n_fracs[c] > EGT_MAX_FRACS) return "invalid n_fracs";
+            for (int i = 0; i < spec.n_fracs[c]; ++i) {
+                if (spec.frac_num[c][i] <= 0 || spec.frac_den[c][i] <= 0) return "fractions must be positive";
+                R.fr[c].push_back({spec.frac_num[c][i], spec.frac_den[c][i]});
+            }
+            R.allin[c] = spec.allin[c] != 0;
+        }
+        G.tree.n_board_states = 1;
+        G.tree.board_cards = {{}};
+        build_river_rec(G.tree, R, 0, 0, 0, 0, "");
+        game_boards.resize(spec.n_games);
+        for (int g = 0; g < spec.n_games; ++g) {
+            std::set<int> seen;
+            for (int k = 0; k < 5; ++k) {
+                int c = spec.boards[g * 5 + k];
+                if (c < 0 || c >= G.n_cards || seen.count(c)) return "invalid board";
+                seen.insert(c);
+                game_boards[g].push_back(c);
+            }
+        }
+        G.hand_size = 2;
+        G.n_combos = G.n_cards * (G.n_cards - 1) / 2;
+        G.H = G.n_combos - (5 * (G.n_cards - 5) + 10);  // combos avoiding 5 board cards
+    } else {
+        return "unknown game kind";
+    }
+    G.H_pad = (G.H + 31) / 32 * 32;
+    build_layout(G);
+    const int Gn = G.n_games, H = G.H, Hp = G.H_pad;
+
+    // hands (internal order) and priors
+    G.hand_cards.assign((size_t)Gn * H * 2, -1);
+    G.hand_combo.assign((size_t)Gn * H, 0);
+    for (int p = 0; p < 2; ++p) G.prior[p].assign((size_t)Gn * Hp, 0.0);
+    G.kappa_game.assign(Gn, 1.0);
+    for (int g = 0; g < Gn; ++g) {
+        if (G.kind != EGT_GAME_RIVER) {
+            for (int h = 0; h < H; ++h) {
+                G.hand_cards[((size_t)g * H + h) * 2] = h;
+                G.hand_combo[(size_t)g * H + h] = h;
+                G.prior[0][(size_t)g * Hp + h] = 1.0;
+                G.prior[1][(size_t)g * Hp + h] = 1.0;
+            }
+            continue;
+        }
+        const std::vector<int>& bd = game_boards[g];
+        std::vector<std::pair<int64_t, int>> hv;  // (strength, combo)
+        std::vector<std::pair<int, int>> cards;
+        for (int c1 = 0; c1 < G.n_cards; ++c1)
+            for (int c2 = c1 + 1; c2 < G.n_cards; ++c2) {
+                if (std::find(bd.begin(), bd.end(), c1) != bd.end() ||
+                    std::find(bd.begin(), bd.end(), c2) != bd.end()) continue;
+                int ranks[7], suits[7], n = 0;
+                ranks[n] = 13 - G.n_ranks + c1 / G.n_suits; suits[n++] = c1 % G.n_suits;
+                ranks[n] = 13 - G.n_ranks + c2 / G.n_suits; suits[n++] = c2 % G.n_suits;
+                for (int c : bd) { ranks[n] = 13 - G.n_ranks + c / G.n_suits; suits[n++] = c % G.n_suits; }
+                hv.push_back({hand_strength(ranks, suits, n), combo_index(c1, c2, G.n_cards)});
+            }
+        if ((int)hv.size() != H) return "internal: hand count";
+        std::sort(hv.begin(), hv.end());
+        std::vector<std::pair<int, int>> combo_cards(G.n_combos);
+        for (int c1 = 0, k = 0; c1 < G.n_cards; ++c1)
+            for (int c2 = c1 + 1; c2 < G.n_cards; ++c2, ++k) combo_cards[k] = {c1, c2};
+        for (int h = 0; h < H; ++h) {
+            int ci = hv[h].second;
+            G.hand_combo[(size_t)g * H + h] = ci;
+            G.hand_cards[((size_t)g * H + h) * 2] = combo_cards[ci].first;
+            G.hand_cards[((size_t)g * H + h) * 2 + 1] = combo_cards[ci].second;
+            for (int p = 0; p < 2; ++p) {
+                const double* pr = p == 0 ? spec.prior1 : spec.prior2;
+                double w = pr ? pr[(size_t)g * G.n_combos + ci] : 1.0;
+                if (!(w >= 0) || !std::isfinite(w)) return "priors must be finite and >= 0";
+                G.prior[p][(size_t)g * Hp + h] = w;
+            }
+        }
+        // Z = sum over disjoint (h1, h2) of prior1 prior2 (inclusion-exclusion over shared cards)
+        std::vector<double> card_sum(G.n_cards, 0.0);
+        double T2 = 0;
+        for (int h = 0; h < H; ++h) {
+            double w = G.prior[1][(size_t)g * Hp + h];
+            T2 += w;
+            card_sum[G.hand_cards[((size_t)g * H + h) * 2]] += w;
+            card_sum[G.hand_cards[((size_t)g * H + h) * 2 + 1]] += w;
+        }
+        double Z = 0;
+        for (int h = 0; h < H; ++h) {
+            const int* hc = &G.hand_cards[((size_t)g * H + h) * 2];
+            double compat = T2 - card_sum[hc[0]] - card_sum[hc[1]] + G.prior[1][(size_t)g * Hp + h];
+            Z += G.prior[0][(size_t)g * Hp + h] * compat;
+        }
+        if (!(Z > 0)) return "priors leave no compatible hand pair";
+        G.kappa_game[g] = 1.0 / Z;
+    }
+
+    // tables per (game, board state)
+    const int nbs = G.tree.n_board_states;
+    G.tables.resize((size_t)Gn * nbs);
+    for (int g = 0; g < Gn; ++g)
+        for (int bs = 0; bs < nbs; ++bs)
+            build_table(G, g, bs, board_of(G, game_boards, g, bs), G.tables[(size_t)g * nbs + bs]);
+
+    // beta and M per (node, hand), validity of game 0
+    // (identical across games: river hands all avoid their board; Kuhn/Leduc games are equal)
+    for (int p = 0; p < 2; ++p) {
+        const PlayerLayout& L = G.pl[p];
+        int nn = (int)L.first.size();
+        std::vector<std::vector<int>> kids(L.n_pub);
+        for (int m = 0; m < nn; ++m) kids[L.parent_seq[m]].push_back(m);
+        G.beta[p].assign((size_t)nn * Hp, 0.0);
+        std::vector<double> f((size_t)nn * Hp, 0.0);
+        G.M[p].assign(Gn, 0.0);
+        for (int m = nn - 1; m >= 0; --m) {
+            const BoardTable& tb = G.tables[L.board_state[m]];
+            for (int h = 0; h < H; ++h) {
+                if (!tb.valid[h]) continue;
+                double b = 2.0, fbest = 0.0;
+                for (int a = 0; a < L.nact[m]; ++a) {
+                    double fs = 0.0;
+                    for (int c : kids[L.first[m] + a]) {
+                        if (!G.tables[L.board_state[c]].valid[h]) continue;
+                        b += 2.0 * G.beta[p][(size_t)c * Hp + h];
+                        fs += f[(size_t)c * Hp + h];
+                    }
+                    fbest = std::max(fbest, fs);
+                }
+                G.beta[p][(size_t)m * Hp + h] = b;
+                f[(size_t)m * Hp + h] = 1.0 + fbest;
+            }
+        }
+        double M = 0;
+        for (int m : kids[0])
+            for (int h = 0; h < H; ++h) M += f[(size_t)m * Hp + h];
+        for (int g = 0; g < Gn; ++g) G.M[p][g] = M;
+    }
+
+    return "";
+}
+
+
+// ||A|| = max |A_ij| of game g (R7); only the theory mu needs it.
+// Per board state: the largest prior product over compatible pairs (fold blocks) and
+// over compatible non-tied pairs (showdown blocks); terminals whose player-1 (-2)
+// sequence is empty aggregate their block's columns (rows) into row (column) 0.
+double compute_max_abs_A(const HostGame& G, int g) {
+    const int H = G.H, Hp = G.H_pad, nbs = G.tree.n_board_states;
+    const double* p1 = &G.prior[0][(size_t)g * Hp];
+    const double* p2 = &G.prior[1][(size_t)g * Hp];
+    auto compat = [&](int a, int b) {
+        const int* ca = &G.hand_cards[((size_t)g * H + a) * 2];
+        const int* cb = &G.hand_cards[((size_t)g * H + b) * 2];
+        for (int i = 0; i < G.hand_size; ++i)
+            for (int j = 0; j < G.hand_size; ++j)
+                if (ca[i] == cb[j]) return false;
+        return true;
+    };
+    std::vector<double> pmax_fold(nbs, -1.0), pmax_sd(nbs, -1.0);
+    std::vector<std::vector<int>> group(nbs, std::vector<int>(H, -1));
+    for (int bs = 0; bs < nbs; ++bs) {
+        const BoardTable& tb = G.tables[(size_t)g * nbs + bs];
+        for (int i = 0; i < tb.nvalid; ++i) group[bs][tb.order[i]] = tb.lo[i];
+    }
+    double best = 0.0;
+    for (const Terminal& t : G.terms) {
+        const int bs = t.board_state;
+        const BoardTable& tb = G.tables[(size_t)g * nbs + bs];
+        const std::vector<int>& grp = group[bs];
+        const bool sd = t.kind == T_SHOWDOWN;
+        auto sign = [&](int a, int b) { return sd ? (grp[b] > grp[a] ? 1.0 : (grp[b] < grp[a] ? -1.0 : 0.0)) : 1.0; };
+        const double scale = t.kappa * G.kappa_game[g] * std::fabs(t.amount);
+        const bool e0 = t.last_seq[0] == 0, e1 = t.last_seq[1] == 0;
+        double m = 0.0;
+        if (!e0 && !e1) {
+            double& cache = sd ? pmax_sd[bs] : pmax_fold[bs];
+            if (cache < 0) {
+                cache = 0.0;
+                for (int a = 0; a < H; ++a)
+                    for (int b = 0; b < H; ++b)
+                        if (tb.valid[a] && tb.valid[b] && compat(a, b) && sign(a, b) != 0.0)
+                            cache = std::max(cache, p1[a] * p2[b]);
+            }
+            m = cache;
+        } else {
+            std::vector<double> agg(e0 && e1 ? 1 : H, 0.0);
+            for (int a = 0; a < H; ++a)
+                for (int b = 0; b < H; ++b)
+                    if (tb.valid[a] && tb.valid[b] && compat(a, b))
+                        agg[e0 && e1 ? 0 : (e1 ? a : b)] += p1[a] * p2[b] * sign(a, b);
+            for (double v : agg) m = std::max(m, std::fabs(v));
+        }
+        best = std::max(best, scale * m);
+    }
+    return best;
+}
+
+}  // namespace egt

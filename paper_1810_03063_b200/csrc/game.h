@@ -1,0 +1,92 @@
+// Host-side game model and GPU layout (no CUDA here).
+//
+// A game of the batch is a public tree (shared by all games) times private hands
+// (per game).  The treeplex of player p is the Cartesian product
+// over hands of the player's public decision tree: simplex
+// (node m, hand h) has index set {(first[m] + a, h)} and parent (parent_seq[m], h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/egt_b200.h"
+
+namespace egt {
+
+enum NodeKind { ND_DECISION = 0, ND_CHANCE = 1, ND_TERMINAL = 2 };
+enum TermKind { T_FOLD_P1 = 0, T_FOLD_P2 = 1, T_SHOWDOWN = 2 };
+
+struct PNode {
+    int kind = ND_DECISION;
+    int player = -1;
+    int board_state = 0;
+    std::string hist;
+    std::vector<int> child;
+    std::vector<std::string> tok;
+    int term_kind = -1;
+    double amount = 0;  // fold: payoff to player 2; showdown: amount W won by the better hand
+    double kappa = 1;   // public chance weight of the path (Kuhn/Leduc deal probabilities)
+};
+
+struct PublicTree {
+    std::vector<PNode> nodes;  // nodes[0] = root
+    int n_board_states = 1;
+    std::vector<std::vector<int>> board_cards;  // per board state (shared part; river: per game)
+};
+
+// Per-player treeplex layout over public sequences.
+struct PlayerLayout {
+    int n_pub = 1;                 // incl. row 0 = empty sequence
+    std::vector<int> node_pub;     // public tree node id of each decision node (top-down order)
+    std::vector<int> first, nact, parent_seq, board_state, level;
+    std::vector<std::string> seq_hist;  // [n_pub], "" for row 0
+    std::vector<int> seq_owner;    // decision node owning the sequence (-1 for row 0)
+    std::vector<int> term_off, term_idx;  // terminals grouped by this player's last sequence
+    int depth = 0;
+};
+
+struct Terminal {
+    int kind;
+    double amount;
+    double kappa;
+    int board_state;
+    int last_seq[2];
+};
+
+// Card-removal / strength-order tables of one (game, board state).
+struct BoardTable {
+    int nvalid = 0;
+    std::vector<int16_t> order;  // sorted position -> hand
+    std::vector<int16_t> lo, hi; // per position: tie-group bounds [lo, hi)
+    std::vector<int16_t> src;    // expanded card array entry -> sorted position
+    std::vector<int16_t> pos4;   // per position, per card k<2: elo, ehi, est, een (8 per position)
+    std::vector<uint8_t> valid;  // per hand
+};
+
+struct HostGame {
+    int kind = 0, n_games = 0;
+    int H = 0, H_pad = 0, hand_size = 1, n_cards = 0, n_combos = 0;
+    int n_ranks = 13, n_suits = 4;
+    PublicTree tree;
+    PlayerLayout pl[2];
+    std::vector<Terminal> terms;
+    std::vector<int> hand_cards;       // [G][H][2]
+    std::vector<int> hand_combo;       // [G][H] canonical combo index of internal hand
+    std::vector<double> prior[2];      // [G][H_pad]
+    std::vector<double> kappa_game;    // [G]
+    std::vector<BoardTable> tables;    // [G * n_board_states]
+    std::vector<double> beta[2];       // [n_nodes][H_pad]
+    std::vector<double> M[2];          // [G]: max l1 norm of the treeplex
+    double big_blind = 100;
+};
+
+// Builds everything from the spec; returns an error string ("" on success).
+std::string build_host_game(const egt_game_spec& spec, HostGame& out);
+
+// ||A|| = max |A_ij| of game g (R7), O(H^2) per board state.
+double compute_max_abs_A(const HostGame& G, int g);
+
+// 5..7-card poker hand strength (larger is better, equal = tie).
+int64_t hand_strength(const int* ranks, const int* suits, int n);
+
+}  // namespace egt

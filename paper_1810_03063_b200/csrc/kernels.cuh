@@ -1,0 +1,109 @@
+// Device-side data structures and kernel launchers (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace egt {
+
+// A per-game vector, optionally double-buffered (slot chosen per game on device).
+struct VecRef {
+    double* base = nullptr;         // slot 0 of game 0
+    long long game_stride = 0;      // doubles between games
+    long long slot_stride = 0;      // doubles between slot 0 and slot 1
+    const int* slot_sel = nullptr;  // per-game current slot (nullptr: slot 0)
+    int slot_xor = 0;               // 0: current slot, 1: the other one
+    __host__ __device__ bool ok() const { return base != nullptr; }
+#ifdef __CUDACC__
+    __device__ __forceinline__ double* at(int g) const {
+        long long off = (long long)g * game_stride;
+        if (slot_sel) off += (long long)((slot_sel[g] ^ slot_xor) & 1) * slot_stride;
+        return base + off;
+    }
+#endif
+};
+
+struct DevTerm {
+    double amount;  // fold: payoff to player 2; showdown: amount W
+    double kappa;   // public chance weight
+    int kind;       // 0 fold by P1, 1 fold by P2, 2 showdown
+    int bs;         // board state
+    int seq[2];     // last public sequence of each player (0 = empty)
+};
+
+struct DevGame {
+    int n_games, H, H_pad, hand_size, n_bs;
+    const int* tab_nvalid;    // [G*n_bs]
+    const int16_t* tab_order; // [G*n_bs][H_pad]
+    const int16_t* tab_lo;    // [G*n_bs][H_pad]
+    const int16_t* tab_hi;    // [G*n_bs][H_pad]
+    const int4* tab_pos;      // [G*n_bs][H_pad] : 8 x int16 (elo, ehi, est, een) x 2 cards
+    const int16_t* tab_src;   // [G*n_bs][2*H_pad+2]
+    const uint8_t* tab_valid; // [G*n_bs][H_pad]
+    const double* prior[2];   // [G][H_pad]
+    const double* kappa_game; // [G]
+    const DevTerm* terms;
+};
+
+struct DevPlayer {
+    int n_pub, n_nodes;
+    const int* node_first;   // [n_nodes], top-down order
+    const int* node_nact;
+    const int* node_parent;  // parent public sequence (0 = empty)
+    const int* node_bs;
+    const double* beta;      // [n_nodes][H_pad]
+    const int* term_off;     // [n_pub+1] terminals grouped by this player's last sequence
+    const int* term_idx;
+};
+
+enum TreeMode { TM_SBR = 0, TM_PROX = 1, TM_BR = 2, TM_CFR = 3, TM_UNIFORM = 4, TM_COMBINE = 5 };
+
+struct TreeArgs {
+    int mode = TM_SBR;
+    VecRef g;                  // gradient input (SBR/PROX/BR/CFR)
+    double gsign = 1.0;        // objective uses gsign * g (min form; CFR: utility)
+    const double* mu = nullptr;     // SBR: per-game mu; PROX: per-game step s
+    VecRef center;             // PROX: centre (behavioural); CFR: current z (in/out); COMBINE: behavioural input
+    VecRef regret;             // CFR
+    VecRef avg;                // CFR: running average (sequence form, in/out)
+    const int* iter = nullptr; // CFR: per-game t (1-based)
+    int cfr_plus = 0;          // CFR: 1 = RM+ threshold
+    int avg_linear = 0;        // CFR: 1 = alpha_t = 2t/(t^2+t), else 1/t
+    VecRef out_b;              // behavioural output
+    VecRef out_q;              // sequence-form output
+    VecRef comb_in, comb_out;  // comb_out = (1 - tau) comb_in + tau q
+    const double* tau = nullptr;
+    double* value = nullptr;   // per-game value (SBR/BR)
+    double* partial = nullptr; // [G][n_tiles] scratch
+    unsigned* counter = nullptr; // [G] zero-initialised
+    const int* mask = nullptr; // run game g only if mask[g] == want
+    int want = 0;
+};
+
+struct DevScalars {
+    double* mu;       // [2][G]
+    double* mu_cand;  // [2][G]
+    double* tau;      // [G]
+    double* step;     // [G]
+    double* val;      // [2][G]
+    double* egv;      // [G]
+    int* focus;       // [G]
+    int* cur;         // [G]
+    int* t;           // [G]
+    int* attempts;    // [G]
+    int* backtracks;  // [G]
+    int* fail;        // [G]
+};
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
+                            const int* mask, int want, cudaStream_t st);
+cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st);
+int tree_tile_width(const DevGame& G, const DevPlayer& P);
+cudaError_t tree_prepare(int max_n_pub);
+
+cudaError_t launch_egt_prepare(int variant, int n_games, DevScalars S, cudaStream_t st);
+cudaError_t launch_egt_accept(int variant, int n_games, DevScalars S, cudaStream_t st);
+cudaError_t launch_tick(int n_games, int* t, cudaStream_t st);
+cudaError_t launch_set_mu_scale(int n_games, DevScalars S, const double* mu_base, double scale, const int* mask, cudaStream_t st);
+
+}  // namespace egt
