@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""bench.py — gradient evaluations/sec of EGT/as (dilated entropy) on HUNL river endgames.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]``;
+for N > 1 it is launched under torchrun, one rank per GPU (RANK/LOCAL_RANK/WORLD_SIZE).
+
+Workload: every rank solves its own batch of ``--batch``
+independent synthetic Libratus-scale river endgames (the paper's
+full bet abstraction, pot 2100, 200-big-blind stacks, 1081 private hands per player,
+152 public sequences per player, 203 terminals -> 237M leaf-hand pairs per endgame;
+boards and hand priors seeded per rank).  Units are shared out across ranks with no
+data-path collective ("scaling": "weak").
+
+One step = one pass of the whole hot path for every game of the batch: one EGT/as
+iteration (Alg. 3 body with Alg. 4's excessive-gap check: 4 gradient evaluations)
+followed by the stopping test eps_sad(x^t, y^t) (Alg. 3 line 5: 2 more gradient
+evaluations + 2 best-response passes) -- 6 gradient evaluations per game per step.
+``value`` = gradient evaluations of all games on all ranks / max-over-ranks device time.
+
+``--impl reference`` times the CPU oracle (``oracle/``) as it stands on the host cores,
+on one endgame of the same workload per step (a bounded sample), same metric.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "gradient evals/sec (EGT/as + eps_sad stopping test, HUNL river endgames)"
+UNIT = "grad_evals/s"
+GRADS_PER_STEP = 6  # EGT/as: 4 (Alg. 2 + EGC check); eps_sad: 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=296, help="endgames per GPU")
+    ap.add_argument("--workload", default="libratus", choices=["libratus", "simple"])
+    ap.add_argument("--seed", type=int, default=2100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--timing-steps", type=int, default=3, help="steps of the per-kernel event-timing pass")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def workload(args, rank):
+    from paper_1810_03063_b200 import workloads as W
+    spec = W.river_spec(args.workload)
+    seed = args.seed + 100003 * rank
+    boards = W.random_boards(args.batch, seed)
+    p1, p2 = W.random_priors(boards, seed)
+    return spec, boards, p1, p2
+
+
+def workload_config(args, game=None, world=1):
+    cfg = {"workload": "%s_river_endgame_batch" % args.workload,
+           "games_per_gpu": args.batch, "global_games": args.batch * world,
+           "solver": "EGT/as (dilated entropy) + eps_sad per step", "pot": 2100, "stack": 18950,
+           "bet_abstraction": "PAPER.md:673-685" if args.workload == "libratus" else "{0.5,1,all-in}",
+           "parallelism": "dp%d (independent endgames per rank)" % world}
+    if game is not None:
+        cfg.update({"hands_per_player": game.H, "pub_seqs": list(game.n_pub),
+                    "terminals": game.n_terminals,
+                    "leaf_hand_pairs_per_game": game.n_terminals * game.H * game.H,
+                    "seq_dims": [game.n_pub[0] * game.H, game.n_pub[1] * game.H]})
+    return cfg
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi samples DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([c.strip() for c in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- roofline
+def grad_bytes_per_game(game, player):
+    """Compulsory HBM bytes of one gradient evaluation of one game:
+    read the other player's vector (public sequences >= 1, H hands, fp64), write this
+    player's gradient (all public sequences, H hands), read both hand priors."""
+    o = 1 - player
+    H = game.H
+    return 8 * H * ((game.n_pub[o] - 1) + game.n_pub[player] + 2)
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kind, workload_name):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(workload_name, {}).get(kind)
+        return None if e is None else float(e["dram_bytes_per_game_launch"])
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+def oracle_sample(args, boards, p1, p2, budget_s=20.0, max_iters=None):
+    """Time the CPU oracle (as it stands) on game 0 of the workload: EGT/as initial point,
+    then EGT/as iterations each followed by eps_sad, until ~budget_s.  Returns
+    (grad evals, seconds, iterations)."""
+    from oracle import br, egt, river
+    from oracle.cards import Deck
+    from paper_1810_03063_b200 import workloads as W
+    spec = W.river_spec(args.workload)
+    deck = Deck(13, 4)
+    rp = river.RiverParams(**{k: spec[k] for k in ("pot", "stack", "fracs", "allin", "raise_cap", "open_fold")})
+    sf = river.RiverSeqForm(rp, deck, boards[0], W.prior_dict(p1[0], deck.n_cards),
+                            W.prior_dict(p2[0], deck.n_cards), build_sparse=False)
+    prob = egt.Problem(sf)
+    mu = egt.theory_mu(sf) * 2.0 ** -8
+    t0 = time.perf_counter()
+    x, y = egt.initialize(prob, mu, mu)
+    st = egt.EGTState(x, y, mu, mu)
+    grads = prob.grads.n
+    iters = 0
+    while True:
+        egt.egt_iteration(prob, st, "as")
+        br.saddle_gap(sf, st.x, st.y)
+        iters += 1
+        grads = prob.grads.n + 2 * iters
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_iters and iters >= max_iters):
+            break
+    return grads, time.perf_counter() - t0, iters
+
+
+def host_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info()]
+        return max(n) if n else 1
+    except Exception:
+        return 1
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    spec, boards, p1, p2 = workload(args, 0)
+    from oracle import br, egt, river
+    from oracle.cards import Deck
+    from paper_1810_03063_b200 import workloads as W
+    deck = Deck(13, 4)
+    rp = river.RiverParams(**{k: spec[k] for k in ("pot", "stack", "fracs", "allin", "raise_cap", "open_fold")})
+    sf = river.RiverSeqForm(rp, deck, boards[0], W.prior_dict(p1[0], deck.n_cards),
+                            W.prior_dict(p2[0], deck.n_cards), build_sparse=False)
+    prob = egt.Problem(sf)
+    mu = egt.theory_mu(sf) * 2.0 ** -8
+    x, y = egt.initialize(prob, mu, mu)
+    st = egt.EGTState(x, y, mu, mu)
+
+    def step():
+        egt.egt_iteration(prob, st, "as")
+        br.saddle_gap(sf, st.x, st.y)
+        prob.grads.n += 2
+
+    for _ in range(args.warmup):
+        step()
+    g0 = prob.grads.n
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    grads = prob.grads.n - g0
+    v = grads / el
+    cores = host_threads()
+    sample = "1 endgame (game 0 of rank 0's batch), %d EGT/as iterations + eps_sad, fp64 numpy" % args.steps
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": workload_config(args, None, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1810_03063_b200 as P
+    from paper_1810_03063_b200 import build as B
+
+    rank, local, world = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    P.load_library()
+
+    spec, boards, p1, p2 = workload(args, rank)
+    game = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2)
+    stream = torch.cuda.current_stream()
+    game.set_stream(stream)
+    game.egt_init(P.EGT_AS)  # practical mu (R14)
+    gap = torch.zeros(args.batch, dtype=torch.float64, device="cuda")
+
+    def step():
+        game.egt_step(1)
+        game.saddle_gap_device(0, gap)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_grads = GRADS_PER_STEP * args.batch * world * args.steps
+    value = total_grads / (ms / 1e3)
+    gaps = gap.cpu().numpy()
+
+    # per-kernel event timing (same kernels, eager launches, events on the library stream)
+    game.timing(True)
+    for _ in range(args.timing_steps):
+        step()
+    kt = game.timing_get()
+    game.timing(False)
+    torch.cuda.synchronize()
+    launches_per_step = sum(v[1] for v in kt.values()) / args.timing_steps
+    step_ms_eager = sum(v[0] for v in kt.values()) / args.timing_steps
+    dom = max(kt, key=lambda k: kt[k][0])
+    peak, peak_src = measured_peak()
+    roof = None
+    if dom.startswith("grad"):
+        p = 0 if dom == "grad_Ay" else 1
+        per_game = grad_bytes_per_game(game, p)
+        ms_k, nl, active = kt[dom]
+        achieved = per_game * active / (ms_k / 1e3) / 1e9
+        tr = ncu_traffic(dom, args.workload)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None if tr is None else tr * active / nl,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": per_game * active / nl,
+                "avg_launch_ms": ms_k / nl, "share_of_step": ms_k / sum(v[0] for v in kt.values())}
+    else:
+        ms_k, nl, active = kt[dom]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+                "traffic": None, "peak_source": peak_src, "avg_launch_ms": ms_k / nl,
+                "share_of_step": ms_k / sum(v[0] for v in kt.values())}
+    kernel_split = {k: {"ms_per_step": v[0] / args.timing_steps, "launches_per_step": v[1] / args.timing_steps}
+                    for k, v in kt.items()}
+
+    line = None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(workload_config(args, game, world),
+                               l2="no flush: per-step working set %.0f MB > 126 MB L2" %
+                               (args.batch * 2 * 7 * 8 * game.H_pad * max(game.n_pub) / 1e6)),
+                "roofline": roof, "kernels": kernel_split, "eager_step_ms": step_ms_eager,
+                "gpu_launches": int(round(launches_per_step * args.steps)),
+                "clocks": ck, "gap_after": {"median": float(np.median(gaps)), "max": float(np.max(gaps)),
+                                            "unit": "chips"}}
+
+    # e2e: the same metric through the public API from host buffers -- load the batch from
+    # host arrays (H2D inside egt_load_game), init, K steps each reading eps_sad back to host.
+    if not args.no_e2e:
+        game.close()
+        del game
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        pinned = torch.zeros(args.batch, dtype=torch.float64).pin_memory()
+        t0 = time.perf_counter()
+        g2 = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2)
+        g2.egt_init(P.EGT_AS)
+        for _ in range(args.steps):
+            g2.egt_step(1)
+            g2.saddle_gap(0, out=pinned)
+        el = time.perf_counter() - t0
+        grads_e2e = float(g2.egt_scalars()[0, 7])
+        te = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        if rank == 0:
+            line["e2e"] = {"value": grads_e2e * args.batch * world / el, "unit": UNIT,
+                           "h2d_bytes_per_step": int(g2.h2d_bytes / args.steps),
+                           "d2h_bytes_per_step": 8 * args.batch,
+                           "what": "wall clock: egt_load_game from host arrays + egt_init (mu search) + "
+                                   "K x (egt_step + saddle_gap to pinned host); counts every gradient "
+                                   "evaluation incl. init", "seconds": el}
+        g2.close()
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        grads, secs, iters = oracle_sample(args, boards, p1, p2)
+        line["cpu_baseline"] = {"value": grads / secs, "unit": UNIT, "cores": host_threads(), "kind": "oracle",
+                                "sample": "1 endgame (game 0), oracle EGT/as initial point + %d iterations "
+                                          "each with eps_sad (%d gradient evals, %.1f s)" % (iters, grads, secs)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

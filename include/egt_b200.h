@@ -90,6 +90,7 @@ typedef struct {
     int32_t depth[2];   /* levels of decision nodes per player */
     int64_t vec_stride[2]; /* doubles per game in a player's vector (= n_pub * H_pad) */
     double max_abs_A[1];   /* reserved: ||A|| of game 0 (max |A_ij|, R7) */
+    int64_t h2d_bytes;     /* bytes egt_load_game copied host -> device (layout, tables, priors) */
 } egt_game_info;
 
 /* ---- game ---------------------------------------------------------------- */
@@ -176,6 +177,10 @@ int cfr_step(egt_game* game, int32_t n_iters);
  * which = 1: the CFR averages (xbar, ybar); for EGT the same as 0. */
 int saddle_gap(egt_game* game, int32_t which, double* host_out);
 
+/* As saddle_gap, but the per-game eps_sad goes to DEVICE dev_out[n_games], stream-ordered
+ * (no host synchronisation; complete when the stream set by egt_set_stream syncs). */
+int saddle_gap_device(egt_game* game, int32_t which, double* dev_out);
+
 /* Strategy of `player` in sequence form, HOST out [n_games][n_pub][n_combos]: the EGT
  * iterate, or the CFR average; canonical combo/card order; hands blocked by the
  * board are 0; row 0 = 1. */
@@ -190,6 +195,21 @@ int get_strategy_device(egt_game* game, int32_t player, int32_t which, double* d
  * mu_x, mu_y, tau, t (accepted steps / CFR iterations), attempts, backtracks,
  * last EGV, gradient evaluations (A y or A^T x, per game). */
 int egt_scalars(egt_game* game, double* host_out);
+
+/* ---- kernel timing (measurement only) -------------------------------------------
+ * egt_timing(game, 1) switches egt_step / cfr_step / saddle_gap* to eager launches,
+ * each bracketed by a pair of CUDA events on the library's stream (the stream the
+ * kernels run on), and clears the accumulators; egt_timing(game, 0) switches back to
+ * CUDA-graph replay.  egt_timing_get writes HOST out[EGT_N_KERNEL_KINDS][3]:
+ * total device ms, launches, and game-launches that did work (a masked EGT launch
+ * only works on the games whose step focuses on that player), per kernel kind. */
+#define EGT_KERNEL_GRAD_AY 0  /* gradient kernel, player 0: A y        */
+#define EGT_KERNEL_GRAD_ATX 1 /* gradient kernel, player 1: A^T x      */
+#define EGT_KERNEL_TREE 2     /* treeplex kernel (SBR / prox / BR / CFR / combine) */
+#define EGT_KERNEL_SCALAR 3   /* per-game scalar kernels (EGT stepsizes, EGC accept, gap) */
+#define EGT_N_KERNEL_KINDS 4
+int egt_timing(egt_game* game, int32_t enable);
+int egt_timing_get(egt_game* game, double* host_out);
 
 const char* egt_last_error(void);
 

@@ -47,6 +47,7 @@ class Info(ctypes.Structure):
         ("n_combos", ctypes.c_int32), ("n_pub", ctypes.c_int32 * 2), ("n_nodes", ctypes.c_int32 * 2),
         ("n_terminals", ctypes.c_int32), ("depth", ctypes.c_int32 * 2),
         ("vec_stride", ctypes.c_int64 * 2), ("max_abs_A", ctypes.c_double * 1),
+        ("h2d_bytes", ctypes.c_int64),
     ]
 
 
@@ -54,8 +55,10 @@ EXPORTS = [
     "egt_load_game", "egt_free_game", "egt_set_stream", "egt_game_info_get", "egt_hand_cards",
     "egt_pub_history", "egt_gradient", "egt_smoothed_br", "egt_prox", "egt_best_response",
     "egt_init", "egt_step", "cfr_init", "cfr_step", "saddle_gap", "get_avg_strategy",
-    "get_strategy_device", "egt_scalars", "egt_last_error",
+    "get_strategy_device", "egt_scalars", "egt_last_error", "saddle_gap_device",
+    "egt_timing", "egt_timing_get",
 ]
+KERNEL_KINDS = ("grad_Ay", "grad_ATx", "tree", "scalar")
 
 _lib = None
 
@@ -94,6 +97,9 @@ def load_library():
         "get_strategy_device": ([P, I32, I32, VP], I32),
         "egt_scalars": ([P, ctypes.POINTER(D)], I32),
         "egt_last_error": ([], ctypes.c_char_p),
+        "saddle_gap_device": ([P, I32, VP], I32),
+        "egt_timing": ([P, I32], I32),
+        "egt_timing_get": ([P, ctypes.POINTER(D)], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -165,6 +171,7 @@ class Game:
         self.depth = (info.depth[0], info.depth[1])
         self.n_terminals = info.n_terminals
         self.vec_stride = (info.vec_stride[0], info.vec_stride[1])
+        self.h2d_bytes = info.h2d_bytes
 
     def close(self):
         if self._h:
@@ -230,6 +237,19 @@ class Game:
             out = np.zeros(self.n_games)
         _check(self._L.saddle_gap(self._h, which, ctypes.cast(_host_ptr(out), ctypes.POINTER(ctypes.c_double))))
         return out
+
+    def saddle_gap_device(self, which, dout):
+        """Per-game eps_sad into a DEVICE fp64 [n_games] buffer, stream-ordered."""
+        _check(self._L.saddle_gap_device(self._h, which, _ptr(dout)))
+
+    def timing(self, enable):
+        _check(self._L.egt_timing(self._h, int(bool(enable))))
+
+    def timing_get(self):
+        """{kind: (ms, launches, active game-launches)} since the last timing(True)."""
+        out = np.zeros(3 * len(KERNEL_KINDS))
+        _check(self._L.egt_timing_get(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return {k: tuple(out[3 * i:3 * i + 3]) for i, k in enumerate(KERNEL_KINDS)}
 
     def get_avg_strategy(self, player, out=None):
         if out is None:

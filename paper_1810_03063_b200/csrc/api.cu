@@ -48,6 +48,7 @@ struct egt_game {
     double* mu_base = nullptr;      // [2][G] for the mu search
     int* search_mask = nullptr;     // [G]
     double* gapval = nullptr;       // [2][G]
+    double* gapout = nullptr;       // [G]
     double* S[2] = {nullptr, nullptr};   // EGT state, 2 slots
     double* C[2] = {nullptr, nullptr};   // EGT cache (behavioural smoothed BR), 2 slots
     double* HAT[2] = {nullptr, nullptr};
@@ -59,7 +60,17 @@ struct egt_game {
     double* AVG[2] = {nullptr, nullptr}; // CFR average
     cudaGraphExec_t graph = nullptr;
     long long grads = 0;            // gradient evaluations per game
+    long long h2d_bytes = 0;        // uploaded by egt_load_game
     int grads_per_iter = 0;
+    // kernel timing mode (egt_timing): eager launches bracketed by CUDA events
+    int timing = 0;
+    std::vector<int> focus_host;    // per-game focus of the current EGT iteration (timing mode)
+    struct Pending { int kind; long long active; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double t_ms[EGT_N_KERNEL_KINDS] = {0};
+    double t_launch[EGT_N_KERNEL_KINDS] = {0};
+    double t_active[EGT_N_KERNEL_KINDS] = {0};
 };
 
 const char* egt_last_error(void) { return g_err.c_str(); }
@@ -80,6 +91,7 @@ static int upload(egt_game* G, T** p, const std::vector<T>& v) {
     int r = dalloc(G, p, v.size());
     if (r) return r;
     if (!v.empty()) CK(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    G->h2d_bytes += (long long)(v.size() * sizeof(T));
     return 0;
 }
 
@@ -249,6 +261,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(dalloc(G, &G->mu_base, 2 * (size_t)Gn));
     TRY(dalloc(G, &G->search_mask, (size_t)Gn));
     TRY(dalloc(G, &G->gapval, 2 * (size_t)Gn));
+    TRY(dalloc(G, &G->gapout, (size_t)Gn));
     for (int p = 0; p < 2; ++p) {
         const size_t n = (size_t)Gn * G->V[p];
         TRY(dalloc(G, &G->GR[p], n));
@@ -267,6 +280,11 @@ extern "C" void egt_free_game(egt_game* G) {
     if (!G) return;
     if (G->graph) cudaGraphExecDestroy(G->graph);
     if (G->st) cudaStreamSynchronize(G->st);
+    for (auto& p : G->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : G->ev_pool) cudaEventDestroy(e);
     for (void* p : G->allocs) cudaFree(p);
     if (G->ev_in) cudaEventDestroy(G->ev_in);
     if (G->ev_out) cudaEventDestroy(G->ev_out);
@@ -296,6 +314,7 @@ extern "C" int egt_game_info_get(const egt_game* G, egt_game_info* o) {
     }
     o->n_terminals = (int)H.terms.size();
     o->max_abs_A[0] = 0.0;
+    o->h2d_bytes = G->h2d_bytes;
     return 0;
 }
 
@@ -391,9 +410,70 @@ static int ensure_egt_buffers(egt_game* G) {
     return 0;
 }
 
-static cudaError_t tree(egt_game* G, int p, const TreeArgs& A) { return launch_tree(G->dg, G->dp[p], p, A, G->st); }
+// ---- kernel timing (egt_timing): every launch bracketed by a pair of events on G->st
+static cudaEvent_t pool_event(egt_game* G) {
+    if (!G->ev_pool.empty()) {
+        cudaEvent_t e = G->ev_pool.back();
+        G->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+static cudaError_t timing_flush(egt_game* G) {
+    if (G->pending.empty()) return cudaSuccess;
+    cudaError_t e = cudaStreamSynchronize(G->st);
+    if (e != cudaSuccess) return e;
+    for (auto& p : G->pending) {
+        float ms = 0.f;
+        e = cudaEventElapsedTime(&ms, p.a, p.b);
+        if (e != cudaSuccess) return e;
+        G->t_ms[p.kind] += ms;
+        G->t_launch[p.kind] += 1;
+        G->t_active[p.kind] += (double)p.active;
+        G->ev_pool.push_back(p.a);
+        G->ev_pool.push_back(p.b);
+    }
+    G->pending.clear();
+    return cudaSuccess;
+}
+
+// games that do work under (mask, want); only known on the host in timing mode
+static long long active_games(egt_game* G, const int* mask, int want) {
+    const int Gn = G->host.n_games;
+    if (!mask) return Gn;
+    if (mask != G->sc.focus || (int)G->focus_host.size() != Gn) return Gn;
+    long long n = 0;
+    for (int g = 0; g < Gn; ++g) n += G->focus_host[g] == want;
+    return n;
+}
+
+template <class F>
+static cudaError_t timed(egt_game* G, int kind, long long active, F&& launch) {
+    if (!G->timing) return launch();
+    cudaEvent_t a = pool_event(G), b = pool_event(G);
+    cudaError_t e = cudaEventRecord(a, G->st);
+    if (e == cudaSuccess) e = launch();
+    if (e == cudaSuccess) e = cudaEventRecord(b, G->st);
+    if (e != cudaSuccess) return e;
+    G->pending.push_back({kind, active, a, b});
+    if (G->pending.size() >= 1024) return timing_flush(G);
+    return cudaSuccess;
+}
+
+static cudaError_t tree(egt_game* G, int p, const TreeArgs& A) {
+    return timed(G, EGT_KERNEL_TREE, active_games(G, A.mask, A.want),
+                 [&] { return launch_tree(G->dg, G->dp[p], p, A, G->st); });
+}
 static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0) {
-    return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, G->st);
+    return timed(G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
+                 [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, G->st); });
+}
+template <class F>
+static cudaError_t scalar_k(egt_game* G, F&& launch) {
+    return timed(G, EGT_KERNEL_SCALAR, G->host.n_games, launch);
 }
 
 // EGT initial point (Alg. 1/3 lines 1-2, R4) at the current per-game mu;
@@ -447,7 +527,13 @@ static int record_egt_iteration(egt_game* G) {
     const int Gn = G->host.n_games;
     DevScalars& S = G->sc;
     const int var = G->variant;
-    CK(launch_egt_prepare(var, Gn, S, G->st));
+    CK(scalar_k(G, [&] { return launch_egt_prepare(var, Gn, S, G->st); }));
+    if (G->timing) {
+        // timing mode only: learn each game's focus so masked launches report their active games
+        G->focus_host.assign(Gn, 0);
+        CK(cudaMemcpyAsync(G->focus_host.data(), S.focus, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
+        CK(cudaStreamSynchronize(G->st));
+    }
     for (int p = 0; p < 2; ++p) {
         const int o = 1 - p;
         if (var != EGT_AS) {
@@ -519,7 +605,7 @@ static int record_egt_iteration(egt_game* G) {
             CK(tree(G, p, A));
         }
     }
-    CK(launch_egt_accept(var, Gn, S, G->st));
+    CK(scalar_k(G, [&] { return launch_egt_accept(var, Gn, S, G->st); }));
     return 0;
 }
 
@@ -618,9 +704,16 @@ extern "C" int egt_step(egt_game* G, int32_t n_iters) {
     if (!G) return fail(EGT_E_ARG, "null game");
     if (G->solver != SOLVER_EGT) return fail(EGT_E_STATE, "egt_step before egt_init");
     if (n_iters <= 0) return 0;
-    if (!G->graph && build_graph(G, record_egt_iteration)) return EGT_E_CUDA;
+    if (!G->timing && !G->graph && build_graph(G, record_egt_iteration)) return EGT_E_CUDA;
     if (begin(G)) return EGT_E_CUDA;
-    for (int i = 0; i < n_iters; ++i) CK(cudaGraphLaunch(G->graph, G->st));
+    for (int i = 0; i < n_iters; ++i) {
+        if (G->timing) {
+            int r = record_egt_iteration(G);
+            if (r) return r;
+        } else {
+            CK(cudaGraphLaunch(G->graph, G->st));
+        }
+    }
     G->grads += (long long)G->grads_per_iter * n_iters;
     return end(G);
 }
@@ -645,7 +738,7 @@ static int record_cfr_iteration(egt_game* G) {
         A.avg_linear = G->variant == CFR_PLUS;
         CK(tree(G, p, A));
     }
-    CK(launch_tick(Gn, G->sc.t, G->st));
+    CK(scalar_k(G, [&] { return launch_tick(Gn, G->sc.t, G->st); }));
     return 0;
 }
 
@@ -689,9 +782,16 @@ extern "C" int cfr_step(egt_game* G, int32_t n_iters) {
     if (!G) return fail(EGT_E_ARG, "null game");
     if (G->solver != SOLVER_CFR) return fail(EGT_E_STATE, "cfr_step before cfr_init");
     if (n_iters <= 0) return 0;
-    if (!G->graph && build_graph(G, record_cfr_iteration)) return EGT_E_CUDA;
+    if (!G->timing && !G->graph && build_graph(G, record_cfr_iteration)) return EGT_E_CUDA;
     if (begin(G)) return EGT_E_CUDA;
-    for (int i = 0; i < n_iters; ++i) CK(cudaGraphLaunch(G->graph, G->st));
+    for (int i = 0; i < n_iters; ++i) {
+        if (G->timing) {
+            int r = record_cfr_iteration(G);
+            if (r) return r;
+        } else {
+            CK(cudaGraphLaunch(G->graph, G->st));
+        }
+    }
     G->grads += 2LL * n_iters;
     return end(G);
 }
@@ -712,13 +812,12 @@ static int strategy_refs(egt_game* G, int which, VecRef out[2]) {
     return 0;
 }
 
-extern "C" int saddle_gap(egt_game* G, int32_t which, double* host_out) {
-    if (!G || !host_out) return fail(EGT_E_ARG, "bad argument");
+// eps_sad = max_y <x, A y> - min_x <x, A y>, enqueued on G->st:
+// gapval[0][g] = min_x <x, A y>, gapval[1][g] = min_y <y, -A^T x>, dev_out[g] = -(both).
+static int enqueue_gap(egt_game* G, int which, double* dev_out) {
     VecRef s[2];
     if (strategy_refs(G, which, s)) return EGT_E_STATE;
     const int Gn = G->host.n_games;
-    if (begin(G)) return EGT_E_CUDA;
-    // eps_sad = max_y <x, A y> - min_x <x, A y>
     for (int p = 0; p < 2; ++p) {
         CK(grad(G, p, s[1 - p], vec(G->GR[p], G->V[p])));
         TreeArgs A = base_args();
@@ -730,12 +829,48 @@ extern "C" int saddle_gap(egt_game* G, int32_t which, double* host_out) {
         A.counter = G->counter;
         CK(tree(G, p, A));
     }
-    std::vector<double> v(2 * (size_t)Gn);
-    CK(cudaMemcpyAsync(v.data(), G->gapval, sizeof(double) * 2 * Gn, cudaMemcpyDeviceToHost, G->st));
-    CK(cudaStreamSynchronize(G->st));
-    for (int g = 0; g < Gn; ++g) host_out[g] = -v[Gn + g] - v[g];
+    CK(scalar_k(G, [&] { return launch_gap_combine(Gn, G->gapval, dev_out, G->st); }));
     G->grads += 2;
+    return 0;
+}
+
+extern "C" int saddle_gap(egt_game* G, int32_t which, double* host_out) {
+    if (!G || !host_out) return fail(EGT_E_ARG, "bad argument");
+    const int Gn = G->host.n_games;
+    if (begin(G)) return EGT_E_CUDA;
+    int r = enqueue_gap(G, which, G->gapout);
+    if (r) return r;
+    CK(cudaMemcpyAsync(host_out, G->gapout, sizeof(double) * Gn, cudaMemcpyDeviceToHost, G->st));
+    CK(cudaStreamSynchronize(G->st));
     return end(G);
+}
+
+extern "C" int saddle_gap_device(egt_game* G, int32_t which, double* dev_out) {
+    if (!G || !dev_out) return fail(EGT_E_ARG, "bad argument");
+    if (begin(G)) return EGT_E_CUDA;
+    int r = enqueue_gap(G, which, dev_out);
+    if (r) return r;
+    return end(G);
+}
+
+extern "C" int egt_timing(egt_game* G, int32_t enable) {
+    if (!G) return fail(EGT_E_ARG, "null game");
+    CK(timing_flush(G));
+    for (int k = 0; k < EGT_N_KERNEL_KINDS; ++k) G->t_ms[k] = G->t_launch[k] = G->t_active[k] = 0.0;
+    G->timing = enable != 0;
+    if (!G->timing) G->focus_host.clear();
+    return 0;
+}
+
+extern "C" int egt_timing_get(egt_game* G, double* host_out) {
+    if (!G || !host_out) return fail(EGT_E_ARG, "bad argument");
+    CK(timing_flush(G));
+    for (int k = 0; k < EGT_N_KERNEL_KINDS; ++k) {
+        host_out[3 * k + 0] = G->t_ms[k];
+        host_out[3 * k + 1] = G->t_launch[k];
+        host_out[3 * k + 2] = G->t_active[k];
+    }
+    return 0;
 }
 
 extern "C" int get_strategy_device(egt_game* G, int32_t player, int32_t which, double* dev_out) {

@@ -424,6 +424,18 @@ __global__ void set_mu_scale_kernel(int n, DevScalars S, const double* base, dou
     S.mu[n + g] = base[n + g] * scale;
 }
 
+// eps_sad per game from the two best-response values:
+// val[g] = min_x <x, A y>, val[n+g] = min_y <y, -A^T x> = -max_y <x, A y>.
+__global__ void gap_combine_kernel(int n, const double* __restrict__ val, double* __restrict__ out) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) out[g] = -val[n + g] - val[g];
+}
+
+cudaError_t launch_gap_combine(int n, const double* val, double* out, cudaStream_t st) {
+    gap_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, val, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_egt_prepare(int variant, int n, DevScalars S, cudaStream_t st) {
     egt_prepare_kernel<<<(n + 127) / 128, 128, 0, st>>>(variant, n, S);
     return cudaGetLastError();
