@@ -152,7 +152,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         cudaError_t e = cudaStreamCreateWithFlags(&G->st, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_in, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_out, cudaEventDisableTiming);
-        if (e == cudaSuccess) e = tree_prepare(0);
+        if (e == cudaSuccess) e = kernels_prepare();
         if (e != cudaSuccess) {
             egt_free_game(G);
             return fail(EGT_E_CUDA, std::string("stream/event: ") + cudaGetErrorString(e));
@@ -160,26 +160,26 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     }
     // tables
     std::vector<int> nvalid;
-    std::vector<int16_t> order, lo, hi, src, pos4;
+    std::vector<int16_t> order, seg;
+    std::vector<uint32_t> lohi, ent;
     std::vector<uint8_t> valid;
     for (const BoardTable& tb : H.tables) {
         nvalid.push_back(tb.nvalid);
         order.insert(order.end(), tb.order.begin(), tb.order.end());
-        lo.insert(lo.end(), tb.lo.begin(), tb.lo.end());
-        hi.insert(hi.end(), tb.hi.begin(), tb.hi.end());
-        src.insert(src.end(), tb.src.begin(), tb.src.end());
-        pos4.insert(pos4.end(), tb.pos4.begin(), tb.pos4.end());
+        lohi.insert(lohi.end(), tb.lohi.begin(), tb.lohi.end());
+        seg.insert(seg.end(), tb.seg.begin(), tb.seg.end());
+        ent.insert(ent.end(), tb.ent.begin(), tb.ent.end());
         valid.insert(valid.end(), tb.valid.begin(), tb.valid.end());
     }
-    int *d_nvalid;
-    int16_t *d_order, *d_lo, *d_hi, *d_src, *d_pos;
+    int* d_nvalid;
+    int16_t *d_order, *d_seg;
+    uint32_t *d_lohi, *d_ent;
     uint8_t* d_valid;
     TRY(upload(G, &d_nvalid, nvalid));
     TRY(upload(G, &d_order, order));
-    TRY(upload(G, &d_lo, lo));
-    TRY(upload(G, &d_hi, hi));
-    TRY(upload(G, &d_src, src));
-    TRY(upload(G, &d_pos, pos4));
+    TRY(upload(G, &d_lohi, lohi));
+    TRY(upload(G, &d_seg, seg));
+    TRY(upload(G, &d_ent, ent));
     TRY(upload(G, &d_valid, valid));
     double *d_p0, *d_p1, *d_kg;
     TRY(upload(G, &d_p0, H.prior[0]));
@@ -203,12 +203,13 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     G->dg.H_pad = Hp;
     G->dg.hand_size = H.hand_size;
     G->dg.n_bs = nbs;
+    G->dg.n_cards = H.n_cards;
+    G->dg.all_valid = H.all_valid;
     G->dg.tab_nvalid = d_nvalid;
     G->dg.tab_order = d_order;
-    G->dg.tab_lo = d_lo;
-    G->dg.tab_hi = d_hi;
-    G->dg.tab_pos = reinterpret_cast<const int4*>(d_pos);
-    G->dg.tab_src = d_src;
+    G->dg.tab_lohi = d_lohi;
+    G->dg.tab_seg = d_seg;
+    G->dg.tab_ent = d_ent;
     G->dg.tab_valid = d_valid;
     G->dg.prior[0] = d_p0;
     G->dg.prior[1] = d_p1;
@@ -219,7 +220,11 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         DevPlayer& P = G->dp[p];
         P.n_pub = L.n_pub;
         P.n_nodes = (int)L.first.size();
-        int *a, *b, *c, *d, *e, *f;
+        P.n_levels = (int)L.lvl_off.size() - 1;
+        P.n_rows_term = (int)L.rows_term.size();
+        P.max_level_width = 0;
+        for (int l = 0; l < P.n_levels; ++l) P.max_level_width = std::max(P.max_level_width, L.lvl_off[l + 1] - L.lvl_off[l]);
+        int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt;
         double* be;
         TRY(upload(G, &a, L.first));
         TRY(upload(G, &b, L.nact));
@@ -228,6 +233,11 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         TRY(upload(G, &be, H.beta[p]));
         TRY(upload(G, &e, L.term_off));
         TRY(upload(G, &f, L.term_idx));
+        TRY(upload(G, &lo, L.lvl_off));
+        TRY(upload(G, &ln, L.lvl_nodes));
+        TRY(upload(G, &ko, L.kid_off));
+        TRY(upload(G, &kd, L.kids));
+        TRY(upload(G, &rt, L.rows_term));
         P.node_first = a;
         P.node_nact = b;
         P.node_parent = c;
@@ -235,6 +245,15 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         P.beta = be;
         P.term_off = e;
         P.term_idx = f;
+        P.lvl_off = lo;
+        P.lvl_nodes = ln;
+        P.kid_off = ko;
+        P.kids = kd;
+        P.rows_term = rt;
+        if (tree_smem_bytes(P) > 200 * 1024) {
+            egt_free_game(G);
+            return fail(EGT_E_ARG, "public tree too large for the treeplex kernel's shared-memory tile");
+        }
         G->V[p] = (long long)L.n_pub * Hp;
     }
     const int max_tiles = (H.H + 31) / 32;
@@ -266,6 +285,11 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         const size_t n = (size_t)Gn * G->V[p];
         TRY(dalloc(G, &G->GR[p], n));
         TRY(dalloc(G, &G->HAT[p], n));
+        // rows that end no terminal are never written by the solver's gradient launches
+        if (cudaMemset(G->GR[p], 0, n * sizeof(double)) != cudaSuccess) {
+            egt_free_game(G);
+            return fail(EGT_E_CUDA, "memset");
+        }
     }
     if (cudaDeviceSynchronize() != cudaSuccess) {
         egt_free_game(G);
@@ -343,7 +367,7 @@ extern "C" int egt_gradient(egt_game* G, int32_t player, const double* din, doub
     if (!G || !din || !dout || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
     if (begin(G)) return EGT_E_CUDA;
     CK(launch_gradient(G->dg, G->dp[player], player, vec(const_cast<double*>(din), G->V[1 - player]),
-                       vec(dout, G->V[player]), nullptr, 0, G->st));
+                       vec(dout, G->V[player]), nullptr, 0, 1, G->st));
     return end(G);
 }
 
@@ -469,7 +493,7 @@ static cudaError_t tree(egt_game* G, int p, const TreeArgs& A) {
 }
 static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0) {
     return timed(G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
-                 [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, G->st); });
+                 [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st); });
 }
 template <class F>
 static cudaError_t scalar_k(egt_game* G, F&& launch) {

@@ -287,6 +287,27 @@ static void build_layout(HostGame& G) {
             for (int t : by[s]) L.term_idx.push_back(t);
         }
         L.term_off[L.n_pub] = (int)L.term_idx.size();
+        L.rows_term.clear();
+        for (int s = 0; s < L.n_pub; ++s)
+            if (L.term_off[s + 1] > L.term_off[s]) L.rows_term.push_back(s);
+        const int nn = (int)L.first.size();
+        L.lvl_off.assign(L.depth + 1, 0);
+        L.lvl_nodes.clear();
+        for (int l = 0; l < L.depth; ++l) {
+            L.lvl_off[l] = (int)L.lvl_nodes.size();
+            for (int m = 0; m < nn; ++m)
+                if (L.level[m] == l) L.lvl_nodes.push_back(m);
+        }
+        L.lvl_off[L.depth] = (int)L.lvl_nodes.size();
+        std::vector<std::vector<int>> kid(L.n_pub);
+        for (int m = 0; m < nn; ++m) kid[L.parent_seq[m]].push_back(m);
+        L.kid_off.assign(L.n_pub + 1, 0);
+        L.kids.clear();
+        for (int s = 0; s < L.n_pub; ++s) {
+            L.kid_off[s] = (int)L.kids.size();
+            for (int m : kid[s]) L.kids.push_back(m);
+        }
+        L.kid_off[L.n_pub] = (int)L.kids.size();
     }
 }
 
@@ -334,42 +355,44 @@ static void build_table(const HostGame& G, int g, int bs, const std::vector<int>
     tb.order.assign(Hp, 0);
     tb.lo.assign(Hp, 0);
     tb.hi.assign(Hp, 0);
+    tb.lohi.assign(Hp, 0);
     for (int i = 0; i < nv; ++i) tb.order[i] = (int16_t)v[i].second;
+    for (int h = 0, i = nv; h < H; ++h)
+        if (!tb.valid[h]) tb.order[i++] = (int16_t)h;  // blocked hands after the valid ones
     for (int i = 0; i < nv;) {
         int j = i;
         while (j < nv && v[j].first == v[i].first) ++j;
-        for (int k = i; k < j; ++k) { tb.lo[k] = (int16_t)i; tb.hi[k] = (int16_t)j; }
+        for (int k = i; k < j; ++k) {
+            tb.lo[k] = (int16_t)i;
+            tb.hi[k] = (int16_t)j;
+            tb.lohi[k] = (uint32_t)i | ((uint32_t)j << 16);
+        }
         i = j;
     }
-    // expanded card array: for each card, the sorted positions of the valid hands holding it
+    // card segments: for each card, the sorted positions of the valid hands holding it
     std::vector<std::vector<int>> by_card(G.n_cards);
-    for (int i = 0; i < nv; ++i) {
-        const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
-        for (int k = 0; k < hs; ++k) by_card[hc[k]].push_back(i);
-    }
-    std::vector<int> seg_start(G.n_cards + 1, 0);
-    tb.src.assign(2 * (size_t)Hp + 2, 0);
-    int ne = 0;
-    for (int c = 0; c < G.n_cards; ++c) {
-        seg_start[c] = ne;
-        for (int i : by_card[c]) tb.src[ne++] = (int16_t)i;
-    }
-    seg_start[G.n_cards] = ne;
-    tb.pos4.assign((size_t)Hp * 8, 0);
+    std::vector<std::vector<int>> slot_of(G.n_cards);
     for (int i = 0; i < nv; ++i) {
         const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
         for (int k = 0; k < hs; ++k) {
-            int c = hc[k];
-            const std::vector<int>& L = by_card[c];
-            int nlo = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.lo[i]) - L.begin());
-            int nhi = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.hi[i]) - L.begin());
-            int16_t* P = &tb.pos4[(size_t)i * 8 + k * 4];
-            P[0] = (int16_t)(seg_start[c] + nlo);   // elo
-            P[1] = (int16_t)(seg_start[c] + nhi);   // ehi
-            P[2] = (int16_t)seg_start[c];           // est
-            P[3] = (int16_t)seg_start[c + 1];       // een
+            by_card[hc[k]].push_back(i);
+            slot_of[hc[k]].push_back(k);
         }
     }
+    tb.seg.assign(G.n_cards + 1, 0);
+    tb.ent.assign(2 * (size_t)Hp, 0);
+    int ne = 0;
+    for (int c = 0; c < G.n_cards; ++c) {
+        tb.seg[c] = (int16_t)ne;
+        const std::vector<int>& L = by_card[c];
+        for (size_t j = 0; j < L.size(); ++j) {
+            const int i = L[j];
+            const int relo = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.lo[i]) - L.begin());
+            const int rehi = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.hi[i]) - L.begin());
+            tb.ent[ne++] = ENT_PACK(i, slot_of[c][j], relo, rehi);
+        }
+    }
+    tb.seg[G.n_cards] = (int16_t)ne;
 }
 
 std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
@@ -422,6 +445,8 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
         return "unknown game kind";
     }
     G.H_pad = (G.H + 31) / 32 * 32;
+    if (G.H > EGT_MAX_HANDS) return "too many private hands for the gradient kernel";
+    if (G.n_cards - 5 - 1 > 64 && G.kind == EGT_GAME_RIVER) return "deck too large (card segments > 64)";
     build_layout(G);
     const int Gn = G.n_games, H = G.H, Hp = G.H_pad;
 
@@ -495,6 +520,9 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
     for (int g = 0; g < Gn; ++g)
         for (int bs = 0; bs < nbs; ++bs)
             build_table(G, g, bs, board_of(G, game_boards, g, bs), G.tables[(size_t)g * nbs + bs]);
+    G.all_valid = 1;
+    for (const BoardTable& tb : G.tables)
+        if (tb.nvalid != H) G.all_valid = 0;
 
     // beta and M per (node, hand), validity of game 0
     // (identical across games: river hands all avoid their board; Kuhn/Leduc games are equal)

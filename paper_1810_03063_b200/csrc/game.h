@@ -13,6 +13,9 @@
 
 namespace egt {
 
+// private hands per game the gradient kernel handles (256 threads x 5 positions)
+constexpr int EGT_MAX_HANDS = 1280;
+
 enum NodeKind { ND_DECISION = 0, ND_CHANCE = 1, ND_TERMINAL = 2 };
 enum TermKind { T_FOLD_P1 = 0, T_FOLD_P2 = 1, T_SHOWDOWN = 2 };
 
@@ -42,6 +45,9 @@ struct PlayerLayout {
     std::vector<std::string> seq_hist;  // [n_pub], "" for row 0
     std::vector<int> seq_owner;    // decision node owning the sequence (-1 for row 0)
     std::vector<int> term_off, term_idx;  // terminals grouped by this player's last sequence
+    std::vector<int> rows_term;           // sequences that end at least one terminal
+    std::vector<int> lvl_off, lvl_nodes;  // decision nodes grouped by level
+    std::vector<int> kid_off, kids;       // child decision nodes of each sequence
     int depth = 0;
 };
 
@@ -54,17 +60,31 @@ struct Terminal {
 };
 
 // Card-removal / strength-order tables of one (game, board state).
+// Positions 0..nvalid-1 are the valid hands in ascending showdown strength; positions
+// nvalid..H-1 hold the hands blocked by the board (their gradient entries are 0).
+// Per card c, the valid hands holding c form a segment [seg[c], seg[c+1]) of the card
+// array, in strength order (<= 64 long); entry e packs (ENT_* below): the hand's
+// position, which of the hand's cards c is (slot), and the number of segment entries
+// strictly weaker than the hand's tie group (relo) / not stronger (rehi).
 struct BoardTable {
     int nvalid = 0;
-    std::vector<int16_t> order;  // sorted position -> hand
-    std::vector<int16_t> lo, hi; // per position: tie-group bounds [lo, hi)
-    std::vector<int16_t> src;    // expanded card array entry -> sorted position
-    std::vector<int16_t> pos4;   // per position, per card k<2: elo, ehi, est, een (8 per position)
-    std::vector<uint8_t> valid;  // per hand
+    std::vector<int16_t> order;  // [H_pad] position -> hand
+    std::vector<int16_t> lo, hi; // [H_pad] per position: tie-group bounds [lo, hi)
+    std::vector<uint32_t> lohi;  // [H_pad] lo | hi << 16
+    std::vector<int16_t> seg;    // [n_cards + 1]
+    std::vector<uint32_t> ent;   // [2 * H_pad]
+    std::vector<uint8_t> valid;  // [H_pad] per hand
 };
+#define ENT_POS(e) ((int)((e) & 0xFFFu))
+#define ENT_SLOT(e) ((int)(((e) >> 12) & 1u))
+#define ENT_RELO(e) ((int)(((e) >> 13) & 0x7Fu))
+#define ENT_REHI(e) ((int)(((e) >> 20) & 0x7Fu))
+#define ENT_PACK(pos, slot, relo, rehi) \
+    ((uint32_t)(pos) | ((uint32_t)(slot) << 12) | ((uint32_t)(relo) << 13) | ((uint32_t)(rehi) << 20))
 
 struct HostGame {
     int kind = 0, n_games = 0;
+    int all_valid = 1;  // every hand valid at every board state
     int H = 0, H_pad = 0, hand_size = 1, n_cards = 0, n_combos = 0;
     int n_ranks = 13, n_suits = 4;
     PublicTree tree;

@@ -11,79 +11,66 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "game.h"  // ENT_* packing of the card-array entries
 
 namespace egt {
 
-// ------------------------------------------------------------------ block scan
-// Exclusive scan of data[0, n) in shared memory, in place; returns the total.
-// Deterministic (fixed association order).  Contains __syncthreads().
-template <int NT>
-__device__ double block_exscan(double* data, int n, double* wtot) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    constexpr int NW = NT / 32;
-    const int per = (n + NT - 1) / NT;
-    const int beg = min(tid * per, n), end = min(beg + per, n);
-    double s = 0.0;
-    for (int i = beg; i < end; ++i) s += data[i];
-    double incl = s;
+// ------------------------------------------------------------------ warp helpers
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        double v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+        const double u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
     }
-    if (lane == 31) wtot[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        double t = lane < NW ? wtot[lane] : 0.0;
-        double it = t;
+    return v;
+}
+
+// exclusive prefix at index r in [0, 64] of a 64-entry segment held as (ex0 at lane r,
+// ex1 at lane r - 32); r = 64 gives the total.  Every lane must call it.
+__device__ __forceinline__ double seg_prefix(double ex0, double ex1, double tot, int r) {
+    const double u = __shfl_sync(0xffffffffu, ex0, r & 31);
+    const double v = __shfl_sync(0xffffffffu, ex1, r & 31);
+    return r < 32 ? u : (r < 64 ? v : tot);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            double v = __shfl_up_sync(0xffffffffu, it, o);
-            if (lane >= o) it += v;
-        }
-        if (lane < NW) wtot[lane] = it - t;
-        if (lane == NW - 1) wtot[NW] = it;
-    }
-    __syncthreads();
-    double run = wtot[wid] + (incl - s);
-    for (int i = beg; i < end; ++i) {
-        double v = data[i];
-        data[i] = run;
-        run += v;
-    }
-    double total = wtot[NW];
-    __syncthreads();
-    return total;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
 
 // ------------------------------------------------------------------ gradient
-// One CTA per (output public sequence s, game g).  For every terminal t whose last
-// sequence of `player` is s (hands of the player: "self"; of the other: "opp"):
-//   w[i]      = prior_opp(h_i) * v_opp[seq_opp(t), h_i]   (opp hands in strength order)
-//   fold:     v(h) = u2 * sum_{opp hands h' disjoint from h} w(h')
-//                  = u2 * (T - sum_{c in h} S_c + [|h| = 2] w(h))      (inclusion-exclusion)
+// One CTA per (public sequence s of `player` that ends a terminal, game g).  For every
+// terminal t whose last `player` sequence is s (hands of `player`: "self", of the other
+// player: "opp"), with hands in ascending showdown strength (positions i):
+//   w[i] = prior_opp(h_i) * v_opp[seq_opp(t), h_i],  P = exclusive prefix sums of w,
+//   for every card c: the entries of w over the hands holding c, in strength order, and
+//   their exclusive prefix sums Pc; S_c their total.
+//   fold:     v(h) = u2 * sum_{opp h' disjoint from h} w(h') = T - sum_{c in h} S_c + [|h|=2] w(h)
 //   showdown: v(h) = sign * W * (stronger(h) - weaker(h)) over disjoint opp hands, with
-//                  weaker(h) = P[lo] - sum_{c in h} Pc[lo],  stronger = (T - P[hi]) - sum_c (S_c - Pc[hi])
-//             P: prefix sums in strength order; Pc: prefix sums over the hands holding card c
-//             (segments of the expanded card array E).  sign = +1 for player 0 (A y: player 2
-//             wins with the stronger hand), -1 for player 1 (A^T x).
+//             weaker   = P[lo] - sum_c Pc[lo],  stronger = (T - P[hi]) - sum_c (S_c - Pc[hi])
+//             ([lo, hi) = h's tie group), i.e.  v = T - P[hi] - P[lo] + sum_c (Pc[lo] + Pc[hi] - S_c).
 //   g[s, h] += kappa_t * kappa_game * prior_self(h) * v(h)
-template <int NT>
-__global__ void __launch_bounds__(NT) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
-                                                  const int* __restrict__ mask, int want) {
+// sign = +1 for player 0 (A y: player 2 wins with the stronger hand), -1 for player 1.
+// P is a block scan over register-resident chunks (K consecutive positions per thread);
+// the card sums are one warp per card (segments <= 64 entries, two per lane).
+template <int NT, int KMAX>
+__global__ void __launch_bounds__(NT, 4) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
+                                                  const int* __restrict__ mask, int want, int all_rows) {
     extern __shared__ double sm[];
-    __shared__ double wtot[NT / 32 + 1];
-    const int s = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
+    __shared__ double wtot[NT / 32];
+    constexpr int NW = NT / 32;
+    const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
+    const int s = all_rows ? (int)blockIdx.x : P.rows_term[blockIdx.x];
     const int Hp = G.H_pad, hs = G.hand_size;
-    double* w = sm;
-    double* Pf = w + Hp;
-    double* E = Pf + Hp + 1;
-    double* acc = E + 2 * Hp + 2;
+    double* w = sm;                // [Hp]   by position
+    double* Pf = w + Hp;           // [Hp+1] by position
+    double* corr = Pf + Hp + 1;    // [2][Hp] by position
+    double* acc = corr + 2 * Hp;   // [Hp]   by hand
     for (int i = tid; i < Hp; i += NT) acc[i] = 0.0;
     const int t0 = P.term_off[s], t1 = P.term_off[s + 1];
-    const double* __restrict__ pself = G.prior[player] + (size_t)g * Hp;
-    const double* __restrict__ popp = G.prior[1 - player] + (size_t)g * Hp;
+    const double* __restrict__ popp = (player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp;
     const double* __restrict__ vo = vin.at(g);
     const double kg = G.kappa_game[g];
     const double sd_sign = player == 0 ? 1.0 : -1.0;
@@ -92,234 +79,278 @@ __global__ void __launch_bounds__(NT) grad_kernel(DevGame G, DevPlayer P, int pl
         const int k = g * G.n_bs + T.bs;
         const int nv = G.tab_nvalid[k];
         const int16_t* __restrict__ order = G.tab_order + (size_t)k * Hp;
-        const int16_t* __restrict__ lo = G.tab_lo + (size_t)k * Hp;
-        const int16_t* __restrict__ hi = G.tab_hi + (size_t)k * Hp;
-        const int4* __restrict__ pos = G.tab_pos + (size_t)k * Hp;
-        const int16_t* __restrict__ src = G.tab_src + (size_t)k * (2 * Hp + 2);
-        const int so = T.seq[1 - player];
-        __syncthreads();  // previous terminal finished with w / Pf / E / acc
-        for (int i = tid; i < nv; i += NT) {
-            const int h = order[i];
-            const double yv = so ? vo[(size_t)so * Hp + h] : 1.0;
-            const double wv = popp[h] * yv;
-            w[i] = wv;
-            Pf[i] = wv;
-        }
-        __syncthreads();
-        const int ne = nv * hs;
-        for (int e = tid; e < ne; e += NT) E[e] = w[src[e]];
-        __syncthreads();
-        const double Ttot = block_exscan<NT>(Pf, nv, wtot);
-        const double Etot = block_exscan<NT>(E, ne, wtot);
-        if (tid == 0) {
-            Pf[nv] = Ttot;
-            E[ne] = Etot;
-        }
-        __syncthreads();
-        const double scale = T.kappa * kg * T.amount;
-        for (int i = tid; i < nv; i += NT) {
-            const int h = order[i];
-            const int4 pr = pos[i];
-            const int16_t* pd = reinterpret_cast<const int16_t*>(&pr);
-            double v;
-            if (T.kind == 2) {
-                double weaker = Pf[lo[i]];
-                double stronger = Ttot - Pf[hi[i]];
-                for (int c = 0; c < hs; ++c) {
-                    const double est = E[pd[c * 4 + 2]];
-                    weaker -= E[pd[c * 4 + 0]] - est;
-                    stronger -= E[pd[c * 4 + 3]] - E[pd[c * 4 + 1]];
-                }
-                v = sd_sign * (stronger - weaker);
-            } else {
-                double comp = Ttot;
-                for (int c = 0; c < hs; ++c) comp -= E[pd[c * 4 + 3]] - E[pd[c * 4 + 2]];
-                if (hs == 2) comp += w[i];
-                v = comp;
+        const uint32_t* __restrict__ lohi = G.tab_lohi + (size_t)k * Hp;
+        const int16_t* __restrict__ seg = G.tab_seg + (size_t)k * (G.n_cards + 1);
+        const uint32_t* __restrict__ ent = G.tab_ent + (size_t)k * 2 * Hp;
+        const int so = player ? T.seq[0] : T.seq[1];
+        const double* __restrict__ vrow = vo + (size_t)so * Hp;
+        const int K = (nv + NT - 1) / NT;
+        const int base = tid * K;
+        // ---- phase A: w in registers (K consecutive positions per thread), block exclusive scan
+        double x[KMAX];
+        double run = 0.0;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            x[j] = 0.0;
+            const int i = base + j;
+            if (j < K && i < nv) {
+                const int h = order[i];
+                x[j] = popp[h] * (so ? vrow[h] : 1.0);
+                w[i] = x[j];
+                run += x[j];
             }
-            acc[h] += scale * pself[h] * v;
+        }
+        __syncthreads();  // previous terminal done with Pf / corr; acc writes ordered
+        const double incl = warp_incl_scan(run, lane);
+        if (lane == 31) wtot[wid] = incl;
+        __syncthreads();
+        double wpre = 0.0, total = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+            const double v = wtot[q];
+            wpre += q < wid ? v : 0.0;
+            total += v;
+        }
+        double pre = wpre + incl - run;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            const int i = base + j;
+            if (j < K && i < nv) {
+                Pf[i] = pre;
+                pre += x[j];
+            }
+        }
+        if (tid == 0) Pf[nv] = total;
+        __syncthreads();
+        // ---- phase B: per-card sums, one warp per card
+        const bool sd = T.kind == 2;
+        for (int c = wid; c < G.n_cards; c += NW) {
+            const int a = seg[c], len = seg[c + 1] - a;
+            if (len == 0) continue;
+            const uint32_t e0 = lane < len ? ent[a + lane] : 0u;
+            const uint32_t e1 = lane + 32 < len ? ent[a + lane + 32] : 0u;
+            const double x0 = lane < len ? w[ENT_POS(e0)] : 0.0;
+            const double x1 = lane + 32 < len ? w[ENT_POS(e1)] : 0.0;
+            const double s0 = warp_incl_scan(x0, lane);
+            const double s1 = warp_incl_scan(x1, lane);
+            const double tot0 = __shfl_sync(0xffffffffu, s0, 31);
+            const double Sc = tot0 + __shfl_sync(0xffffffffu, s1, 31);
+            const double ex0 = s0 - x0, ex1 = tot0 + s1 - x1;
+            // lanes beyond len hold 0, so index len gives the total
+            double d0 = -Sc, d1 = -Sc;
+            if (sd) {
+                d0 += seg_prefix(ex0, ex1, Sc, ENT_RELO(e0)) + seg_prefix(ex0, ex1, Sc, ENT_REHI(e0));
+                d1 += seg_prefix(ex0, ex1, Sc, ENT_RELO(e1)) + seg_prefix(ex0, ex1, Sc, ENT_REHI(e1));
+            }
+            if (lane < len) corr[ENT_SLOT(e0) * Hp + ENT_POS(e0)] = d0;
+            if (lane + 32 < len) corr[ENT_SLOT(e1) * Hp + ENT_POS(e1)] = d1;
+        }
+        __syncthreads();
+        // ---- phase C: per hand
+        const double scale = T.kappa * kg * T.amount;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            const int i = base + j;
+            if (j < K && i < nv) {
+                double v = total + corr[i];
+                if (hs == 2) v += corr[Hp + i];
+                if (sd) {
+                    const uint32_t lh = lohi[i];
+                    v = sd_sign * (v - Pf[lh & 0xFFFFu] - Pf[lh >> 16]);
+                } else if (hs == 2) {
+                    v += x[j];
+                }
+                acc[order[i]] += scale * v;
+            }
         }
     }
     __syncthreads();
+    const double* __restrict__ pself = (player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
     double* __restrict__ out = gout.at(g) + (size_t)s * Hp;
-    for (int i = tid; i < Hp; i += NT) out[i] = acc[i];
+    for (int i = tid; i < Hp; i += NT) out[i] = pself[i] * acc[i];
 }
 
-static constexpr int GRAD_NT = 256;
+static constexpr int GRAD_NT = 256, GRAD_KMAX = 5;
+
+static size_t grad_smem_bytes(int Hp) { return sizeof(double) * (size_t)(5 * Hp + 1); }
 
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
-                            const int* mask, int want, cudaStream_t st) {
-    const size_t smem = sizeof(double) * (size_t)(G.H_pad + (G.H_pad + 1) + (2 * G.H_pad + 2) + G.H_pad);
-    dim3 grid(P.n_pub, G.n_games);
-    grad_kernel<GRAD_NT><<<grid, GRAD_NT, smem, st>>>(G, P, player, vin, gout, mask, want);
+                            const int* mask, int want, int all_rows, cudaStream_t st) {
+    const int rows = all_rows ? P.n_pub : P.n_rows_term;
+    if (rows == 0) return cudaSuccess;
+    dim3 grid(rows, G.n_games);
+    grad_kernel<GRAD_NT, GRAD_KMAX><<<grid, GRAD_NT, grad_smem_bytes(G.H_pad), st>>>(G, P, player, vin, gout, mask,
+                                                                                    want, all_rows);
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ treeplex pass
-// One thread per private hand, HT hands per CTA; the gradient tile [n_pub][HT] is
-// staged in shared memory; the bottom-up pass overwrites each simplex's entries
-// with its behavioural strategy and adds the simplex value into the parent entry;
-// the top-down pass turns behavioural into sequence form in place.
-template <int HT>
-__global__ void __launch_bounds__(HT) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
+// CTA = (TH_HANDS hands, game); TH_WARPS warps.  The player's whole gradient tile
+// [n_pub][TH_HANDS] is staged in shared memory (lane = hand).  Bottom-up, level by level
+// (deepest first; nodes of a level are independent and spread over the warps), each
+// simplex j = (node m, hand) pulls the values of its child simplexes (D_j^i) into its
+// entries, solves its local problem (softmax / prox / argmin / regret
+// matching), overwrites its entries with the behavioural strategy and stores its value in
+// val[m].  Top-down (shallowest first) each entry becomes q_i = q_{p_j} * qbar_i in place,
+// and the requested outputs (behavioural, sequence form, EGT convex combinations, CFR
+// average) are written row by row (coalesced, 32 hands per row).
+static constexpr int TH_HANDS = 32, TH_WARPS = 8, TH_NT = TH_HANDS * TH_WARPS;
+
+size_t tree_smem_bytes(const DevPlayer& P) {
+    return sizeof(double) * (size_t)TH_HANDS * (P.n_pub + P.n_nodes) +
+           sizeof(int) * (size_t)(6 * P.n_nodes + P.n_pub + 1 + P.n_levels + 1);
+}
+
+__global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
     extern __shared__ double tile[];
-    __shared__ double red[HT / 32];
-    const int g = blockIdx.y, tid = threadIdx.x;
+    const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (A.mask && A.mask[g] != A.want) return;
-    const int Hp = G.H_pad;
-    const int h = blockIdx.x * HT + tid;
+    const int Hp = G.H_pad, n_pub = P.n_pub, n_nodes = P.n_nodes, n_lv = P.n_levels;
+    const int h = blockIdx.x * TH_HANDS + lane;
     const bool live = h < G.H;
-    const int n_pub = P.n_pub;
     const int mode = A.mode;
     const bool has_grad = mode == TM_SBR || mode == TM_PROX || mode == TM_BR || mode == TM_CFR;
-    double* col = tile + tid;  // column of this hand: col[s * HT]
+    double* val = tile + (size_t)n_pub * TH_HANDS;  // [n_nodes][TH_HANDS]
+    int* s_first = reinterpret_cast<int*>(val + (size_t)n_nodes * TH_HANDS);
+    int* s_nact = s_first + n_nodes;
+    int* s_par = s_nact + n_nodes;
+    int* s_bs = s_par + n_nodes;
+    int* s_lvn = s_bs + n_nodes;       // [n_nodes]
+    int* s_kidoff = s_lvn + n_nodes;   // [n_pub+1]
+    int* s_kids = s_kidoff + n_pub + 1; // [n_nodes]
+    int* s_lvoff = s_kids + n_nodes;   // [n_lv+1]
+    for (int i = tid; i < n_nodes; i += TH_NT) {
+        s_first[i] = P.node_first[i];
+        s_nact[i] = P.node_nact[i];
+        s_par[i] = P.node_parent[i];
+        s_bs[i] = P.node_bs[i];
+        s_lvn[i] = P.lvl_nodes[i];
+        s_kids[i] = P.kids[i];
+    }
+    for (int i = tid; i <= n_pub; i += TH_NT) s_kidoff[i] = P.kid_off[i];
+    for (int i = tid; i <= n_lv; i += TH_NT) s_lvoff[i] = P.lvl_off[i];
     const uint8_t* __restrict__ valid_g = G.tab_valid + (size_t)g * G.n_bs * Hp;
+    const bool all_valid = G.all_valid != 0;
 
-    // ---- load
+    // ---- load the gradient tile (one 32-hand row per warp instruction)
     if (has_grad) {
         const double* __restrict__ gp = A.g.at(g);
         double sc = A.gsign;
         if (mode == TM_PROX) sc *= A.mu[g];
-        for (int s = 0; s < n_pub; ++s) col[s * HT] = live ? sc * gp[(size_t)s * Hp + h] : 0.0;
+        for (int r = wid; r < n_pub; r += TH_WARPS)
+            tile[r * TH_HANDS + lane] = live ? sc * gp[(size_t)r * Hp + h] : 0.0;
     }
+    __syncthreads();
 
-    // ---- bottom-up
+    // ---- bottom-up, deepest level first
     const double mu = (mode == TM_SBR) ? A.mu[g] : 1.0;
     double* __restrict__ cz = A.center.ok() ? A.center.at(g) : nullptr;
     double* __restrict__ rg = A.regret.ok() ? A.regret.at(g) : nullptr;
-    if (live && mode != TM_UNIFORM && mode != TM_COMBINE) {
-        for (int m = P.n_nodes - 1; m >= 0; --m) {
-            const int first = P.node_first[m], n = P.node_nact[m], par = P.node_parent[m];
-            if (!valid_g[(size_t)P.node_bs[m] * Hp + h]) {
-                for (int a = 0; a < n; ++a) col[(first + a) * HT] = 0.0;
-                continue;
+    if (has_grad) {
+        for (int L = n_lv - 1; L >= 0; --L) {
+            for (int idx = s_lvoff[L] + wid; idx < s_lvoff[L + 1]; idx += TH_WARPS) {
+                const int m = s_lvn[idx];
+                const int first = s_first[m], n = s_nact[m];
+                double* col = tile + (size_t)first * TH_HANDS + lane;
+                const bool ok = live && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
+                if (!ok) {
+                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] = 0.0;
+                    val[m * TH_HANDS + lane] = 0.0;
+                    continue;
+                }
+                // pull the child simplexes' values into this simplex's entries (D_j^i)
+                for (int a = 0; a < n; ++a) {
+                    const int s = first + a;
+                    double x = col[a * TH_HANDS];
+                    for (int c = s_kidoff[s]; c < s_kidoff[s + 1]; ++c) x += val[s_kids[c] * TH_HANDS + lane];
+                    col[a * TH_HANDS] = x;
+                }
+                double value;
+                if (mode == TM_SBR) {
+                    // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
+                    // i* = argmax qbar, w = mu beta_j
+                    const double wgt = mu * P.beta[(size_t)m * Hp + h];
+                    double mn = DBL_MAX;
+                    for (int a = 0; a < n; ++a) mn = fmin(mn, col[a * TH_HANDS]);
+                    double S = 0.0;
+                    for (int a = 0; a < n; ++a) {
+                        const double e = exp(-(col[a * TH_HANDS] - mn) / wgt);
+                        col[a * TH_HANDS] = e;
+                        S += e;
+                    }
+                    const double inv = 1.0 / S;
+                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
+                    value = mn - wgt * log(S) + wgt * log((double)n);
+                } else if (mode == TM_PROX) {
+                    // shifted-gradient SBR in multiplicative form:
+                    // qbar_i ~ zbar_i exp(-g_i / beta), value = -beta log sum_i zbar_i exp(-g_i / beta)
+                    const double beta = P.beta[(size_t)m * Hp + h];
+                    const double* __restrict__ zr = cz + (size_t)first * Hp + h;
+                    double mn = DBL_MAX;
+                    for (int a = 0; a < n; ++a)
+                        if (zr[(size_t)a * Hp] > 0.0) mn = fmin(mn, col[a * TH_HANDS]);
+                    double S = 0.0;
+                    for (int a = 0; a < n; ++a) {
+                        const double za = zr[(size_t)a * Hp];
+                        const double e = za > 0.0 ? za * exp(-(col[a * TH_HANDS] - mn) / beta) : 0.0;
+                        col[a * TH_HANDS] = e;
+                        S += e;
+                    }
+                    const double inv = 1.0 / S;
+                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
+                    value = mn - beta * log(S);
+                } else if (mode == TM_BR) {
+                    int best = 0;
+                    double mn = col[0];
+                    for (int a = 1; a < n; ++a) {
+                        const double v = col[a * TH_HANDS];
+                        if (v < mn) {
+                            mn = v;
+                            best = a;
+                        }
+                    }
+                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] = a == best ? 1.0 : 0.0;
+                    value = mn;
+                } else {  // TM_CFR: utility u = gsign * g, current strategy z, regrets r
+                    double v = 0.0;
+                    for (int a = 0; a < n; ++a) v += col[a * TH_HANDS] * cz[(size_t)(first + a) * Hp + h];
+                    double S = 0.0;
+                    for (int a = 0; a < n; ++a) {
+                        const size_t ix = (size_t)(first + a) * Hp + h;
+                        const double u = col[a * TH_HANDS], r0 = rg[ix];
+                        double r = r0 + u - v;
+                        if (A.cfr_plus) r = fmax(r, 0.0);
+                        rg[ix] = r;
+                        // DESIGN.md R15: regrets at the rounding-noise level of their own update count as 0
+                        const double tol = 1e-13 * (fabs(r0) + fabs(u) + fabs(v));
+                        const double pr = r > tol ? r : 0.0;
+                        col[a * TH_HANDS] = pr;
+                        S += pr;
+                    }
+                    for (int a = 0; a < n; ++a) {
+                        const double z = S > 0.0 ? col[a * TH_HANDS] / S : 1.0 / n;
+                        col[a * TH_HANDS] = z;
+                        cz[(size_t)(first + a) * Hp + h] = z;
+                    }
+                    value = v;
+                }
+                val[m * TH_HANDS + lane] = value;
             }
-            if (mode == TM_SBR) {
-                const double wgt = mu * P.beta[(size_t)m * Hp + h];
-                double mn = DBL_MAX;
-                for (int a = 0; a < n; ++a) mn = fmin(mn, col[(first + a) * HT]);
-                double S = 0.0;
-                for (int a = 0; a < n; ++a) {
-                    const double e = exp(-(col[(first + a) * HT] - mn) / wgt);
-                    col[(first + a) * HT] = e;
-                    S += e;
-                }
-                const double inv = 1.0 / S;
-                for (int a = 0; a < n; ++a) col[(first + a) * HT] *= inv;
-                // value = g_{i*} + w log qbar_{i*} + w log n, i* = argmax qbar
-                col[par * HT] += mn - wgt * log(S) + wgt * log((double)n);
-            } else if (mode == TM_PROX) {
-                // multiplicative form of the shifted-gradient SBR:
-                // qbar_i ~ zbar_i exp(-H_i / beta), U = -beta log sum_i zbar_i exp(-H_i / beta)
-                const double beta = P.beta[(size_t)m * Hp + h];
-                double mn = DBL_MAX;
-                for (int a = 0; a < n; ++a)
-                    if (cz[(size_t)(first + a) * Hp + h] > 0.0) mn = fmin(mn, col[(first + a) * HT]);
-                double S = 0.0;
-                for (int a = 0; a < n; ++a) {
-                    const double z = cz[(size_t)(first + a) * Hp + h];
-                    const double e = z > 0.0 ? z * exp(-(col[(first + a) * HT] - mn) / beta) : 0.0;
-                    col[(first + a) * HT] = e;
-                    S += e;
-                }
-                const double inv = 1.0 / S;
-                for (int a = 0; a < n; ++a) col[(first + a) * HT] *= inv;
-                col[par * HT] += mn - beta * log(S);
-            } else if (mode == TM_BR) {
-                int best = 0;
-                double mn = col[first * HT];
-                for (int a = 1; a < n; ++a) {
-                    const double v = col[(first + a) * HT];
-                    if (v < mn) { mn = v; best = a; }
-                }
-                for (int a = 0; a < n; ++a) col[(first + a) * HT] = a == best ? 1.0 : 0.0;
-                col[par * HT] += mn;
-            } else {  // TM_CFR: utility u = gsign * g, current strategy z, regrets r
-                double val = 0.0;
-                for (int a = 0; a < n; ++a) val += col[(first + a) * HT] * cz[(size_t)(first + a) * Hp + h];
-                double S = 0.0;
-                for (int a = 0; a < n; ++a) {
-                    const size_t idx = (size_t)(first + a) * Hp + h;
-                    const double u = col[(first + a) * HT], r0 = rg[idx];
-                    double r = r0 + u - val;
-                    if (A.cfr_plus) r = fmax(r, 0.0);
-                    rg[idx] = r;
-                    // DESIGN.md R15: regrets at the rounding-noise level of their own update count as 0
-                    const double tol = 1e-13 * (fabs(r0) + fabs(u) + fabs(val));
-                    const double pr = r > tol ? r : 0.0;
-                    col[(first + a) * HT] = pr;
-                    S += pr;
-                }
-                for (int a = 0; a < n; ++a) {
-                    const double z = S > 0.0 ? col[(first + a) * HT] / S : 1.0 / n;
-                    col[(first + a) * HT] = z;
-                    cz[(size_t)(first + a) * Hp + h] = z;
-                }
-                col[par * HT] += val;
-            }
-        }
-    }
-    const double myval = live ? col[0] : 0.0;
-
-    // ---- top-down
-    const bool want_td = A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR;
-    if (want_td) {
-        double* __restrict__ ob = A.out_b.ok() ? A.out_b.at(g) : nullptr;
-        double* __restrict__ oq = A.out_q.ok() ? A.out_q.at(g) : nullptr;
-        const double* __restrict__ ci = A.comb_in.ok() ? A.comb_in.at(g) : nullptr;
-        double* __restrict__ co = A.comb_out.ok() ? A.comb_out.at(g) : nullptr;
-        double* __restrict__ av = A.avg.ok() ? A.avg.at(g) : nullptr;
-        const double tau = A.tau ? A.tau[g] : 0.0;
-        double alpha = 0.0;
-        if (av) {
-            const double t = (double)A.iter[g];
-            alpha = A.avg_linear ? 2.0 * t / (t * t + t) : 1.0 / t;
-        }
-        const double* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
-        col[0] = live ? 1.0 : 0.0;
-        if (h < Hp) {
-            const double q0 = live ? 1.0 : 0.0;
-            if (ob) ob[h] = q0;
-            if (oq) oq[h] = q0;
-            if (co) co[h] = live ? (1.0 - tau) * ci[h] + tau : 0.0;
-            if (av) av[h] = q0;
-        }
-        for (int m = 0; m < P.n_nodes; ++m) {
-            const int first = P.node_first[m], n = P.node_nact[m], par = P.node_parent[m];
-            const bool ok = live && valid_g[(size_t)P.node_bs[m] * Hp + h];
-            const double qp = col[par * HT];
-            for (int a = 0; a < n; ++a) {
-                const int s = first + a;
-                double b;
-                if (!ok) b = 0.0;
-                else if (mode == TM_UNIFORM) b = 1.0 / n;
-                else if (mode == TM_COMBINE) b = bin[(size_t)s * Hp + h];
-                else b = col[s * HT];
-                const double q = qp * b;
-                col[s * HT] = q;
-                if (h < Hp) {
-                    const size_t idx = (size_t)s * Hp + h;
-                    if (ob) ob[idx] = b;
-                    if (oq) oq[idx] = q;
-                    if (co) co[idx] = (1.0 - tau) * ci[idx] + tau * q;
-                    if (av) av[idx] = alpha * q + (1.0 - alpha) * av[idx];
-                }
-            }
+            __syncthreads();
         }
     }
 
-    // ---- per-game value: deterministic block sum, then the last CTA sums the tiles in order
+    // ---- per-game value: root entry + root simplexes' values, deterministic reductions
     if (A.value) {
-        double v = myval;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if ((tid & 31) == 0) red[tid >> 5] = v;
-        __syncthreads();
+        double v = 0.0;
+        if (wid == 0 && live) {
+            v = tile[lane];
+            for (int c = s_kidoff[0]; c < s_kidoff[1]; ++c) v += val[s_kids[c] * TH_HANDS + lane];
+        }
+        v = warp_sum(v);
         __shared__ bool last;
         if (tid == 0) {
-            double b = 0.0;
-            for (int i = 0; i < HT / 32; ++i) b += red[i];
-            A.partial[(size_t)g * gridDim.x + blockIdx.x] = b;
+            A.partial[(size_t)g * gridDim.x + blockIdx.x] = v;
             __threadfence();
             const unsigned ticket = atomicAdd(&A.counter[g], 1u);
             last = ticket == gridDim.x - 1;
@@ -334,42 +365,69 @@ __global__ void __launch_bounds__(HT) tree_kernel(DevGame G, DevPlayer P, int pl
             A.counter[g] = 0;
         }
     }
-}
 
-template <int HT>
-static cudaError_t launch_tree_ht(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A,
-                                  cudaStream_t st) {
-    const size_t smem = sizeof(double) * (size_t)P.n_pub * HT;
-    dim3 grid((G.H + HT - 1) / HT, G.n_games);
-    tree_kernel<HT><<<grid, HT, smem, st>>>(G, P, player, A);
-    return cudaGetLastError();
-}
-
-int tree_tile_width(const DevGame& G, const DevPlayer& P) {
-    const size_t per_hand = sizeof(double) * (size_t)P.n_pub;
-    if (G.H >= 128 && per_hand * 128 <= 64 * 1024) return 128;
-    if (G.H >= 64 && per_hand * 64 <= 64 * 1024) return 64;
-    return 32;
-}
-
-cudaError_t tree_prepare(int max_n_pub) {
-    (void)max_n_pub;
-    cudaError_t e = cudaSuccess;
-    e = cudaFuncSetAttribute(grad_kernel<GRAD_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tree_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tree_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(tree_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    // ---- top-down, shallowest level first
+    const bool want_td = A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR;
+    if (!want_td) return;
+    double* __restrict__ ob = A.out_b.ok() ? A.out_b.at(g) : nullptr;
+    double* __restrict__ oq = A.out_q.ok() ? A.out_q.at(g) : nullptr;
+    const double* __restrict__ ci = A.comb_in.ok() ? A.comb_in.at(g) : nullptr;
+    double* __restrict__ co = A.comb_out.ok() ? A.comb_out.at(g) : nullptr;
+    double* __restrict__ av = A.avg.ok() ? A.avg.at(g) : nullptr;
+    const double tau = A.tau ? A.tau[g] : 0.0;
+    double alpha = 0.0;
+    if (av) {
+        const double t = (double)A.iter[g];
+        alpha = A.avg_linear ? 2.0 * t / (t * t + t) : 1.0 / t;
+    }
+    const double* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
+    const bool hvalid = h < Hp;
+    if (wid == 0 && hvalid) {
+        const double q0 = live ? 1.0 : 0.0;
+        if (ob) ob[h] = q0;
+        if (oq) oq[h] = q0;
+        if (co) co[h] = live ? (1.0 - tau) * ci[h] + tau : 0.0;
+        if (av) av[h] = q0;
+    }
+    for (int L = 0; L < n_lv; ++L) {
+        for (int idx = s_lvoff[L] + wid; idx < s_lvoff[L + 1]; idx += TH_WARPS) {
+            const int m = s_lvn[idx];
+            const int first = s_first[m], n = s_nact[m], par = s_par[m];
+            const bool ok = live && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
+            const double qp = par == 0 ? (live ? 1.0 : 0.0) : tile[par * TH_HANDS + lane];
+            for (int a = 0; a < n; ++a) {
+                const int s = first + a;
+                double b;
+                if (!ok) b = 0.0;
+                else if (mode == TM_UNIFORM) b = 1.0 / n;
+                else if (mode == TM_COMBINE) b = bin[(size_t)s * Hp + h];
+                else b = tile[s * TH_HANDS + lane];
+                const double q = qp * b;
+                tile[s * TH_HANDS + lane] = q;
+                if (hvalid) {
+                    const size_t ix = (size_t)s * Hp + h;
+                    if (ob) ob[ix] = b;
+                    if (oq) oq[ix] = q;
+                    if (co) co[ix] = (1.0 - tau) * ci[ix] + tau * q;
+                    if (av) av[ix] = alpha * q + (1.0 - alpha) * av[ix];
+                }
+            }
+        }
+        __syncthreads();
+    }
 }
 
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st) {
-    switch (tree_tile_width(G, P)) {
-        case 128: return launch_tree_ht<128>(G, P, player, A, st);
-        case 64: return launch_tree_ht<64>(G, P, player, A, st);
-        default: return launch_tree_ht<32>(G, P, player, A, st);
-    }
+    dim3 grid((G.H_pad + TH_HANDS - 1) / TH_HANDS, G.n_games);
+    tree_kernel<<<grid, TH_NT, tree_smem_bytes(P), st>>>(G, P, player, A);
+    return cudaGetLastError();
+}
+
+cudaError_t kernels_prepare() {
+    cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 // ------------------------------------------------------------------ per-game scalars

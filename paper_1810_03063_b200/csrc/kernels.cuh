@@ -31,13 +31,13 @@ struct DevTerm {
 };
 
 struct DevGame {
-    int n_games, H, H_pad, hand_size, n_bs;
+    int n_games, H, H_pad, hand_size, n_bs, n_cards;
+    int all_valid;            // 1: every hand is valid at every board state (river endgames)
     const int* tab_nvalid;    // [G*n_bs]
-    const int16_t* tab_order; // [G*n_bs][H_pad]
-    const int16_t* tab_lo;    // [G*n_bs][H_pad]
-    const int16_t* tab_hi;    // [G*n_bs][H_pad]
-    const int4* tab_pos;      // [G*n_bs][H_pad] : 8 x int16 (elo, ehi, est, een) x 2 cards
-    const int16_t* tab_src;   // [G*n_bs][2*H_pad+2]
+    const int16_t* tab_order; // [G*n_bs][H_pad]   position -> hand (valid hands first, strength order)
+    const uint32_t* tab_lohi; // [G*n_bs][H_pad]   tie group [lo, hi) of each position
+    const int16_t* tab_seg;   // [G*n_bs][n_cards+1] card segments of the card array
+    const uint32_t* tab_ent;  // [G*n_bs][2*H_pad] card-array entries (ENT_* packing, game.h)
     const uint8_t* tab_valid; // [G*n_bs][H_pad]
     const double* prior[2];   // [G][H_pad]
     const double* kappa_game; // [G]
@@ -45,14 +45,20 @@ struct DevGame {
 };
 
 struct DevPlayer {
-    int n_pub, n_nodes;
+    int n_pub, n_nodes, n_levels, max_level_width;
+    int n_rows_term;         // public sequences that end at least one terminal
     const int* node_first;   // [n_nodes], top-down order
     const int* node_nact;
     const int* node_parent;  // parent public sequence (0 = empty)
     const int* node_bs;
+    const int* lvl_off;      // [n_levels+1] nodes grouped by level (treeplex depth b_Q^j)
+    const int* lvl_nodes;    // [n_nodes]
+    const int* kid_off;      // [n_pub+1] child nodes of each sequence (D_j^i)
+    const int* kids;         // [n_nodes]
     const double* beta;      // [n_nodes][H_pad]
     const int* term_off;     // [n_pub+1] terminals grouped by this player's last sequence
     const int* term_idx;
+    const int* rows_term;    // [n_rows_term]
 };
 
 enum TreeMode { TM_SBR = 0, TM_PROX = 1, TM_BR = 2, TM_CFR = 3, TM_UNIFORM = 4, TM_COMBINE = 5 };
@@ -95,11 +101,13 @@ struct DevScalars {
 };
 
 // Launchers (return cudaGetLastError()).
+// all_rows = 1 writes every row of gout (rows without terminals get 0); 0 writes only the
+// rows that end a terminal (the solver's gradient buffers are zeroed once at allocation).
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
-                            const int* mask, int want, cudaStream_t st);
+                            const int* mask, int want, int all_rows, cudaStream_t st);
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st);
-int tree_tile_width(const DevGame& G, const DevPlayer& P);
-cudaError_t tree_prepare(int max_n_pub);
+cudaError_t kernels_prepare();
+size_t tree_smem_bytes(const DevPlayer& P);
 
 cudaError_t launch_egt_prepare(int variant, int n_games, DevScalars S, cudaStream_t st);
 cudaError_t launch_egt_accept(int variant, int n_games, DevScalars S, cudaStream_t st);
