@@ -307,24 +307,25 @@ def run_b200(args):
     torch.cuda.synchronize()
     launches_per_step = sum(v[1] for v in kt.values()) / args.timing_steps
     step_ms_eager = sum(v[0] for v in kt.values()) / args.timing_steps
-    dom = max(kt, key=lambda k: kt[k][0])
+    tot_ms = sum(v[0] for v in kt.values())
+    grad_ms = kt["grad_Ay"][0] + kt["grad_ATx"][0]
     peak, peak_src = measured_peak()
-    roof = None
-    if dom.startswith("grad"):
-        p = 0 if dom == "grad_Ay" else 1
-        per_game = grad_bytes_per_game(game, p)
-        ms_k, nl, active = kt[dom]
-        achieved = per_game * active / (ms_k / 1e3) / 1e9
-        tr = ncu_traffic(dom, args.workload)
-        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None if tr is None else tr * active / nl,
-                "peak_source": peak_src, "algorithmic_bytes_per_launch": per_game * active / nl,
-                "avg_launch_ms": ms_k / nl, "share_of_step": ms_k / sum(v[0] for v in kt.values())}
+    if grad_ms >= kt["tree"][0]:
+        # the gradient kernel (both players' launches): algorithmic bytes / event-timed duration
+        nl = kt["grad_Ay"][1] + kt["grad_ATx"][1]
+        byts = grad_bytes_per_game(game, 0) * kt["grad_Ay"][2] + grad_bytes_per_game(game, 1) * kt["grad_ATx"][2]
+        achieved = byts / (grad_ms / 1e3) / 1e9
+        tr = ncu_traffic("grad", args.workload)
+        active = kt["grad_Ay"][2] + kt["grad_ATx"][2]
+        roof = {"bound": "hbm", "kernel": "grad_kernel (A y and A^T x)", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None if tr is None else tr * active / nl,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": byts / nl,
+                "avg_launch_ms": grad_ms / nl, "share_of_step": grad_ms / tot_ms}
     else:
-        ms_k, nl, active = kt[dom]
-        roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
-                "traffic": None, "peak_source": peak_src, "avg_launch_ms": ms_k / nl,
-                "share_of_step": ms_k / sum(v[0] for v in kt.values())}
+        ms_k, nl, active = kt["tree"]
+        roof = {"bound": "hbm", "kernel": "tree_kernel", "achieved": None, "peak": peak, "unit": "GB/s",
+                "frac": None, "traffic": None, "peak_source": peak_src, "avg_launch_ms": ms_k / nl,
+                "share_of_step": ms_k / tot_ms}
     kernel_split = {k: {"ms_per_step": v[0] / args.timing_steps, "launches_per_step": v[1] / args.timing_steps}
                     for k, v in kt.items()}
 

@@ -160,26 +160,28 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     }
     // tables
     std::vector<int> nvalid;
-    std::vector<int16_t> order, seg;
-    std::vector<uint32_t> lohi, ent;
+    std::vector<int16_t> order;
+    std::vector<uint16_t> cent;
+    std::vector<uint32_t> lohi, pcard;
     std::vector<uint8_t> valid;
     for (const BoardTable& tb : H.tables) {
         nvalid.push_back(tb.nvalid);
         order.insert(order.end(), tb.order.begin(), tb.order.end());
         lohi.insert(lohi.end(), tb.lohi.begin(), tb.lohi.end());
-        seg.insert(seg.end(), tb.seg.begin(), tb.seg.end());
-        ent.insert(ent.end(), tb.ent.begin(), tb.ent.end());
+        cent.insert(cent.end(), tb.cent.begin(), tb.cent.end());
+        pcard.insert(pcard.end(), tb.pcard.begin(), tb.pcard.end());
         valid.insert(valid.end(), tb.valid.begin(), tb.valid.end());
     }
     int* d_nvalid;
-    int16_t *d_order, *d_seg;
-    uint32_t *d_lohi, *d_ent;
+    int16_t* d_order;
+    uint16_t* d_cent;
+    uint32_t *d_lohi, *d_pcard;
     uint8_t* d_valid;
     TRY(upload(G, &d_nvalid, nvalid));
     TRY(upload(G, &d_order, order));
     TRY(upload(G, &d_lohi, lohi));
-    TRY(upload(G, &d_seg, seg));
-    TRY(upload(G, &d_ent, ent));
+    TRY(upload(G, &d_cent, cent));
+    TRY(upload(G, &d_pcard, pcard));
     TRY(upload(G, &d_valid, valid));
     double *d_p0, *d_p1, *d_kg;
     TRY(upload(G, &d_p0, H.prior[0]));
@@ -208,8 +210,13 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     G->dg.tab_nvalid = d_nvalid;
     G->dg.tab_order = d_order;
     G->dg.tab_lohi = d_lohi;
-    G->dg.tab_seg = d_seg;
-    G->dg.tab_ent = d_ent;
+    G->dg.tab_cent = d_cent;
+    G->dg.tab_pcard = reinterpret_cast<const uint2*>(d_pcard);
+    G->dg.n_ce = CE_SLOTS(Hp, H.n_cards);
+    G->dg.ident = 1;
+    for (const BoardTable& tb : H.tables)
+        for (int i = 0; i < H.H; ++i)
+            if (tb.order[i] != i) G->dg.ident = 0;
     G->dg.tab_valid = d_valid;
     G->dg.prior[0] = d_p0;
     G->dg.prior[1] = d_p1;
@@ -224,7 +231,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         P.n_rows_term = (int)L.rows_term.size();
         P.max_level_width = 0;
         for (int l = 0; l < P.n_levels; ++l) P.max_level_width = std::max(P.max_level_width, L.lvl_off[l + 1] - L.lvl_off[l]);
-        int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt;
+        int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt, *co;
         double* be;
         TRY(upload(G, &a, L.first));
         TRY(upload(G, &b, L.nact));
@@ -238,6 +245,9 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         TRY(upload(G, &ko, L.kid_off));
         TRY(upload(G, &kd, L.kids));
         TRY(upload(G, &rt, L.rows_term));
+        TRY(upload(G, &co, L.chunk_off));
+        P.n_chunks = (int)L.chunk_off.size() - 1;
+        P.chunk_off = co;
         P.node_first = a;
         P.node_nact = b;
         P.node_parent = c;

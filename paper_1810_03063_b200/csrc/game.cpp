@@ -290,6 +290,15 @@ static void build_layout(HostGame& G) {
         L.rows_term.clear();
         for (int s = 0; s < L.n_pub; ++s)
             if (L.term_off[s + 1] > L.term_off[s]) L.rows_term.push_back(s);
+        L.chunk_off.assign(1, 0);
+        for (int r = 0, n = 0; r < (int)L.rows_term.size(); ++r) {
+            const int s = L.rows_term[r];
+            n += L.term_off[s + 1] - L.term_off[s];
+            if (n >= GRAD_CHUNK_TERMS || r + 1 == (int)L.rows_term.size()) {
+                L.chunk_off.push_back(r + 1);
+                n = 0;
+            }
+        }
         const int nn = (int)L.first.size();
         L.lvl_off.assign(L.depth + 1, 0);
         L.lvl_nodes.clear();
@@ -369,30 +378,29 @@ static void build_table(const HostGame& G, int g, int bs, const std::vector<int>
         }
         i = j;
     }
-    // card segments: for each card, the sorted positions of the valid hands holding it
+    // card array: for each card, the sorted positions of the valid hands holding it + an end slot
     std::vector<std::vector<int>> by_card(G.n_cards);
-    std::vector<std::vector<int>> slot_of(G.n_cards);
     for (int i = 0; i < nv; ++i) {
         const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
-        for (int k = 0; k < hs; ++k) {
-            by_card[hc[k]].push_back(i);
-            slot_of[hc[k]].push_back(k);
-        }
+        for (int k = 0; k < hs; ++k) by_card[hc[k]].push_back(i);
     }
-    tb.seg.assign(G.n_cards + 1, 0);
-    tb.ent.assign(2 * (size_t)Hp, 0);
+    tb.cent.assign(CE_SLOTS((size_t)Hp, G.n_cards), (uint16_t)CE_END);
+    tb.pcard.assign(2 * (size_t)Hp, 0);
     int ne = 0;
     for (int c = 0; c < G.n_cards; ++c) {
-        tb.seg[c] = (int16_t)ne;
         const std::vector<int>& L = by_card[c];
-        for (size_t j = 0; j < L.size(); ++j) {
+        const int start = ne, len = (int)L.size();
+        for (int j = 0; j < len; ++j) {
             const int i = L[j];
+            tb.cent[ne++] = (uint16_t)(i | (j == 0 ? CE_FIRST : 0u));
             const int relo = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.lo[i]) - L.begin());
             const int rehi = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.hi[i]) - L.begin());
-            tb.ent[ne++] = ENT_PACK(i, slot_of[c][j], relo, rehi);
+            const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
+            const int k = (hs == 2 && hc[1] == c) ? 1 : 0;
+            tb.pcard[2 * (size_t)i + k] = PC_PACK(start, relo, rehi, len);
         }
+        tb.cent[ne++] = (uint16_t)(CE_END | (len == 0 ? CE_FIRST : 0u));
     }
-    tb.seg[G.n_cards] = (int16_t)ne;
 }
 
 std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
@@ -446,7 +454,7 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
     }
     G.H_pad = (G.H + 31) / 32 * 32;
     if (G.H > EGT_MAX_HANDS) return "too many private hands for the gradient kernel";
-    if (G.n_cards - 5 - 1 > 64 && G.kind == EGT_GAME_RIVER) return "deck too large (card segments > 64)";
+    if (G.n_cards - 5 - 1 > 63 && G.kind == EGT_GAME_RIVER) return "deck too large (card segments > 63)";
     build_layout(G);
     const int Gn = G.n_games, H = G.H, Hp = G.H_pad;
 

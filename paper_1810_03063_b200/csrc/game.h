@@ -15,6 +15,8 @@ namespace egt {
 
 // private hands per game the gradient kernel handles (256 threads x 5 positions)
 constexpr int EGT_MAX_HANDS = 1280;
+// terminals per CTA of the staged river gradient kernel (rows are never split)
+constexpr int GRAD_CHUNK_TERMS = 32;
 
 enum NodeKind { ND_DECISION = 0, ND_CHANCE = 1, ND_TERMINAL = 2 };
 enum TermKind { T_FOLD_P1 = 0, T_FOLD_P2 = 1, T_SHOWDOWN = 2 };
@@ -46,6 +48,7 @@ struct PlayerLayout {
     std::vector<int> seq_owner;    // decision node owning the sequence (-1 for row 0)
     std::vector<int> term_off, term_idx;  // terminals grouped by this player's last sequence
     std::vector<int> rows_term;           // sequences that end at least one terminal
+    std::vector<int> chunk_off;           // rows_term split into chunks of ~GRAD_CHUNK_TERMS terminals
     std::vector<int> lvl_off, lvl_nodes;  // decision nodes grouped by level
     std::vector<int> kid_off, kids;       // child decision nodes of each sequence
     int depth = 0;
@@ -62,25 +65,31 @@ struct Terminal {
 // Card-removal / strength-order tables of one (game, board state).
 // Positions 0..nvalid-1 are the valid hands in ascending showdown strength; positions
 // nvalid..H-1 hold the hands blocked by the board (their gradient entries are 0).
-// Per card c, the valid hands holding c form a segment [seg[c], seg[c+1]) of the card
-// array, in strength order (<= 64 long); entry e packs (ENT_* below): the hand's
-// position, which of the hand's cards c is (slot), and the number of segment entries
-// strictly weaker than the hand's tie group (relo) / not stronger (rehi).
+// Card array: for every card c, the valid hands holding c in strength order (a segment
+// of <= 64 entries), followed by one end slot; an entry is the hand's position
+// (CE_END for the end slot) with CE_FIRST on the first slot of each segment, so the
+// segmented exclusive scan of the card array leaves the segment total in the end slot.
+// Per position and card slot k (the hand's k-th card), pcard packs the card's segment
+// start in the card array, the segment indices of the hand's tie group [relo, rehi)
+// and the segment length (PC_* below).
 struct BoardTable {
     int nvalid = 0;
     std::vector<int16_t> order;  // [H_pad] position -> hand
     std::vector<int16_t> lo, hi; // [H_pad] per position: tie-group bounds [lo, hi)
     std::vector<uint32_t> lohi;  // [H_pad] lo | hi << 16
-    std::vector<int16_t> seg;    // [n_cards + 1]
-    std::vector<uint32_t> ent;   // [2 * H_pad]
+    std::vector<uint16_t> cent;  // [CE_SLOTS(H_pad, n_cards)] card array
+    std::vector<uint32_t> pcard; // [H_pad][2]
     std::vector<uint8_t> valid;  // [H_pad] per hand
 };
-#define ENT_POS(e) ((int)((e) & 0xFFFu))
-#define ENT_SLOT(e) ((int)(((e) >> 12) & 1u))
-#define ENT_RELO(e) ((int)(((e) >> 13) & 0x7Fu))
-#define ENT_REHI(e) ((int)(((e) >> 20) & 0x7Fu))
-#define ENT_PACK(pos, slot, relo, rehi) \
-    ((uint32_t)(pos) | ((uint32_t)(slot) << 12) | ((uint32_t)(relo) << 13) | ((uint32_t)(rehi) << 20))
+#define CE_END 0x0FFFu
+#define CE_FIRST 0x1000u
+#define CE_SLOTS(Hp, n_cards) ((2 * (Hp) + (n_cards) + 7) / 8 * 8)  // 16-byte multiple
+#define PC_START(v) ((int)((v) & 0xFFFu))
+#define PC_RELO(v) ((int)(((v) >> 12) & 0x3Fu))
+#define PC_REHI(v) ((int)(((v) >> 18) & 0x7Fu))
+#define PC_LEN(v) ((int)(((v) >> 25) & 0x7Fu))
+#define PC_PACK(start, relo, rehi, len) \
+    ((uint32_t)(start) | ((uint32_t)(relo) << 12) | ((uint32_t)(rehi) << 18) | ((uint32_t)(len) << 25))
 
 struct HostGame {
     int kind = 0, n_games = 0;

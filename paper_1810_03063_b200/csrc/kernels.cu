@@ -11,7 +11,7 @@
 #include <cmath>
 
 #include "kernels.cuh"
-#include "game.h"  // ENT_* packing of the card-array entries
+#include "game.h"  // CE_* / PC_* packing of the card tables
 
 namespace egt {
 
@@ -25,14 +25,6 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
     return v;
 }
 
-// exclusive prefix at index r in [0, 64] of a 64-entry segment held as (ex0 at lane r,
-// ex1 at lane r - 32); r = 64 gives the total.  Every lane must call it.
-__device__ __forceinline__ double seg_prefix(double ex0, double ex1, double tot, int r) {
-    const double u = __shfl_sync(0xffffffffu, ex0, r & 31);
-    const double v = __shfl_sync(0xffffffffu, ex1, r & 31);
-    return r < 32 ? u : (r < 64 ? v : tot);
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -42,68 +34,119 @@ __device__ __forceinline__ double warp_sum(double v) {
 // ------------------------------------------------------------------ gradient
 // One CTA per (public sequence s of `player` that ends a terminal, game g).  For every
 // terminal t whose last `player` sequence is s (hands of `player`: "self", of the other
-// player: "opp"), with hands in ascending showdown strength (positions i):
-//   w[i] = prior_opp(h_i) * v_opp[seq_opp(t), h_i],  P = exclusive prefix sums of w,
-//   for every card c: the entries of w over the hands holding c, in strength order, and
-//   their exclusive prefix sums Pc; S_c their total.
-//   fold:     v(h) = u2 * sum_{opp h' disjoint from h} w(h') = T - sum_{c in h} S_c + [|h|=2] w(h)
-//   showdown: v(h) = sign * W * (stronger(h) - weaker(h)) over disjoint opp hands, with
+// player: "opp"), with the hands in ascending showdown strength (positions i):
+//   w[i] = prior_opp(h_i) * v_opp[seq_opp(t), h_i],  P = exclusive prefix sums of w, T = sum w,
+//   for every card c: Pc = exclusive prefix sums of w over the hands holding c (in strength
+//   order, the card array's segment of c), S_c = their total.
+//   fold:     v(h) = sum_{opp h' disjoint from h} w(h') = T - sum_{c in h} S_c + [|h|=2] w(h)
+//   showdown: v(h) = sign * (stronger(h) - weaker(h)) over disjoint opp hands, with
 //             weaker   = P[lo] - sum_c Pc[lo],  stronger = (T - P[hi]) - sum_c (S_c - Pc[hi])
 //             ([lo, hi) = h's tie group), i.e.  v = T - P[hi] - P[lo] + sum_c (Pc[lo] + Pc[hi] - S_c).
-//   g[s, h] += kappa_t * kappa_game * prior_self(h) * v(h)
+//   g[s, h] += kappa_t * kappa_game * amount_t * prior_self(h) * v(h)
 // sign = +1 for player 0 (A y: player 2 wins with the stronger hand), -1 for player 1.
-// P is a block scan over register-resident chunks (K consecutive positions per thread);
-// the card sums are one warp per card (segments <= 64 entries, two per lane).
-template <int NT, int KMAX>
-__global__ void __launch_bounds__(NT, 4) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
-                                                  const int* __restrict__ mask, int want, int all_rows) {
+// P: block scan over register-resident chunks of K consecutive positions per thread.
+// Pc: one segmented block scan over the card array (EPT consecutive slots per thread,
+// reset at each segment's first slot); each segment's end slot receives its total S_c.
+// Hands that do not share their tie group read their own P / Pc from registers.
+template <int NT, int KMAX, int EMAX>
+__global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
+                                                     const int* __restrict__ mask, int want, int all_rows) {
     extern __shared__ double sm[];
-    __shared__ double wtot[NT / 32];
     constexpr int NW = NT / 32;
+    __shared__ double wtot[NW];
+    __shared__ double segv[NW];
+    __shared__ int segf[NW];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
     const int s = all_rows ? (int)blockIdx.x : P.rows_term[blockIdx.x];
-    const int Hp = G.H_pad, hs = G.hand_size;
-    double* w = sm;                // [Hp]   by position
-    double* Pf = w + Hp;           // [Hp+1] by position
-    double* corr = Pf + Hp + 1;    // [2][Hp] by position
-    double* acc = corr + 2 * Hp;   // [Hp]   by hand
-    for (int i = tid; i < Hp; i += NT) acc[i] = 0.0;
+    const int Hp = G.H_pad, hs = G.hand_size, H = G.H, n_ce = G.n_ce;
+    const bool fast = G.ident && G.all_valid;  // positions are hands and every hand is valid
+    double* w = sm;               // [Hp]   by position
+    double* Pf = w + Hp;          // [Hp+1] by position
+    double* Ex = Pf + Hp + 1;     // [n_ce] card array
+    double* acc = Ex + n_ce;      // [Hp]   by hand (general path only)
+    if (!fast)
+        for (int i = tid; i < Hp; i += NT) acc[i] = 0.0;
+    double racc[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) racc[j] = 0.0;
     const int t0 = P.term_off[s], t1 = P.term_off[s + 1];
     const double* __restrict__ popp = (player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp;
     const double* __restrict__ vo = vin.at(g);
     const double kg = G.kappa_game[g];
     const double sd_sign = player == 0 ? 1.0 : -1.0;
+    const int EPT = (n_ce + NT - 1) / NT;
+    const int ebase = tid * EPT;
     for (int ti = t0; ti < t1; ++ti) {
         const DevTerm T = G.terms[P.term_idx[ti]];
         const int k = g * G.n_bs + T.bs;
         const int nv = G.tab_nvalid[k];
         const int16_t* __restrict__ order = G.tab_order + (size_t)k * Hp;
         const uint32_t* __restrict__ lohi = G.tab_lohi + (size_t)k * Hp;
-        const int16_t* __restrict__ seg = G.tab_seg + (size_t)k * (G.n_cards + 1);
-        const uint32_t* __restrict__ ent = G.tab_ent + (size_t)k * 2 * Hp;
+        const uint16_t* __restrict__ cent = G.tab_cent + (size_t)k * n_ce;
+        const uint2* __restrict__ pcard = G.tab_pcard + (size_t)k * Hp;
         const int so = player ? T.seq[0] : T.seq[1];
         const double* __restrict__ vrow = vo + (size_t)so * Hp;
+        const bool sd = T.kind == 2;
         const int K = (nv + NT - 1) / NT;
         const int base = tid * K;
-        // ---- phase A: w in registers (K consecutive positions per thread), block exclusive scan
+        __syncthreads();  // the previous terminal is done with w / Pf / Ex
+        // ---- phase A: w (coalesced), then per-thread chunks of K positions, block scan
+        for (int i = tid; i < nv; i += NT) {
+            const int h = fast ? i : order[i];
+            w[i] = popp[h] * (so ? vrow[h] : 1.0);
+        }
+        __syncthreads();
         double x[KMAX];
         double run = 0.0;
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
-            x[j] = 0.0;
             const int i = base + j;
-            if (j < K && i < nv) {
-                const int h = order[i];
-                x[j] = popp[h] * (so ? vrow[h] : 1.0);
-                w[i] = x[j];
-                run += x[j];
-            }
+            x[j] = (j < K && i < nv) ? w[i] : 0.0;
+            run += x[j];
         }
-        __syncthreads();  // previous terminal done with Pf / corr; acc writes ordered
         const double incl = warp_incl_scan(run, lane);
         if (lane == 31) wtot[wid] = incl;
+        // ---- phase B (local part): card-array chunk, segmented scan inside the thread
+        double ex[EMAX];
+        double srun = 0.0;
+        bool sflag = false;
+        int first_flag = EMAX;
+        unsigned endmask = 0u;
+#pragma unroll
+        for (int j = 0; j < EMAX; ++j) {
+            const int e = ebase + j;
+            const bool in = j < EPT && e < n_ce;
+            const unsigned c = in ? cent[e] : CE_END;
+            if (in && (c & CE_FIRST)) {
+                srun = 0.0;
+                if (!sflag) first_flag = j;
+                sflag = true;
+            }
+            const unsigned pos = c & CE_END;
+            if (pos == CE_END) endmask |= 1u << j;
+            const double y = pos != CE_END ? w[pos] : 0.0;
+            ex[j] = srun;
+            srun += y;
+        }
+        // segmented inclusive scan of (srun, sflag) over the warp
+        double sv = srun;
+        int sf = sflag;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double uv = __shfl_up_sync(0xffffffffu, sv, o);
+            const int uf = __shfl_up_sync(0xffffffffu, sf, o);
+            if (lane >= o) {
+                if (!sf) sv += uv;
+                sf |= uf;
+            }
+        }
+        if (lane == 31) {
+            segv[wid] = sv;
+            segf[wid] = sf;
+        }
         __syncthreads();
+        // block prefix of P
         double wpre = 0.0, total = 0.0;
 #pragma unroll
         for (int q = 0; q < NW; ++q) {
@@ -111,76 +154,386 @@ __global__ void __launch_bounds__(NT, 4) grad_kernel(DevGame G, DevPlayer P, int
             wpre += q < wid ? v : 0.0;
             total += v;
         }
-        double pre = wpre + incl - run;
+        const double pbase = wpre + incl - run;
+        if (sd) {
+            double p = pbase;
 #pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            const int i = base + j;
-            if (j < K && i < nv) {
-                Pf[i] = pre;
-                pre += x[j];
+            for (int j = 0; j < KMAX; ++j) {
+                const int i = base + j;
+                if (j < K && i < nv) Pf[i] = p;
+                p += x[j];
+            }
+            if (tid == 0) Pf[nv] = total;
+        }
+        // carry into this thread's first segment: segmented exclusive prefix over threads
+        {
+            double carry = 0.0;
+            for (int q = 0; q < wid; ++q) carry = segf[q] ? segv[q] : carry + segv[q];
+            const double pv = __shfl_up_sync(0xffffffffu, sv, 1);
+            const int pf = __shfl_up_sync(0xffffffffu, sf, 1);
+            if (lane > 0) carry = pf ? pv : carry + pv;
+#pragma unroll
+            for (int j = 0; j < EMAX; ++j) {
+                const int e = ebase + j;
+                if (j < EPT && e < n_ce) {
+                    const double v = j < first_flag ? carry + ex[j] : ex[j];
+                    if (sd || ((endmask >> j) & 1u)) Ex[e] = v;
+                }
             }
         }
-        if (tid == 0) Pf[nv] = total;
         __syncthreads();
-        // ---- phase B: per-card sums, one warp per card
-        const bool sd = T.kind == 2;
-        for (int c = wid; c < G.n_cards; c += NW) {
-            const int a = seg[c], len = seg[c + 1] - a;
-            if (len == 0) continue;
-            const uint32_t e0 = lane < len ? ent[a + lane] : 0u;
-            const uint32_t e1 = lane + 32 < len ? ent[a + lane + 32] : 0u;
-            const double x0 = lane < len ? w[ENT_POS(e0)] : 0.0;
-            const double x1 = lane + 32 < len ? w[ENT_POS(e1)] : 0.0;
-            const double s0 = warp_incl_scan(x0, lane);
-            const double s1 = warp_incl_scan(x1, lane);
-            const double tot0 = __shfl_sync(0xffffffffu, s0, 31);
-            const double Sc = tot0 + __shfl_sync(0xffffffffu, s1, 31);
-            const double ex0 = s0 - x0, ex1 = tot0 + s1 - x1;
-            // lanes beyond len hold 0, so index len gives the total
-            double d0 = -Sc, d1 = -Sc;
-            if (sd) {
-                d0 += seg_prefix(ex0, ex1, Sc, ENT_RELO(e0)) + seg_prefix(ex0, ex1, Sc, ENT_REHI(e0));
-                d1 += seg_prefix(ex0, ex1, Sc, ENT_RELO(e1)) + seg_prefix(ex0, ex1, Sc, ENT_REHI(e1));
-            }
-            if (lane < len) corr[ENT_SLOT(e0) * Hp + ENT_POS(e0)] = d0;
-            if (lane + 32 < len) corr[ENT_SLOT(e1) * Hp + ENT_POS(e1)] = d1;
-        }
-        __syncthreads();
-        // ---- phase C: per hand
+        // ---- phase C: per position
         const double scale = T.kappa * kg * T.amount;
+        double pre = pbase;
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
             const int i = base + j;
             if (j < K && i < nv) {
-                double v = total + corr[i];
-                if (hs == 2) v += corr[Hp + i];
+                const uint2 pc = pcard[i];
+                double v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
+                if (hs == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
                 if (sd) {
                     const uint32_t lh = lohi[i];
-                    v = sd_sign * (v - Pf[lh & 0xFFFFu] - Pf[lh >> 16]);
+                    const int lo = lh & 0xFFFFu, hi = lh >> 16;
+                    if (lo == i && hi == i + 1) {
+                        // alone in its tie group: its own prefixes
+                        const double ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
+                        v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
+                        if (hs == 2) {
+                            const double cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
+                            v += cb + (cb + x[j]);
+                        }
+                    } else {
+                        v += -(Pf[lo] + Pf[hi]) + Ex[PC_START(pc.x) + PC_RELO(pc.x)] +
+                             Ex[PC_START(pc.x) + PC_REHI(pc.x)];
+                        if (hs == 2) v += Ex[PC_START(pc.y) + PC_RELO(pc.y)] + Ex[PC_START(pc.y) + PC_REHI(pc.y)];
+                    }
+                    v *= sd_sign;
                 } else if (hs == 2) {
                     v += x[j];
                 }
-                acc[order[i]] += scale * v;
+                if (fast) racc[j] += scale * v;
+                else acc[order[i]] += scale * v;
+            }
+            pre += x[j];
+        }
+    }
+    const double* __restrict__ pself = (player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
+    double* __restrict__ out = gout.at(g) + (size_t)s * Hp;
+    __syncthreads();
+    if (fast) {
+        const int K = (H + NT - 1) / NT;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            const int i = tid * K + j;
+            if (j < K && i < H) w[i] = racc[j];
+        }
+        __syncthreads();
+        for (int i = tid; i < Hp; i += NT) out[i] = i < H ? pself[i] * w[i] : 0.0;
+    } else {
+        for (int i = tid; i < Hp; i += NT) out[i] = pself[i] * acc[i];
+    }
+}
+
+// ------------------------------------------------------------------ staged river gradient
+// The same computation for games whose positions are the hands and where every hand is
+// valid (river endgames, Kuhn): one CTA per (chunk of sequences, game), persistent over
+// the chunk's terminals.  The game's tables and priors are staged in shared memory once
+// per CTA with bulk async copies (TMA engine, cp.async.bulk + mbarrier); each terminal's
+// opponent row is double-buffered -- the copy of terminal t+1's row overlaps terminal t.
+// Every global read is a bulk copy; each output row leaves in one bulk store.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int NT, int KMAX, int EMAX>
+__global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
+                                                            VecRef gout, const int* __restrict__ mask, int want) {
+    extern __shared__ __align__(16) double sm[];
+    constexpr int NW = NT / 32;
+    __shared__ double wtot[NW];
+    __shared__ double segv[NW];
+    __shared__ int segf[NW];
+    __shared__ __align__(8) uint64_t bar[3];
+    const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (mask && mask[g] != want) return;
+    const int Hp = G.H_pad, hs = G.hand_size, H = G.H, n_ce = G.n_ce;
+    double* popp = sm;                 // [Hp]
+    double* pself = popp + Hp;         // [Hp]
+    double* vb = pself + Hp;           // [2][Hp] opponent rows
+    double* w = vb + 2 * Hp;           // [Hp]
+    double* ob = w + Hp;               // [Hp] output row staging
+    double* Pf = ob + Hp;              // [Hp + 2]
+    double* Ex = Pf + Hp + 2;          // [n_ce]
+    uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [Hp]
+    uint32_t* lohi = reinterpret_cast<uint32_t*>(pcard + Hp);        // [Hp]
+    uint16_t* cent = reinterpret_cast<uint16_t*>(lohi + Hp);         // [n_ce]
+    const int r0 = P.chunk_off[blockIdx.x], r1 = P.chunk_off[blockIdx.x + 1];
+    const int T0 = P.term_off[P.rows_term[r0]], T1 = P.term_off[P.rows_term[r1 - 1] + 1];
+    const double* __restrict__ vo = vin.at(g);
+    double* __restrict__ outg = gout.at(g);
+    const int* __restrict__ tidx = P.term_idx;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto opp_seq = [&](int ti) {
+        const DevTerm& T = G.terms[tidx[ti]];
+        return player ? T.seq[0] : T.seq[1];
+    };
+    if (tid == 0) {
+        const unsigned bD = Hp * sizeof(double), bU2 = Hp * sizeof(uint2), bU = Hp * sizeof(uint32_t),
+                       bC = n_ce * sizeof(uint16_t);
+        mbar_expect_tx(&bar[0], 2 * bD + bU2 + bU + bC);
+        bulk_g2s(popp, (player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp, bD, &bar[0]);
+        bulk_g2s(pself, (player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp, bD, &bar[0]);
+        bulk_g2s(pcard, G.tab_pcard + (size_t)g * Hp, bU2, &bar[0]);
+        bulk_g2s(lohi, G.tab_lohi + (size_t)g * Hp, bU, &bar[0]);
+        bulk_g2s(cent, G.tab_cent + (size_t)g * n_ce, bC, &bar[0]);
+        for (int q = 0; q < 2 && T0 + q < T1; ++q) {
+            const int so = opp_seq(T0 + q);
+            if (so) {
+                mbar_expect_tx(&bar[1 + q], bD);
+                bulk_g2s(vb + q * Hp, vo + (size_t)so * Hp, bD, &bar[1 + q]);
             }
         }
     }
-    __syncthreads();
-    const double* __restrict__ pself = (player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
-    double* __restrict__ out = gout.at(g) + (size_t)s * Hp;
-    for (int i = tid; i < Hp; i += NT) out[i] = pself[i] * acc[i];
+    for (int i = H + tid; i < Hp; i += NT) ob[i] = 0.0;  // padding columns of every output row
+    const double kg = G.kappa_game[g];
+    const double sd_sign = player == 0 ? 1.0 : -1.0;
+    const int K = (H + NT - 1) / NT, base = tid * K;
+    const int EPT = (n_ce + NT - 1) / NT, ebase = tid * EPT;
+    double racc[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) racc[j] = 0.0;
+    unsigned par[2] = {0u, 0u};
+    mbar_wait(&bar[0], 0);
+    int r = r0;
+    for (int ti = T0; ti < T1; ++ti) {
+        const int q = (ti - T0) & 1;
+        const DevTerm T = G.terms[tidx[ti]];
+        const int so = player ? T.seq[0] : T.seq[1];
+        const bool sd = T.kind == 2;
+        // prefetch terminal ti+1's row into the other buffer (its last reader, terminal ti-1,
+        // finished phase A before the barriers of terminal ti-1)
+        if (tid == 0 && ti > T0 && ti + 1 < T1) {
+            const int so1 = opp_seq(ti + 1);
+            if (so1) {
+                fence_proxy_async();
+                mbar_expect_tx(&bar[1 + (q ^ 1)], Hp * sizeof(double));
+                bulk_g2s(vb + (q ^ 1) * Hp, vo + (size_t)so1 * Hp, Hp * sizeof(double), &bar[1 + (q ^ 1)]);
+            }
+        }
+        if (so) {
+            mbar_wait(&bar[1 + q], par[q]);
+            par[q] ^= 1u;
+        }
+        const double* vrow = vb + q * Hp;
+        // ---- phase A: w in chunks of K consecutive positions per thread
+        double x[KMAX];
+        double run = 0.0;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            const int i = base + j;
+            x[j] = 0.0;
+            if (j < K && i < H) {
+                x[j] = popp[i] * (so ? vrow[i] : 1.0);
+                w[i] = x[j];
+            }
+            run += x[j];
+        }
+        const double incl = warp_incl_scan(run, lane);
+        if (lane == 31) wtot[wid] = incl;
+        __syncthreads();
+        // ---- phase B: card-array chunk, segmented scan inside the thread, then over threads
+        double ex[EMAX];
+        double srun = 0.0;
+        bool sflag = false;
+        int first_flag = EMAX;
+        unsigned endmask = 0u;
+#pragma unroll
+        for (int j = 0; j < EMAX; ++j) {
+            const int e = ebase + j;
+            const bool in = j < EPT && e < n_ce;
+            const unsigned c = in ? cent[e] : CE_END;
+            if (in && (c & CE_FIRST)) {
+                srun = 0.0;
+                if (!sflag) first_flag = j;
+                sflag = true;
+            }
+            const unsigned pos = c & CE_END;
+            if (pos == CE_END) endmask |= 1u << j;
+            const double y = pos != CE_END ? w[pos] : 0.0;
+            ex[j] = srun;
+            srun += y;
+        }
+        double sv = srun;
+        int sf = sflag;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double uv = __shfl_up_sync(0xffffffffu, sv, o);
+            const int uf = __shfl_up_sync(0xffffffffu, sf, o);
+            if (lane >= o) {
+                if (!sf) sv += uv;
+                sf |= uf;
+            }
+        }
+        if (lane == 31) {
+            segv[wid] = sv;
+            segf[wid] = sf;
+        }
+        __syncthreads();
+        double wpre = 0.0, total = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < NW; ++qq) {
+            const double v = wtot[qq];
+            wpre += qq < wid ? v : 0.0;
+            total += v;
+        }
+        const double pbase = wpre + incl - run;
+        if (sd) {
+            double p = pbase;
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j) {
+                const int i = base + j;
+                if (j < K && i < H) Pf[i] = p;
+                p += x[j];
+            }
+            if (tid == 0) Pf[H] = total;
+        }
+        {
+            double carry = 0.0;
+            for (int qq = 0; qq < wid; ++qq) carry = segf[qq] ? segv[qq] : carry + segv[qq];
+            const double pv = __shfl_up_sync(0xffffffffu, sv, 1);
+            const int pf = __shfl_up_sync(0xffffffffu, sf, 1);
+            if (lane > 0) carry = pf ? pv : carry + pv;
+#pragma unroll
+            for (int j = 0; j < EMAX; ++j) {
+                const int e = ebase + j;
+                if (j < EPT && e < n_ce && (sd || ((endmask >> j) & 1u))) Ex[e] = j < first_flag ? carry + ex[j] : ex[j];
+            }
+        }
+        __syncthreads();
+        // ---- phase C
+        const double scale = T.kappa * kg * T.amount;
+        double pre = pbase;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            const int i = base + j;
+            if (j < K && i < H) {
+                const uint2 pc = pcard[i];
+                double v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
+                if (hs == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
+                if (sd) {
+                    const uint32_t lh = lohi[i];
+                    const int lo = lh & 0xFFFFu, hi = lh >> 16;
+                    if (lo == i && hi == i + 1) {
+                        const double ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
+                        v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
+                        if (hs == 2) {
+                            const double cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
+                            v += cb + (cb + x[j]);
+                        }
+                    } else {
+                        v += -(Pf[lo] + Pf[hi]) + Ex[PC_START(pc.x) + PC_RELO(pc.x)] +
+                             Ex[PC_START(pc.x) + PC_REHI(pc.x)];
+                        if (hs == 2) v += Ex[PC_START(pc.y) + PC_RELO(pc.y)] + Ex[PC_START(pc.y) + PC_REHI(pc.y)];
+                    }
+                    v *= sd_sign;
+                } else if (hs == 2) {
+                    v += x[j];
+                }
+                racc[j] += scale * v;
+            }
+            pre += x[j];
+        }
+        // ---- row end: stage prior_self * acc, one bulk store per row
+        const int srow = P.rows_term[r];
+        if (ti + 1 == P.term_off[srow + 1]) {
+            if (tid == 0) bulk_wait_read0();  // the previous row's store has left ob
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j) {
+                const int i = base + j;
+                if (j < K && i < H) ob[i] = pself[i] * racc[j];
+                racc[j] = 0.0;
+            }
+            fence_proxy_async();
+            __syncthreads();
+            if (tid == 0) bulk_s2g(outg + (size_t)srow * Hp, ob, Hp * sizeof(double));
+            ++r;
+        }
+    }
+    if (tid == 0) bulk_wait0();
 }
 
-static constexpr int GRAD_NT = 256, GRAD_KMAX = 5;
+static constexpr int GRAD_NT = 512, GRAD_KMAX = 3, GRAD_EMAX = 6;  // H <= 1536, card array <= 3072
 
-static size_t grad_smem_bytes(int Hp) { return sizeof(double) * (size_t)(5 * Hp + 1); }
+static size_t grad_smem_bytes(const DevGame& G) {
+    return sizeof(double) * (size_t)(3 * G.H_pad + 1 + G.n_ce);
+}
+
+static size_t grad_staged_smem_bytes(const DevGame& G) {
+    const size_t Hp = G.H_pad;
+    return sizeof(double) * (7 * Hp + 2 + G.n_ce) + sizeof(uint2) * Hp + sizeof(uint32_t) * Hp +
+           sizeof(uint16_t) * G.n_ce;
+}
+
+static bool staged_ok(const DevGame& G) { return G.ident && G.all_valid && G.n_bs == 1; }
 
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
                             const int* mask, int want, int all_rows, cudaStream_t st) {
     const int rows = all_rows ? P.n_pub : P.n_rows_term;
     if (rows == 0) return cudaSuccess;
+    if (staged_ok(G) && (!all_rows || gout.slot_sel == nullptr)) {
+        if (all_rows) {
+            // rows that end no terminal are 0; the staged kernel writes the others
+            for (int g = 0; g < G.n_games; ++g) {
+                cudaError_t e = cudaMemsetAsync(gout.base + (size_t)g * gout.game_stride, 0,
+                                                sizeof(double) * (size_t)P.n_pub * G.H_pad, st);
+                if (e != cudaSuccess) return e;
+            }
+        }
+        if (P.n_chunks == 0) return cudaSuccess;
+        dim3 grid(P.n_chunks, G.n_games);
+        grad_staged_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX>
+            <<<grid, GRAD_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want);
+        return cudaGetLastError();
+    }
     dim3 grid(rows, G.n_games);
-    grad_kernel<GRAD_NT, GRAD_KMAX><<<grid, GRAD_NT, grad_smem_bytes(G.H_pad), st>>>(G, P, player, vin, gout, mask,
-                                                                                    want, all_rows);
+    grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX><<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout,
+                                                                                         mask, want, all_rows);
     return cudaGetLastError();
 }
 
@@ -424,8 +777,11 @@ cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const 
 }
 
 cudaError_t kernels_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX>,
+    cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(grad_staged_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }

@@ -33,11 +33,13 @@ struct DevTerm {
 struct DevGame {
     int n_games, H, H_pad, hand_size, n_bs, n_cards;
     int all_valid;            // 1: every hand is valid at every board state (river endgames)
+    int ident;                // 1: position order = hand order at every board state (river endgames)
+    int n_ce;                 // card-array slots per table (CE_SLOTS)
     const int* tab_nvalid;    // [G*n_bs]
     const int16_t* tab_order; // [G*n_bs][H_pad]   position -> hand (valid hands first, strength order)
     const uint32_t* tab_lohi; // [G*n_bs][H_pad]   tie group [lo, hi) of each position
-    const int16_t* tab_seg;   // [G*n_bs][n_cards+1] card segments of the card array
-    const uint32_t* tab_ent;  // [G*n_bs][2*H_pad] card-array entries (ENT_* packing, game.h)
+    const uint16_t* tab_cent; // [G*n_bs][n_ce]      card array (CE_* packing, game.h)
+    const uint2* tab_pcard;   // [G*n_bs][H_pad]     per position, per card: segment info (PC_*)
     const uint8_t* tab_valid; // [G*n_bs][H_pad]
     const double* prior[2];   // [G][H_pad]
     const double* kappa_game; // [G]
@@ -59,6 +61,8 @@ struct DevPlayer {
     const int* term_off;     // [n_pub+1] terminals grouped by this player's last sequence
     const int* term_idx;
     const int* rows_term;    // [n_rows_term]
+    int n_chunks;
+    const int* chunk_off;    // [n_chunks+1] ranges of rows_term, one CTA each (staged gradient kernel)
 };
 
 enum TreeMode { TM_SBR = 0, TM_PROX = 1, TM_BR = 2, TM_CFR = 3, TM_UNIFORM = 4, TM_COMBINE = 5 };
