@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--timing-steps", type=int, default=3, help="steps of the per-kernel event-timing pass")
+    ap.add_argument("--converge-games", type=int, default=0,
+                    help="also time EGT/as and CFR+ to eps_sad <= --eps-mbb on this many endgames (0: skip)")
+    ap.add_argument("--eps-mbb", type=float, default=1.0, help="target saddle gap in milli-big-blinds")
+    ap.add_argument("--converge-max-steps", type=int, default=2000)
     return ap.parse_args()
 
 
@@ -67,6 +71,68 @@ def workload(args, rank):
     boards = W.random_boards(args.batch, seed)
     p1, p2 = W.random_priors(boards, seed)
     return spec, boards, p1, p2
+
+
+def max_over_ranks(x, world, device="cpu"):
+    """Max of a per-rank scalar over all ranks (the contract's max-over-ranks timing)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def throughput(games_per_rank, world, steps, ms):
+    """Whole-job gradient evaluations per second: every rank's games, every step."""
+    return GRADS_PER_STEP * games_per_rank * world * steps / (ms / 1e3)
+
+
+def time_to_gap(P, spec, boards, p1, p2, solver, eps_chips, max_steps, check_every=10):
+    """Wall time (CUDA events) for every game of the batch to reach eps_sad <= eps_chips:
+    graph-launched solver steps, eps_sad on the device after each step, read back every
+    `check_every` steps (sum of regrets in mbb; 1 mbb = big blind / 1000)."""
+    import torch
+    n = len(boards)
+    game = P.Game(P.RIVER, n_games=n, river=spec, boards=boards, prior1=p1, prior2=p2)
+    st = torch.cuda.current_stream()
+    game.set_stream(st)
+    gap = torch.zeros(n, dtype=torch.float64, device="cuda")
+    if solver == "egt_as":
+        game.egt_init(P.EGT_AS)
+        step = lambda: game.egt_step(1)  # noqa: E731
+        which = 0
+    else:
+        game.cfr_init(P.CFR_PLUS)
+        step = lambda: game.cfr_step(1)  # noqa: E731
+        which = 1
+    done_at = np.full(n, -1)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(st)
+    steps = 0
+    while steps < max_steps:
+        for _ in range(check_every):
+            step()
+            game.saddle_gap_device(which, gap)
+            steps += 1
+        g = gap.cpu().numpy()
+        newly = (done_at < 0) & (g <= eps_chips)
+        done_at[newly] = steps
+        if (done_at >= 0).all():
+            break
+    ev1.record(st)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    sc = game.egt_scalars()
+    game.close()
+    reached = done_at >= 0
+    return {"solver": solver, "games": n, "eps_chips": eps_chips, "reached": int(reached.sum()),
+            "steps_median": float(np.median(done_at[reached])) if reached.any() else None,
+            "steps_max": int(done_at.max()) if reached.all() else None, "steps_run": steps,
+            "seconds": ms / 1e3, "final_gap_median": float(np.median(g)),
+            "grad_evals_per_game": float(sc[0, 7])}
 
 
 def workload_config(args, game=None, world=1):
@@ -289,13 +355,8 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     ck = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    total_grads = GRADS_PER_STEP * args.batch * world * args.steps
-    value = total_grads / (ms / 1e3)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world, "cuda")
+    value = throughput(args.batch, world, args.steps, ms)
     gaps = gap.cpu().numpy()
 
     # per-kernel event timing (same kernels, eager launches, events on the library stream)
@@ -359,10 +420,7 @@ def run_b200(args):
             g2.saddle_gap(0, out=pinned)
         el = time.perf_counter() - t0
         grads_e2e = float(g2.egt_scalars()[0, 7])
-        te = torch.tensor([el], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        el = float(te.item())
+        el = max_over_ranks(el, world, "cuda")
         if rank == 0:
             line["e2e"] = {"value": grads_e2e * args.batch * world / el, "unit": UNIT,
                            "h2d_bytes_per_step": int(g2.h2d_bytes / args.steps),
@@ -371,6 +429,15 @@ def run_b200(args):
                                    "K x (egt_step + saddle_gap to pinned host); counts every gradient "
                                    "evaluation incl. init", "seconds": el}
         g2.close()
+
+    if args.converge_games > 0:
+        from paper_1810_03063_b200 import workloads as W
+        eps = args.eps_mbb * W.river_spec(args.workload)["big_blind"] / 1000.0
+        n = args.converge_games
+        conv = [time_to_gap(P, spec, boards[:n], p1[:n], p2[:n], sv, eps, args.converge_max_steps)
+                for sv in ("egt_as", "cfr_plus")]
+        if rank == 0:
+            line["time_to_gap"] = conv
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         grads, secs, iters = oracle_sample(args, boards, p1, p2)

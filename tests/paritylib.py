@@ -15,7 +15,10 @@ from paper_1810_03063_b200 import workloads
 class Pair:
     """Product game (batch) + one oracle sequence form per game."""
 
-    def __init__(self, kind, n_games=1, spec=None, seed=0, n_ranks=13, n_suits=4, build_sparse=True):
+    def __init__(self, kind, n_games=1, spec=None, seed=0, n_ranks=13, n_suits=4, build_sparse=True,
+                 sample=None, boards=None, priors=None):
+        """``sample``: games that get an oracle sequence form (default: all); ``boards`` /
+        ``priors`` override the seeded river inputs."""
         import paper_1810_03063_b200 as P
         self.kind = kind
         self.n_games = n_games
@@ -29,16 +32,21 @@ class Pair:
             self.sf = [sf] * n_games
         else:
             spec = spec or workloads.river_spec("tiny", pot=2, stack=6, raise_cap=2)
-            boards = workloads.random_boards(n_games, seed, n_ranks, n_suits)
-            p1, p2 = workloads.random_priors(boards, seed, n_ranks, n_suits)
+            if boards is None:
+                boards = workloads.random_boards(n_games, seed, n_ranks, n_suits)
+            if priors is None:
+                priors = workloads.random_priors(boards, seed, n_ranks, n_suits)
+            p1, p2 = priors
+            self.boards, self.priors = boards, (p1, p2)
             self.game = P.Game(P.RIVER, n_games=n_games, river=spec, boards=boards, prior1=p1, prior2=p2,
                                n_ranks=n_ranks, n_suits=n_suits)
             deck = Deck(n_ranks, n_suits)
             rp = river.RiverParams(**{k: spec[k] for k in ("pot", "stack", "fracs", "allin", "raise_cap",
                                                            "open_fold")})
-            self.sf = [river.RiverSeqForm(rp, deck, boards[g], workloads.prior_dict(p1[g], deck.n_cards),
-                                          workloads.prior_dict(p2[g], deck.n_cards), build_sparse=build_sparse)
-                       for g in range(n_games)]
+            games = range(n_games) if sample is None else sample
+            self.sf = {g: river.RiverSeqForm(rp, deck, boards[g], workloads.prior_dict(p1[g], deck.n_cards),
+                                             workloads.prior_dict(p2[g], deck.n_cards), build_sparse=build_sparse)
+                       for g in games}
         self._maps = {}
 
     def tp(self, g, p):
