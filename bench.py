@@ -52,10 +52,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--timing-steps", type=int, default=3, help="steps of the per-kernel event-timing pass")
-    ap.add_argument("--converge-games", type=int, default=0,
+    ap.add_argument("--converge-games", type=int, default=16,
                     help="also time EGT/as and CFR+ to eps_sad <= --eps-mbb on this many endgames (0: skip)")
     ap.add_argument("--eps-mbb", type=float, default=1.0, help="target saddle gap in milli-big-blinds")
-    ap.add_argument("--converge-max-steps", type=int, default=2000)
+    ap.add_argument("--converge-max-steps", type=int, default=4000)
     return ap.parse_args()
 
 
