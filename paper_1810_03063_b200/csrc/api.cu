@@ -212,7 +212,8 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     G->dg.tab_lohi = d_lohi;
     G->dg.tab_cent = d_cent;
     G->dg.tab_pcard = reinterpret_cast<const uint2*>(d_pcard);
-    G->dg.n_ce = CE_SLOTS(Hp, H.n_cards);
+    G->dg.n_ce = H.n_ce;
+    G->dg.seg_w = H.seg_w;
     G->dg.ident = 1;
     for (const BoardTable& tb : H.tables)
         for (int i = 0; i < H.H; ++i)

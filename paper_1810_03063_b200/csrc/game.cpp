@@ -384,22 +384,24 @@ static void build_table(const HostGame& G, int g, int bs, const std::vector<int>
         const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
         for (int k = 0; k < hs; ++k) by_card[hc[k]].push_back(i);
     }
-    tb.cent.assign(CE_SLOTS((size_t)Hp, G.n_cards), (uint16_t)CE_END);
+    // uniform segments: card c owns slots [c * seg_w, (c + 1) * seg_w); its hands first, then
+    // padding, the end slot last
+    const int W = G.seg_w;
+    tb.cent.assign((size_t)G.n_ce, (uint16_t)CE_END);
     tb.pcard.assign(2 * (size_t)Hp, 0);
-    int ne = 0;
     for (int c = 0; c < G.n_cards; ++c) {
         const std::vector<int>& L = by_card[c];
-        const int start = ne, len = (int)L.size();
+        const int start = c * W, len = (int)L.size();
         for (int j = 0; j < len; ++j) {
             const int i = L[j];
-            tb.cent[ne++] = (uint16_t)(i | (j == 0 ? CE_FIRST : 0u));
+            tb.cent[start + j] = (uint16_t)i;
             const int relo = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.lo[i]) - L.begin());
             const int rehi = (int)(std::lower_bound(L.begin(), L.end(), (int)tb.hi[i]) - L.begin());
             const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
             const int k = (hs == 2 && hc[1] == c) ? 1 : 0;
-            tb.pcard[2 * (size_t)i + k] = PC_PACK(start, relo, rehi, len);
+            tb.pcard[2 * (size_t)i + k] = PC_PACK(start, relo, rehi, W - 1);
         }
-        tb.cent[ne++] = (uint16_t)(CE_END | (len == 0 ? CE_FIRST : 0u));
+        tb.cent[start] |= (uint16_t)CE_FIRST;
     }
 }
 
@@ -454,6 +456,9 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
     }
     G.H_pad = (G.H + 31) / 32 * 32;
     if (G.H > EGT_MAX_HANDS) return "too many private hands for the gradient kernel";
+    // card segments: at most (n_cards - 6) valid river hands hold a card; one hand per card otherwise
+    G.seg_w = (G.hand_size == 2 ? G.n_cards - 6 : 1) + 1;
+    G.n_ce = (G.n_cards * G.seg_w + 7) / 8 * 8;
     if (G.n_cards - 5 - 1 > 63 && G.kind == EGT_GAME_RIVER) return "deck too large (card segments > 63)";
     build_layout(G);
     const int Gn = G.n_games, H = G.H, Hp = G.H_pad;

@@ -65,10 +65,11 @@ struct Terminal {
 // Card-removal / strength-order tables of one (game, board state).
 // Positions 0..nvalid-1 are the valid hands in ascending showdown strength; positions
 // nvalid..H-1 hold the hands blocked by the board (their gradient entries are 0).
-// Card array: for every card c, the valid hands holding c in strength order (a segment
-// of <= 64 entries), followed by one end slot; an entry is the hand's position
-// (CE_END for the end slot) with CE_FIRST on the first slot of each segment, so the
-// segmented exclusive scan of the card array leaves the segment total in the end slot.
+// Card array: card c owns the seg_w slots [c * seg_w, (c + 1) * seg_w): the valid hands
+// holding c in strength order (<= 63), then padding, then one end slot; a slot holds the
+// hand's position (CE_END for padding and the end slot), CE_FIRST marks slot 0 of every
+// segment, so the segmented exclusive scan of the card array leaves each segment's total
+// in its end slot.
 // Per position and card slot k (the hand's k-th card), pcard packs the card's segment
 // start in the card array, the segment indices of the hand's tie group [relo, rehi)
 // and the segment length (PC_* below).
@@ -83,7 +84,6 @@ struct BoardTable {
 };
 #define CE_END 0x0FFFu
 #define CE_FIRST 0x1000u
-#define CE_SLOTS(Hp, n_cards) ((2 * (Hp) + (n_cards) + 7) / 8 * 8)  // 16-byte multiple
 #define PC_START(v) ((int)((v) & 0xFFFu))
 #define PC_RELO(v) ((int)(((v) >> 12) & 0x3Fu))
 #define PC_REHI(v) ((int)(((v) >> 18) & 0x7Fu))
@@ -94,6 +94,7 @@ struct BoardTable {
 struct HostGame {
     int kind = 0, n_games = 0;
     int all_valid = 1;  // every hand valid at every board state
+    int seg_w = 0, n_ce = 0;  // card-array segment width (incl. end slot) and slots per table
     int H = 0, H_pad = 0, hand_size = 1, n_cards = 0, n_combos = 0;
     int n_ranks = 13, n_suits = 4;
     PublicTree tree;

@@ -25,6 +25,26 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
     return v;
 }
 
+// exp(x) for x <= 0 to ~1 ulp: x = (64 k + j) ln2 / 64 + r, |r| <= ln2 / 128,
+// exp(x) = 2^k' * tab[j] * (1 + r + ... + r^5/120) (truncation < 4e-17 relative).
+// tab[j] = 2^(j/64) lives in shared memory.  Returns 0 below exp's normal range.
+__device__ __forceinline__ double exp_nonpos(double x, const double* __restrict__ tab) {
+    if (x < -707.0) return 0.0;  // keeps 2^k' * v a normal number
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+    const double big = fma(x, 92.332482616893656877, magic);
+    const int k = __double2loint(big);
+    const double kd = big - magic;
+    double r = fma(kd, -0.010830424696223417, x);
+    r = fma(kd, -2.572804622327669e-14, r);
+    double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const double v = tab[k & 63] * p;
+    return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -274,28 +294,29 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-template <int NT, int KMAX, int EMAX>
+// Card sums: every card's segment (seg_w slots) is scanned by one group of GL lanes (CH
+// slots each, GL * CH >= seg_w), so segments never straddle groups or warps.
+template <int NT, int K, int CH, int HS>
 __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
-                                                            VecRef gout, const int* __restrict__ mask, int want) {
+                                                            VecRef gout, const int* __restrict__ mask, int want,
+                                                            int gl_log2) {
     extern __shared__ __align__(16) double sm[];
-    constexpr int NW = NT / 32;
+    constexpr int NW = NT / 32, NP = NT * K;  // positions padded to NP
     __shared__ double wtot[NW];
-    __shared__ double segv[NW];
-    __shared__ int segf[NW];
     __shared__ __align__(8) uint64_t bar[3];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
-    const int Hp = G.H_pad, hs = G.hand_size, H = G.H, n_ce = G.n_ce;
-    double* popp = sm;                 // [Hp]
-    double* pself = popp + Hp;         // [Hp]
-    double* vb = pself + Hp;           // [2][Hp] opponent rows
-    double* w = vb + 2 * Hp;           // [Hp]
-    double* ob = w + Hp;               // [Hp] output row staging
-    double* Pf = ob + Hp;              // [Hp + 2]
-    double* Ex = Pf + Hp + 2;          // [n_ce]
-    uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [Hp]
-    uint32_t* lohi = reinterpret_cast<uint32_t*>(pcard + Hp);        // [Hp]
-    uint16_t* cent = reinterpret_cast<uint16_t*>(lohi + Hp);         // [n_ce]
+    const int Hp = G.H_pad, H = G.H, n_ce = G.n_ce, W = G.seg_w;
+    double* popp = sm;                 // [NP] (0 beyond H)
+    double* pself = popp + NP;         // [Hp]
+    double* vb = pself + Hp;           // [2][NP] opponent rows (0 beyond Hp)
+    double* w = vb + 2 * NP;           // [NP]
+    double* ob = w + NP;               // [Hp] output row staging
+    double* Pf = ob + Hp;              // [NP + 2]
+    double* Ex = Pf + NP + 2;          // [n_ce]
+    uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [NP]
+    uint32_t* lohi = reinterpret_cast<uint32_t*>(pcard + NP);        // [NP]
+    uint16_t* cent = reinterpret_cast<uint16_t*>(lohi + NP);         // [n_ce]
     const int r0 = P.chunk_off[blockIdx.x], r1 = P.chunk_off[blockIdx.x + 1];
     const int T0 = P.term_off[P.rows_term[r0]], T1 = P.term_off[P.rows_term[r1 - 1] + 1];
     const double* __restrict__ vo = vin.at(g);
@@ -307,11 +328,16 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         mbar_init(&bar[2], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // padding beyond the copied ranges (never overwritten by the bulk copies)
+    for (int i = Hp + tid; i < NP; i += NT) {
+        popp[i] = 0.0;
+        vb[i] = 0.0;
+        vb[NP + i] = 0.0;
+        pcard[i] = make_uint2(0u, 0u);
+        lohi[i] = 0u;
+    }
+    for (int i = H + tid; i < Hp; i += NT) ob[i] = 0.0;
     __syncthreads();
-    auto opp_seq = [&](int ti) {
-        const DevTerm& T = G.terms[tidx[ti]];
-        return player ? T.seq[0] : T.seq[1];
-    };
     if (tid == 0) {
         const unsigned bD = Hp * sizeof(double), bU2 = Hp * sizeof(uint2), bU = Hp * sizeof(uint32_t),
                        bC = n_ce * sizeof(uint16_t);
@@ -322,21 +348,26 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         bulk_g2s(lohi, G.tab_lohi + (size_t)g * Hp, bU, &bar[0]);
         bulk_g2s(cent, G.tab_cent + (size_t)g * n_ce, bC, &bar[0]);
         for (int q = 0; q < 2 && T0 + q < T1; ++q) {
-            const int so = opp_seq(T0 + q);
+            const DevTerm& T = G.terms[tidx[T0 + q]];
+            const int so = player ? T.seq[0] : T.seq[1];
             if (so) {
                 mbar_expect_tx(&bar[1 + q], bD);
-                bulk_g2s(vb + q * Hp, vo + (size_t)so * Hp, bD, &bar[1 + q]);
+                bulk_g2s(vb + q * NP, vo + (size_t)so * Hp, bD, &bar[1 + q]);
             }
         }
     }
-    for (int i = H + tid; i < Hp; i += NT) ob[i] = 0.0;  // padding columns of every output row
     const double kg = G.kappa_game[g];
     const double sd_sign = player == 0 ? 1.0 : -1.0;
-    const int K = (H + NT - 1) / NT, base = tid * K;
-    const int EPT = (n_ce + NT - 1) / NT, ebase = tid * EPT;
-    double racc[KMAX];
+    const int base = tid * K;
+    // card-array role: segment sgi, part of it [sbeg, sbeg + CH)
+    const int GL = 1 << gl_log2;
+    const int sgi = tid >> gl_log2, part = tid & (GL - 1);
+    const bool has_seg = sgi < G.n_cards;
+    const int sbeg = sgi * W + part * CH;
+    const int send = has_seg ? min(sgi * W + W, sbeg + CH) : sbeg;
+    double racc[K];
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) racc[j] = 0.0;
+    for (int j = 0; j < K; ++j) racc[j] = 0.0;
     unsigned par[2] = {0u, 0u};
     mbar_wait(&bar[0], 0);
     int r = r0;
@@ -345,75 +376,64 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         const DevTerm T = G.terms[tidx[ti]];
         const int so = player ? T.seq[0] : T.seq[1];
         const bool sd = T.kind == 2;
-        // prefetch terminal ti+1's row into the other buffer (its last reader, terminal ti-1,
-        // finished phase A before the barriers of terminal ti-1)
+        // prefetch terminal ti+1's row into the other buffer (its previous reader, terminal
+        // ti-1, finished phase A before that terminal's first barrier)
         if (tid == 0 && ti > T0 && ti + 1 < T1) {
-            const int so1 = opp_seq(ti + 1);
+            const DevTerm& T1n = G.terms[tidx[ti + 1]];
+            const int so1 = player ? T1n.seq[0] : T1n.seq[1];
             if (so1) {
                 fence_proxy_async();
                 mbar_expect_tx(&bar[1 + (q ^ 1)], Hp * sizeof(double));
-                bulk_g2s(vb + (q ^ 1) * Hp, vo + (size_t)so1 * Hp, Hp * sizeof(double), &bar[1 + (q ^ 1)]);
+                bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)so1 * Hp, Hp * sizeof(double), &bar[1 + (q ^ 1)]);
             }
         }
         if (so) {
             mbar_wait(&bar[1 + q], par[q]);
             par[q] ^= 1u;
         }
-        const double* vrow = vb + q * Hp;
-        // ---- phase A: w in chunks of K consecutive positions per thread
-        double x[KMAX];
+        const double* vrow = vb + q * NP;
+        // ---- phase A: w = prior_opp * v_opp in chunks of K positions, warp scan of the chunk sums
+        double x[K];
         double run = 0.0;
 #pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            const int i = base + j;
-            x[j] = 0.0;
-            if (j < K && i < H) {
-                x[j] = popp[i] * (so ? vrow[i] : 1.0);
-                w[i] = x[j];
-            }
+        for (int j = 0; j < K; ++j) {
+            x[j] = so ? popp[base + j] * vrow[base + j] : popp[base + j];
+            w[base + j] = x[j];
             run += x[j];
         }
         const double incl = warp_incl_scan(run, lane);
         if (lane == 31) wtot[wid] = incl;
         __syncthreads();
-        // ---- phase B: card-array chunk, segmented scan inside the thread, then over threads
-        double ex[EMAX];
-        double srun = 0.0;
-        bool sflag = false;
-        int first_flag = EMAX;
-        unsigned endmask = 0u;
+        // ---- phase B: card sums (segment scans inside lane groups) and the block prefix of w
+        {
+            double y[CH];
+            double ssum = 0.0;
 #pragma unroll
-        for (int j = 0; j < EMAX; ++j) {
-            const int e = ebase + j;
-            const bool in = j < EPT && e < n_ce;
-            const unsigned c = in ? cent[e] : CE_END;
-            if (in && (c & CE_FIRST)) {
-                srun = 0.0;
-                if (!sflag) first_flag = j;
-                sflag = true;
+            for (int j = 0; j < CH; ++j) {
+                const int e = sbeg + j;
+                const unsigned pos = e < send ? (cent[e] & CE_END) : CE_END;
+                y[j] = pos != CE_END ? w[pos] : 0.0;
+                ssum += y[j];
             }
-            const unsigned pos = c & CE_END;
-            if (pos == CE_END) endmask |= 1u << j;
-            const double y = pos != CE_END ? w[pos] : 0.0;
-            ex[j] = srun;
-            srun += y;
-        }
-        double sv = srun;
-        int sf = sflag;
+            // exclusive scan of the part sums inside the segment's lane group
+            double inc = ssum;
+            for (int o = 1; o < GL; o <<= 1) {
+                const double u = __shfl_up_sync(0xffffffffu, inc, o, GL);
+                if (part >= o) inc += u;
+            }
+            if (has_seg) {
+                double run2 = inc - ssum;
+                if (sd) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double uv = __shfl_up_sync(0xffffffffu, sv, o);
-            const int uf = __shfl_up_sync(0xffffffffu, sf, o);
-            if (lane >= o) {
-                if (!sf) sv += uv;
-                sf |= uf;
+                    for (int j = 0; j < CH; ++j) {
+                        if (sbeg + j < send) Ex[sbeg + j] = run2;
+                        run2 += y[j];
+                    }
+                } else if (send == sgi * W + W && send > sbeg) {
+                    Ex[send - 1] = inc;  // fold: only the segment totals (end slot)
+                }
             }
         }
-        if (lane == 31) {
-            segv[wid] = sv;
-            segf[wid] = sf;
-        }
-        __syncthreads();
         double wpre = 0.0, total = 0.0;
 #pragma unroll
         for (int qq = 0; qq < NW; ++qq) {
@@ -425,57 +445,40 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         if (sd) {
             double p = pbase;
 #pragma unroll
-            for (int j = 0; j < KMAX; ++j) {
-                const int i = base + j;
-                if (j < K && i < H) Pf[i] = p;
+            for (int j = 0; j < K; ++j) {
+                Pf[base + j] = p;
                 p += x[j];
-            }
-            if (tid == 0) Pf[H] = total;
-        }
-        {
-            double carry = 0.0;
-            for (int qq = 0; qq < wid; ++qq) carry = segf[qq] ? segv[qq] : carry + segv[qq];
-            const double pv = __shfl_up_sync(0xffffffffu, sv, 1);
-            const int pf = __shfl_up_sync(0xffffffffu, sf, 1);
-            if (lane > 0) carry = pf ? pv : carry + pv;
-#pragma unroll
-            for (int j = 0; j < EMAX; ++j) {
-                const int e = ebase + j;
-                if (j < EPT && e < n_ce && (sd || ((endmask >> j) & 1u))) Ex[e] = j < first_flag ? carry + ex[j] : ex[j];
             }
         }
         __syncthreads();
-        // ---- phase C
+        // ---- phase C (positions beyond H compute on padding and are never stored)
         const double scale = T.kappa * kg * T.amount;
         double pre = pbase;
 #pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
+        for (int j = 0; j < K; ++j) {
             const int i = base + j;
-            if (j < K && i < H) {
-                const uint2 pc = pcard[i];
-                double v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
-                if (hs == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
-                if (sd) {
-                    const uint32_t lh = lohi[i];
-                    const int lo = lh & 0xFFFFu, hi = lh >> 16;
-                    if (lo == i && hi == i + 1) {
-                        const double ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
-                        v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
-                        if (hs == 2) {
-                            const double cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
-                            v += cb + (cb + x[j]);
-                        }
-                    } else {
-                        v += -(Pf[lo] + Pf[hi]) + Ex[PC_START(pc.x) + PC_RELO(pc.x)] +
-                             Ex[PC_START(pc.x) + PC_REHI(pc.x)];
-                        if (hs == 2) v += Ex[PC_START(pc.y) + PC_RELO(pc.y)] + Ex[PC_START(pc.y) + PC_REHI(pc.y)];
+            const uint2 pc = pcard[i];
+            double v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
+            if (HS == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
+            if (sd) {
+                const uint32_t lh = lohi[i];
+                const int lo = lh & 0xFFFFu, hi = lh >> 16;
+                if (lo == i && hi == i + 1) {
+                    const double ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
+                    v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
+                    if (HS == 2) {
+                        const double cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
+                        v += cb + (cb + x[j]);
                     }
-                    v *= sd_sign;
-                } else if (hs == 2) {
-                    v += x[j];
+                } else {
+                    v += -(Pf[lo] + Pf[hi]) + Ex[PC_START(pc.x) + PC_RELO(pc.x)] + Ex[PC_START(pc.x) + PC_REHI(pc.x)];
+                    if (HS == 2) v += Ex[PC_START(pc.y) + PC_RELO(pc.y)] + Ex[PC_START(pc.y) + PC_REHI(pc.y)];
                 }
-                racc[j] += scale * v;
+                v *= sd_sign;
+            } else if (HS == 2) {
+                v += x[j];
             }
+            racc[j] += scale * v;
             pre += x[j];
         }
         // ---- row end: stage prior_self * acc, one bulk store per row
@@ -484,9 +487,9 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             if (tid == 0) bulk_wait_read0();  // the previous row's store has left ob
             __syncthreads();
 #pragma unroll
-            for (int j = 0; j < KMAX; ++j) {
+            for (int j = 0; j < K; ++j) {
                 const int i = base + j;
-                if (j < K && i < H) ob[i] = pself[i] * racc[j];
+                if (i < H) ob[i] = pself[i] * racc[j];
                 racc[j] = 0.0;
             }
             fence_proxy_async();
@@ -504,13 +507,24 @@ static size_t grad_smem_bytes(const DevGame& G) {
     return sizeof(double) * (size_t)(3 * G.H_pad + 1 + G.n_ce);
 }
 
+static constexpr int STG_NT = 512, STG_K = 3, STG_CH = 6;  // positions <= 1536, segments <= 6 * GL
+
 static size_t grad_staged_smem_bytes(const DevGame& G) {
-    const size_t Hp = G.H_pad;
-    return sizeof(double) * (7 * Hp + 2 + G.n_ce) + sizeof(uint2) * Hp + sizeof(uint32_t) * Hp +
+    const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
+    return sizeof(double) * (2 * Hp + 4 * NP + 2 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
            sizeof(uint16_t) * G.n_ce;
 }
 
-static bool staged_ok(const DevGame& G) { return G.ident && G.all_valid && G.n_bs == 1; }
+static int staged_gl_log2(const DevGame& G) {
+    int l = 0;
+    while ((1 << l) * STG_CH < G.seg_w) ++l;
+    return l;
+}
+
+static bool staged_ok(const DevGame& G) {
+    return G.ident && G.all_valid && G.n_bs == 1 && G.H_pad <= STG_NT * STG_K && (G.hand_size == 1 || G.hand_size == 2) &&
+           (G.n_cards << staged_gl_log2(G)) <= STG_NT && (1 << staged_gl_log2(G)) <= 32;
+}
 
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
                             const int* mask, int want, int all_rows, cudaStream_t st) {
@@ -527,8 +541,13 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
         }
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
-        grad_staged_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX>
-            <<<grid, GRAD_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want);
+        const int gl = staged_gl_log2(G);
+        if (G.hand_size == 2)
+            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2>
+                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
+        else
+            grad_staged_kernel<STG_NT, STG_K, STG_CH, 1>
+                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
         return cudaGetLastError();
     }
     dim3 grid(rows, G.n_games);
@@ -550,7 +569,7 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 static constexpr int TH_HANDS = 32, TH_WARPS = 8, TH_NT = TH_HANDS * TH_WARPS;
 
 size_t tree_smem_bytes(const DevPlayer& P) {
-    return sizeof(double) * (size_t)TH_HANDS * (P.n_pub + P.n_nodes) +
+    return sizeof(double) * ((size_t)TH_HANDS * (P.n_pub + P.n_nodes) + 64 + P.n_nodes) +
            sizeof(int) * (size_t)(6 * P.n_nodes + P.n_pub + 1 + P.n_levels + 1);
 }
 
@@ -564,7 +583,9 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
     const int mode = A.mode;
     const bool has_grad = mode == TM_SBR || mode == TM_PROX || mode == TM_BR || mode == TM_CFR;
     double* val = tile + (size_t)n_pub * TH_HANDS;  // [n_nodes][TH_HANDS]
-    int* s_first = reinterpret_cast<int*>(val + (size_t)n_nodes * TH_HANDS);
+    double* s_exptab = val + (size_t)n_nodes * TH_HANDS;  // [64] 2^(j/64)
+    double* s_logn = s_exptab + 64;                        // [n_nodes] log(number of actions)
+    int* s_first = reinterpret_cast<int*>(s_logn + n_nodes);
     int* s_nact = s_first + n_nodes;
     int* s_par = s_nact + n_nodes;
     int* s_bs = s_par + n_nodes;
@@ -581,17 +602,27 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
         s_kids[i] = P.kids[i];
     }
     for (int i = tid; i <= n_pub; i += TH_NT) s_kidoff[i] = P.kid_off[i];
+    for (int i = tid; i < 64; i += TH_NT) s_exptab[i] = exp2((double)i / 64.0);
+    for (int i = tid; i < n_nodes; i += TH_NT) s_logn[i] = log((double)P.node_nact[i]);
     for (int i = tid; i <= n_lv; i += TH_NT) s_lvoff[i] = P.lvl_off[i];
     const uint8_t* __restrict__ valid_g = G.tab_valid + (size_t)g * G.n_bs * Hp;
     const bool all_valid = G.all_valid != 0;
 
-    // ---- load the gradient tile (one 32-hand row per warp instruction)
+    // ---- load the gradient tile: asynchronous 16-byte copies (LDGSTS), all rows in flight
+    // at once; the objective's scale sc = gsign (* step for prox) is applied when the
+    // bottom-up pass first reads an entry
+    double sc = A.gsign;
     if (has_grad) {
-        const double* __restrict__ gp = A.g.at(g);
-        double sc = A.gsign;
         if (mode == TM_PROX) sc *= A.mu[g];
-        for (int r = wid; r < n_pub; r += TH_WARPS)
-            tile[r * TH_HANDS + lane] = live ? sc * gp[(size_t)r * Hp + h] : 0.0;
+        const double* __restrict__ gp = A.g.at(g) + (size_t)blockIdx.x * TH_HANDS;
+        const int n_chunks = n_pub * (TH_HANDS / 2);
+        for (int c = tid; c < n_chunks; c += TH_NT) {
+            const int r = c / (TH_HANDS / 2), k = c % (TH_HANDS / 2);
+            const unsigned dst = smem_u32(tile + r * TH_HANDS + 2 * k);
+            const double* src = gp + (size_t)r * Hp + 2 * k;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
 
@@ -614,7 +645,7 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
                 // pull the child simplexes' values into this simplex's entries (D_j^i)
                 for (int a = 0; a < n; ++a) {
                     const int s = first + a;
-                    double x = col[a * TH_HANDS];
+                    double x = sc * col[a * TH_HANDS];
                     for (int c = s_kidoff[s]; c < s_kidoff[s + 1]; ++c) x += val[s_kids[c] * TH_HANDS + lane];
                     col[a * TH_HANDS] = x;
                 }
@@ -623,21 +654,23 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
                     // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
                     // i* = argmax qbar, w = mu beta_j
                     const double wgt = mu * P.beta[(size_t)m * Hp + h];
+                    const double iw = 1.0 / wgt;
                     double mn = DBL_MAX;
                     for (int a = 0; a < n; ++a) mn = fmin(mn, col[a * TH_HANDS]);
                     double S = 0.0;
                     for (int a = 0; a < n; ++a) {
-                        const double e = exp(-(col[a * TH_HANDS] - mn) / wgt);
+                        const double e = exp_nonpos((mn - col[a * TH_HANDS]) * iw, s_exptab);
                         col[a * TH_HANDS] = e;
                         S += e;
                     }
                     const double inv = 1.0 / S;
                     for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
-                    value = mn - wgt * log(S) + wgt * log((double)n);
+                    value = mn - wgt * (log(S) - s_logn[m]);
                 } else if (mode == TM_PROX) {
                     // shifted-gradient SBR in multiplicative form:
                     // qbar_i ~ zbar_i exp(-g_i / beta), value = -beta log sum_i zbar_i exp(-g_i / beta)
                     const double beta = P.beta[(size_t)m * Hp + h];
+                    const double ib = 1.0 / beta;
                     const double* __restrict__ zr = cz + (size_t)first * Hp + h;
                     double mn = DBL_MAX;
                     for (int a = 0; a < n; ++a)
@@ -645,7 +678,7 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
                     double S = 0.0;
                     for (int a = 0; a < n; ++a) {
                         const double za = zr[(size_t)a * Hp];
-                        const double e = za > 0.0 ? za * exp(-(col[a * TH_HANDS] - mn) / beta) : 0.0;
+                        const double e = za > 0.0 ? za * exp_nonpos((mn - col[a * TH_HANDS]) * ib, s_exptab) : 0.0;
                         col[a * TH_HANDS] = e;
                         S += e;
                     }
@@ -697,7 +730,7 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
     if (A.value) {
         double v = 0.0;
         if (wid == 0 && live) {
-            v = tile[lane];
+            v = sc * tile[lane];
             for (int c = s_kidoff[0]; c < s_kidoff[1]; ++c) v += val[s_kids[c] * TH_HANDS + lane];
         }
         v = warp_sum(v);
@@ -780,7 +813,10 @@ cudaError_t kernels_prepare() {
     cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(grad_staged_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX>,
+    e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -34,7 +34,8 @@ struct DevGame {
     int n_games, H, H_pad, hand_size, n_bs, n_cards;
     int all_valid;            // 1: every hand is valid at every board state (river endgames)
     int ident;                // 1: position order = hand order at every board state (river endgames)
-    int n_ce;                 // card-array slots per table (CE_SLOTS)
+    int n_ce;                 // card-array slots per table (n_cards * seg_w, padded to 8)
+    int seg_w;                // card-array slots per card (incl. the end slot)
     const int* tab_nvalid;    // [G*n_bs]
     const int16_t* tab_order; // [G*n_bs][H_pad]   position -> hand (valid hands first, strength order)
     const uint32_t* tab_lohi; // [G*n_bs][H_pad]   tie group [lo, hi) of each position

@@ -43,10 +43,10 @@ class Pair:
             deck = Deck(n_ranks, n_suits)
             rp = river.RiverParams(**{k: spec[k] for k in ("pot", "stack", "fracs", "allin", "raise_cap",
                                                            "open_fold")})
-            games = range(n_games) if sample is None else sample
+            which = range(n_games) if sample is None else sample
             self.sf = {g: river.RiverSeqForm(rp, deck, boards[g], workloads.prior_dict(p1[g], deck.n_cards),
                                              workloads.prior_dict(p2[g], deck.n_cards), build_sparse=build_sparse)
-                       for g in games}
+                       for g in which}
         self._maps = {}
 
     def tp(self, g, p):
