@@ -507,11 +507,11 @@ static size_t grad_smem_bytes(const DevGame& G) {
     return sizeof(double) * (size_t)(3 * G.H_pad + 1 + G.n_ce);
 }
 
-static constexpr int STG_NT = 512, STG_K = 3, STG_CH = 6;  // positions <= 1536, segments <= 6 * GL
+static constexpr int STG_NT = 416, STG_K = 3, STG_CH = 6;  // positions <= 1248, 52 cards x 8 lanes
 
 static size_t grad_staged_smem_bytes(const DevGame& G) {
     const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
-    return sizeof(double) * (2 * Hp + 4 * NP + 2 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
+    return sizeof(double) * (2 * Hp + 5 * NP + 2 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
            sizeof(uint16_t) * G.n_ce;
 }
 
