@@ -40,7 +40,7 @@ def build(force=False, verbose=False):
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
+               "-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-pthread", "-I", os.path.join(ROOT, "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
@@ -49,7 +49,7 @@ def build(force=False, verbose=False):
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-Xcompiler", "-pthread"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     for o in objs:

@@ -8,6 +8,7 @@
 #include <functional>
 #include <numeric>
 #include <set>
+#include <thread>
 
 namespace egt {
 
@@ -334,10 +335,8 @@ static int64_t strength_of(const HostGame& G, int g, int bs, int h, const std::v
         int r = hc[0] / 2, b = board[0] / 2;
         return r == b ? 10 + r : r;
     }
-    int ranks[7], suits[7], n = 0;
-    for (int k = 0; k < 2; ++k) { ranks[n] = 13 - G.n_ranks + hc[k] / G.n_suits; suits[n++] = hc[k] % G.n_suits; }
-    for (int c : board) { ranks[n] = 13 - G.n_ranks + c / G.n_suits; suits[n++] = c % G.n_suits; }
-    return hand_strength(ranks, suits, n);
+    (void)board;
+    return G.strength[(size_t)g * G.H + h];  // river: computed once while ordering the hands
 }
 
 static std::vector<int> board_of(const HostGame& G, const std::vector<std::vector<int>>& game_boards, int g, int bs) {
@@ -405,6 +404,25 @@ static void build_table(const HostGame& G, int g, int bs, const std::vector<int>
     }
 }
 
+// Runs f(g) for every game on the host's cores (games are independent); first error wins.
+template <class F>
+static std::string parallel_games(int n, F&& f) {
+    const int nt = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
+    std::vector<std::string> errs(nt);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (int g = t; g < n; g += nt) {
+                std::string e = f(g);
+                if (!e.empty() && errs[t].empty()) errs[t] = e;
+            }
+        });
+    for (auto& x : th) x.join();
+    for (auto& e : errs)
+        if (!e.empty()) return e;
+    return "";
+}
+
 std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
     G = HostGame();
     if (spec.n_games < 1) return "n_games must be >= 1";
@@ -466,9 +484,10 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
     // hands (internal order) and priors
     G.hand_cards.assign((size_t)Gn * H * 2, -1);
     G.hand_combo.assign((size_t)Gn * H, 0);
+    G.strength.assign((size_t)Gn * H, 0);
     for (int p = 0; p < 2; ++p) G.prior[p].assign((size_t)Gn * Hp, 0.0);
     G.kappa_game.assign(Gn, 1.0);
-    for (int g = 0; g < Gn; ++g) {
+    auto per_game = [&](int g) -> std::string {
         if (G.kind != EGT_GAME_RIVER) {
             for (int h = 0; h < H; ++h) {
                 G.hand_cards[((size_t)g * H + h) * 2] = h;
@@ -476,7 +495,7 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
                 G.prior[0][(size_t)g * Hp + h] = 1.0;
                 G.prior[1][(size_t)g * Hp + h] = 1.0;
             }
-            continue;
+            return "";
         }
         const std::vector<int>& bd = game_boards[g];
         std::vector<std::pair<int64_t, int>> hv;  // (strength, combo)
@@ -498,6 +517,7 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
             for (int c2 = c1 + 1; c2 < G.n_cards; ++c2, ++k) combo_cards[k] = {c1, c2};
         for (int h = 0; h < H; ++h) {
             int ci = hv[h].second;
+            G.strength[(size_t)g * H + h] = hv[h].first;
             G.hand_combo[(size_t)g * H + h] = ci;
             G.hand_cards[((size_t)g * H + h) * 2] = combo_cards[ci].first;
             G.hand_cards[((size_t)g * H + h) * 2 + 1] = combo_cards[ci].second;
@@ -525,14 +545,19 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
         }
         if (!(Z > 0)) return "priors leave no compatible hand pair";
         G.kappa_game[g] = 1.0 / Z;
-    }
+        return "";
+    };
+    std::string err = parallel_games(Gn, per_game);
+    if (!err.empty()) return err;
 
     // tables per (game, board state)
     const int nbs = G.tree.n_board_states;
     G.tables.resize((size_t)Gn * nbs);
-    for (int g = 0; g < Gn; ++g)
+    parallel_games(Gn, [&](int g) -> std::string {
         for (int bs = 0; bs < nbs; ++bs)
             build_table(G, g, bs, board_of(G, game_boards, g, bs), G.tables[(size_t)g * nbs + bs]);
+        return "";
+    });
     G.all_valid = 1;
     for (const BoardTable& tb : G.tables)
         if (tb.nvalid != H) G.all_valid = 0;
@@ -576,56 +601,108 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
 
 
 // ||A|| = max |A_ij| of game g (R7); only the theory mu needs it.
-// Per board state: the largest prior product over compatible pairs (fold blocks) and
-// over compatible non-tied pairs (showdown blocks); terminals whose player-1 (-2)
-// sequence is empty aggregate their block's columns (rows) into row (column) 0.
+// Per board state: the largest prior product over compatible pairs (fold blocks) and over
+// compatible non-tied pairs (showdown blocks) -- for each hand a, the player-2 hands in
+// descending prior order are scanned until the first admissible partner (a hand blocks at
+// most 2 * 46 others, so the scan is short); terminals whose player-1 (-2) sequence is
+// empty aggregate their block's columns (rows) into row (column) 0, computed with the
+// same card-removal sums as the gradient (O(H) per terminal).
 double compute_max_abs_A(const HostGame& G, int g) {
-    const int H = G.H, Hp = G.H_pad, nbs = G.tree.n_board_states;
-    const double* p1 = &G.prior[0][(size_t)g * Hp];
-    const double* p2 = &G.prior[1][(size_t)g * Hp];
+    const int H = G.H, Hp = G.H_pad, nbs = G.tree.n_board_states, hs = G.hand_size;
+    const double* pr[2] = {&G.prior[0][(size_t)g * Hp], &G.prior[1][(size_t)g * Hp]};
+    const int* hc = &G.hand_cards[(size_t)g * H * 2];
     auto compat = [&](int a, int b) {
-        const int* ca = &G.hand_cards[((size_t)g * H + a) * 2];
-        const int* cb = &G.hand_cards[((size_t)g * H + b) * 2];
-        for (int i = 0; i < G.hand_size; ++i)
-            for (int j = 0; j < G.hand_size; ++j)
-                if (ca[i] == cb[j]) return false;
+        for (int i = 0; i < hs; ++i)
+            for (int j = 0; j < hs; ++j)
+                if (hc[2 * a + i] == hc[2 * b + j]) return false;
         return true;
     };
-    std::vector<double> pmax_fold(nbs, -1.0), pmax_sd(nbs, -1.0);
-    std::vector<std::vector<int>> group(nbs, std::vector<int>(H, -1));
+    std::vector<int> desc2(H);
+    std::iota(desc2.begin(), desc2.end(), 0);
+    std::sort(desc2.begin(), desc2.end(), [&](int x, int y) { return pr[1][x] > pr[1][y]; });
+    double best = 0.0;
     for (int bs = 0; bs < nbs; ++bs) {
         const BoardTable& tb = G.tables[(size_t)g * nbs + bs];
-        for (int i = 0; i < tb.nvalid; ++i) group[bs][tb.order[i]] = tb.lo[i];
-    }
-    double best = 0.0;
-    for (const Terminal& t : G.terms) {
-        const int bs = t.board_state;
-        const BoardTable& tb = G.tables[(size_t)g * nbs + bs];
-        const std::vector<int>& grp = group[bs];
-        const bool sd = t.kind == T_SHOWDOWN;
-        auto sign = [&](int a, int b) { return sd ? (grp[b] > grp[a] ? 1.0 : (grp[b] < grp[a] ? -1.0 : 0.0)) : 1.0; };
-        const double scale = t.kappa * G.kappa_game[g] * std::fabs(t.amount);
-        const bool e0 = t.last_seq[0] == 0, e1 = t.last_seq[1] == 0;
-        double m = 0.0;
-        if (!e0 && !e1) {
-            double& cache = sd ? pmax_sd[bs] : pmax_fold[bs];
-            if (cache < 0) {
-                cache = 0.0;
-                for (int a = 0; a < H; ++a)
-                    for (int b = 0; b < H; ++b)
-                        if (tb.valid[a] && tb.valid[b] && compat(a, b) && sign(a, b) != 0.0)
-                            cache = std::max(cache, p1[a] * p2[b]);
+        std::vector<int> grp(H, -1);
+        for (int i = 0; i < tb.nvalid; ++i) grp[tb.order[i]] = tb.lo[i];
+        // max prior products over admissible pairs
+        double pmax_fold = 0.0, pmax_sd = 0.0;
+        for (int a = 0; a < H; ++a) {
+            if (!tb.valid[a] || pr[0][a] == 0.0) continue;
+            bool got_f = false, got_s = false;
+            for (int k = 0; k < H && !(got_f && got_s); ++k) {
+                const int b = desc2[k];
+                if (!tb.valid[b] || !compat(a, b)) continue;
+                if (!got_f) {
+                    pmax_fold = std::max(pmax_fold, pr[0][a] * pr[1][b]);
+                    got_f = true;
+                }
+                if (!got_s && grp[b] != grp[a]) {
+                    pmax_sd = std::max(pmax_sd, pr[0][a] * pr[1][b]);
+                    got_s = true;
+                }
             }
-            m = cache;
-        } else {
-            std::vector<double> agg(e0 && e1 ? 1 : H, 0.0);
-            for (int a = 0; a < H; ++a)
-                for (int b = 0; b < H; ++b)
-                    if (tb.valid[a] && tb.valid[b] && compat(a, b))
-                        agg[e0 && e1 ? 0 : (e1 ? a : b)] += p1[a] * p2[b] * sign(a, b);
-            for (double v : agg) m = std::max(m, std::fabs(v));
         }
-        best = std::max(best, scale * m);
+        // aggregated rows / columns: for each hand of the non-empty side, the signed sum over
+        // the compatible hands of the empty side (fold: all, showdown: stronger - weaker)
+        auto agg_max = [&](int side, bool sd) {
+            // side = the player whose sequence is non-empty (its hands index the aggregate)
+            const double* ps = pr[side];
+            const double* po = pr[1 - side];
+            std::vector<double> w(tb.nvalid), P(tb.nvalid + 1, 0.0);
+            std::vector<std::vector<double>> cardP(G.n_cards);  // prefix sums per card, strength order
+            std::vector<std::vector<int>> cardPos(G.n_cards);
+            for (int i = 0; i < tb.nvalid; ++i) {
+                const int h = tb.order[i];
+                w[i] = po[h];
+                P[i + 1] = P[i] + w[i];
+                for (int k = 0; k < hs; ++k) cardPos[hc[2 * h + k]].push_back(i);
+            }
+            for (int c = 0; c < G.n_cards; ++c) {
+                cardP[c].assign(cardPos[c].size() + 1, 0.0);
+                for (size_t j = 0; j < cardPos[c].size(); ++j) cardP[c][j + 1] = cardP[c][j] + w[cardPos[c][j]];
+            }
+            auto cprefix = [&](int c, int pos) {  // sum of w over hands holding c at positions < pos
+                const auto& L = cardPos[c];
+                return cardP[c][std::lower_bound(L.begin(), L.end(), pos) - L.begin()];
+            };
+            double m = 0.0, tot = 0.0;
+            const double T = P[tb.nvalid];
+            std::vector<double> rowsum(tb.nvalid);
+            for (int i = 0; i < tb.nvalid; ++i) {
+                const int h = tb.order[i];
+                double v;
+                if (!sd) {
+                    v = T + (hs == 2 ? w[i] : 0.0);
+                    for (int k = 0; k < hs; ++k) v -= cardP[hc[2 * h + k]].back();
+                } else {
+                    const int lo = tb.lo[i], hi = tb.hi[i];
+                    double weaker = P[lo], stronger = T - P[hi];
+                    for (int k = 0; k < hs; ++k) {
+                        const int c = hc[2 * h + k];
+                        weaker -= cprefix(c, lo);
+                        stronger -= cardP[c].back() - cprefix(c, hi);
+                    }
+                    // sign of player 2's payoff: + when player 2's hand is stronger
+                    v = side == 0 ? stronger - weaker : weaker - stronger;
+                }
+                rowsum[i] = ps[h] * v;
+                m = std::max(m, std::fabs(rowsum[i]));
+                tot += rowsum[i];
+            }
+            return std::make_pair(m, std::fabs(tot));
+        };
+        for (const Terminal& t : G.terms) {
+            if (t.board_state != bs) continue;
+            const bool sd = t.kind == T_SHOWDOWN;
+            const double scale = t.kappa * G.kappa_game[g] * std::fabs(t.amount);
+            const bool e0 = t.last_seq[0] == 0, e1 = t.last_seq[1] == 0;
+            double m;
+            if (!e0 && !e1) m = sd ? pmax_sd : pmax_fold;
+            else if (e0 && e1) m = agg_max(0, sd).second;
+            else m = agg_max(e1 ? 0 : 1, sd).first;
+            best = std::max(best, scale * m);
+        }
     }
     return best;
 }

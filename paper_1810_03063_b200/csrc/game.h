@@ -102,6 +102,7 @@ struct HostGame {
     std::vector<Terminal> terms;
     std::vector<int> hand_cards;       // [G][H][2]
     std::vector<int> hand_combo;       // [G][H] canonical combo index of internal hand
+    std::vector<int64_t> strength;     // [G][H] river: showdown strength of internal hand
     std::vector<double> prior[2];      // [G][H_pad]
     std::vector<double> kappa_game;    // [G]
     std::vector<BoardTable> tables;    // [G * n_board_states]
