@@ -194,12 +194,11 @@ class Clocks:
 
 # ----------------------------------------------------------------------------- roofline
 def grad_bytes_per_game(game, player):
-    """Compulsory HBM bytes of one gradient evaluation of one game:
-    read the other player's vector (public sequences >= 1, H hands, fp64), write this
-    player's gradient (all public sequences, H hands), read both hand priors."""
-    o = 1 - player
-    H = game.H
-    return 8 * H * ((game.n_pub[o] - 1) + game.n_pub[player] + 2)
+    """Compulsory HBM bytes of one gradient evaluation of one game: read
+    the rows of the other player's vector that terminals end on, write the rows of this
+    player's gradient that can be nonzero (sequences ending a terminal; the others are
+    identically 0), read both hand priors -- H hands, fp64."""
+    return 8 * game.H * (game.grad_rows_read[player] + game.grad_rows_written[player] + 2)
 
 
 def measured_peak():

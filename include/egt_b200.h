@@ -91,6 +91,11 @@ typedef struct {
     int64_t vec_stride[2]; /* doubles per game in a player's vector (= n_pub * H_pad) */
     double max_abs_A[1];   /* reserved: ||A|| of game 0 (max |A_ij|, R7) */
     int64_t h2d_bytes;     /* bytes egt_load_game copied host -> device (layout, tables, priors) */
+    /* gradient of player p: rows (public sequences) of the other player's vector it reads
+     * (the distinct sequences terminals end on) and rows of its own output that can be
+     * nonzero (sequences that end a terminal) -- the compulsory traffic */
+    int32_t grad_rows_read[2];
+    int32_t grad_rows_written[2];
 } egt_game_info;
 
 /* ---- game ---------------------------------------------------------------- */

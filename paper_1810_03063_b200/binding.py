@@ -48,6 +48,7 @@ class Info(ctypes.Structure):
         ("n_terminals", ctypes.c_int32), ("depth", ctypes.c_int32 * 2),
         ("vec_stride", ctypes.c_int64 * 2), ("max_abs_A", ctypes.c_double * 1),
         ("h2d_bytes", ctypes.c_int64),
+        ("grad_rows_read", ctypes.c_int32 * 2), ("grad_rows_written", ctypes.c_int32 * 2),
     ]
 
 
@@ -172,6 +173,8 @@ class Game:
         self.n_terminals = info.n_terminals
         self.vec_stride = (info.vec_stride[0], info.vec_stride[1])
         self.h2d_bytes = info.h2d_bytes
+        self.grad_rows_read = (info.grad_rows_read[0], info.grad_rows_read[1])
+        self.grad_rows_written = (info.grad_rows_written[0], info.grad_rows_written[1])
 
     def close(self):
         if self._h:

@@ -350,6 +350,15 @@ extern "C" int egt_game_info_get(const egt_game* G, egt_game_info* o) {
     o->n_terminals = (int)H.terms.size();
     o->max_abs_A[0] = 0.0;
     o->h2d_bytes = G->h2d_bytes;
+    for (int p = 0; p < 2; ++p) {
+        std::vector<char> seen(H.pl[1 - p].n_pub, 0);
+        for (const Terminal& t : H.terms)
+            if (t.last_seq[1 - p] != 0) seen[t.last_seq[1 - p]] = 1;
+        int n = 0;
+        for (char c : seen) n += c;
+        o->grad_rows_read[p] = n;
+        o->grad_rows_written[p] = (int)H.pl[p].rows_term.size();
+    }
     return 0;
 }
 
