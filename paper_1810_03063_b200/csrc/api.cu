@@ -232,7 +232,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         P.n_rows_term = (int)L.rows_term.size();
         P.max_level_width = 0;
         for (int l = 0; l < P.n_levels; ++l) P.max_level_width = std::max(P.max_level_width, L.lvl_off[l + 1] - L.lvl_off[l]);
-        int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt, *co;
+        int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt, *co, *so, *sn, *rs;
         double* be;
         TRY(upload(G, &a, L.first));
         TRY(upload(G, &b, L.nact));
@@ -247,6 +247,13 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         TRY(upload(G, &kd, L.kids));
         TRY(upload(G, &rt, L.rows_term));
         TRY(upload(G, &co, L.chunk_off));
+        TRY(upload(G, &so, L.sched_off));
+        TRY(upload(G, &sn, L.sched_nodes));
+        TRY(upload(G, &rs, L.root_slot));
+        P.sched_off = so;
+        P.sched_nodes = sn;
+        P.root_slot = rs;
+        P.n_root = L.n_root;
         P.n_chunks = (int)L.chunk_off.size() - 1;
         P.chunk_off = co;
         P.node_first = a;

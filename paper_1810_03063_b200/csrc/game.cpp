@@ -318,6 +318,49 @@ static void build_layout(HostGame& G) {
             for (int m : kid[s]) L.kids.push_back(m);
         }
         L.kid_off[L.n_pub] = (int)L.kids.size();
+        // warp schedule per level: groups of nodes with a common (non-empty) parent sequence,
+        // largest first onto the least-loaded warp (load = actions)
+        L.sched_off.assign((size_t)L.depth * TREE_WARPS + 1, 0);
+        L.sched_nodes.clear();
+        L.root_slot.assign(nn, -1);
+        L.n_root = 0;
+        for (int m = 0; m < nn; ++m)
+            if (L.parent_seq[m] == 0) L.root_slot[m] = L.n_root++;
+        for (int l = 0; l < L.depth; ++l) {
+            std::vector<std::vector<int>> groups;
+            std::vector<int> gid(L.n_pub, -1);
+            for (int idx = L.lvl_off[l]; idx < L.lvl_off[l + 1]; ++idx) {
+                const int m = L.lvl_nodes[idx], par = L.parent_seq[m];
+                if (par == 0) {
+                    groups.push_back({m});
+                } else {
+                    if (gid[par] < 0) {
+                        gid[par] = (int)groups.size();
+                        groups.push_back({});
+                    }
+                    groups[gid[par]].push_back(m);
+                }
+            }
+            auto load = [&](const std::vector<int>& gr) {
+                int a = 0;
+                for (int m : gr) a += L.nact[m];
+                return a;
+            };
+            std::stable_sort(groups.begin(), groups.end(),
+                             [&](const std::vector<int>& a, const std::vector<int>& b) { return load(a) > load(b); });
+            std::vector<std::vector<int>> per(TREE_WARPS);
+            std::vector<int> wl(TREE_WARPS, 0);
+            for (const auto& gr : groups) {
+                const int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
+                wl[w] += load(gr);
+                for (int m : gr) per[w].push_back(m);
+            }
+            for (int w = 0; w < TREE_WARPS; ++w) {
+                L.sched_off[(size_t)l * TREE_WARPS + w] = (int)L.sched_nodes.size();
+                for (int m : per[w]) L.sched_nodes.push_back(m);
+            }
+        }
+        L.sched_off[(size_t)L.depth * TREE_WARPS] = (int)L.sched_nodes.size();
     }
 }
 

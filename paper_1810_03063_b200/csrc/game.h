@@ -15,6 +15,8 @@ namespace egt {
 
 // private hands per game the gradient kernel handles (256 threads x 5 positions)
 constexpr int EGT_MAX_HANDS = 1280;
+// warps of the treeplex kernel; each level's nodes are scheduled onto them on the host
+constexpr int TREE_WARPS = 8;
 // terminals per CTA of the staged river gradient kernel (rows are never split)
 constexpr int GRAD_CHUNK_TERMS = 32;
 
@@ -51,6 +53,13 @@ struct PlayerLayout {
     std::vector<int> chunk_off;           // rows_term split into chunks of ~GRAD_CHUNK_TERMS terminals
     std::vector<int> lvl_off, lvl_nodes;  // decision nodes grouped by level
     std::vector<int> kid_off, kids;       // child decision nodes of each sequence
+    // treeplex-kernel schedule: nodes of level l run on warp w in the order
+    // sched_nodes[sched_off[l * TREE_WARPS + w] .. sched_off[l * TREE_WARPS + w + 1]); all
+    // nodes sharing a parent sequence (other than the empty one) run on one warp, so their
+    // values can be added into the parent entry without races; root nodes (parent = empty
+    // sequence) keep their values in root_slot[m] >= 0
+    std::vector<int> sched_off, sched_nodes, root_slot;
+    int n_root = 0;
     int depth = 0;
 };
 

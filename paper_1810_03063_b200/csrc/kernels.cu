@@ -557,170 +557,196 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 }
 
 // ------------------------------------------------------------------ treeplex pass
-// CTA = (TH_HANDS hands, game); TH_WARPS warps.  The player's whole gradient tile
-// [n_pub][TH_HANDS] is staged in shared memory (lane = hand).  Bottom-up, level by level
-// (deepest first; nodes of a level are independent and spread over the warps), each
-// simplex j = (node m, hand) pulls the values of its child simplexes (D_j^i) into its
-// entries, solves its local problem (softmax / prox / argmin / regret
-// matching), overwrites its entries with the behavioural strategy and stores its value in
-// val[m].  Top-down (shallowest first) each entry becomes q_i = q_{p_j} * qbar_i in place,
-// and the requested outputs (behavioural, sequence form, EGT convex combinations, CFR
-// average) are written row by row (coalesced, 32 hands per row).
-static constexpr int TH_HANDS = 32, TH_WARPS = 8, TH_NT = TH_HANDS * TH_WARPS;
+// CTA = (TH_HANDS = 64 hands, game), TREE_WARPS warps; lane l handles hands l and l + 32 of
+// the tile.  The player's whole gradient tile [n_pub][64] is staged in shared memory by
+// asynchronous 16-byte copies and scaled once.  Bottom-up, level by level (deepest first),
+// every warp runs the nodes the host scheduled for it (game.h): each simplex j = (node,
+// hand) solves its local problem (softmax / prox / argmin / regret
+// matching) on its entries -- which already hold the values of the simplexes below --,
+// overwrites them with the behavioural strategy and adds its value into the parent entry
+// (nodes sharing a parent run on one warp, in a fixed order: no races, deterministic);
+// root simplexes keep their values apart.  Top-down (shallowest first) each entry becomes
+// q_i = q_{p_j} * qbar_i in place and the requested outputs (behavioural, sequence form,
+// EGT convex combinations, CFR average) are written row by row.
+static constexpr int TH_HANDS = 64, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
 
 size_t tree_smem_bytes(const DevPlayer& P) {
-    return sizeof(double) * ((size_t)TH_HANDS * (P.n_pub + P.n_nodes) + 64 + P.n_nodes) +
-           sizeof(int) * (size_t)(6 * P.n_nodes + P.n_pub + 1 + P.n_levels + 1);
+    return sizeof(double) * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + 64 + P.n_nodes) +
+           sizeof(int) * (size_t)(6 * P.n_nodes + P.n_levels * TH_WARPS + 1);
 }
 
-__global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
-    extern __shared__ double tile[];
+struct TreeNodeCtx {
+    int mode, cfr_plus;
+    double mu;
+    const double* __restrict__ exptab;
+};
+
+// Bottom-up work of simplex (node m, hand h) on its column; returns the simplex value.
+__device__ __forceinline__ double tree_node_up(const TreeNodeCtx& C, const DevPlayer& P, double* col, int first,
+                                               int n, int m, int h, int Hp, double logn, double* __restrict__ cz,
+                                               double* __restrict__ rg) {
+    const int mode = C.mode;
+    if (mode == TM_SBR) {
+        // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
+        // i* = argmax qbar, w = mu beta_j
+        const double wgt = C.mu * P.beta[(size_t)m * Hp + h];
+        const double iw = 1.0 / wgt;
+        double mn = DBL_MAX;
+        for (int a = 0; a < n; ++a) mn = fmin(mn, col[a * TH_HANDS]);
+        double S = 0.0;
+        for (int a = 0; a < n; ++a) {
+            const double e = exp_nonpos((mn - col[a * TH_HANDS]) * iw, C.exptab);
+            col[a * TH_HANDS] = e;
+            S += e;
+        }
+        const double inv = 1.0 / S;
+        for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
+        return mn - wgt * (log(S) - logn);
+    }
+    if (mode == TM_PROX) {
+        // shifted-gradient SBR in multiplicative form (R16):
+        // qbar_i ~ zbar_i exp(-g_i / beta), value = -beta log sum_i zbar_i exp(-g_i / beta)
+        const double beta = P.beta[(size_t)m * Hp + h];
+        const double ib = 1.0 / beta;
+        const double* __restrict__ zr = cz + (size_t)first * Hp + h;
+        double mn = DBL_MAX;
+        for (int a = 0; a < n; ++a)
+            if (zr[(size_t)a * Hp] > 0.0) mn = fmin(mn, col[a * TH_HANDS]);
+        double S = 0.0;
+        for (int a = 0; a < n; ++a) {
+            const double za = zr[(size_t)a * Hp];
+            const double e = za > 0.0 ? za * exp_nonpos((mn - col[a * TH_HANDS]) * ib, C.exptab) : 0.0;
+            col[a * TH_HANDS] = e;
+            S += e;
+        }
+        const double inv = 1.0 / S;
+        for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
+        return mn - beta * log(S);
+    }
+    if (mode == TM_BR) {
+        int best = 0;
+        double mn = col[0];
+        for (int a = 1; a < n; ++a) {
+            const double v = col[a * TH_HANDS];
+            if (v < mn) {
+                mn = v;
+                best = a;
+            }
+        }
+        for (int a = 0; a < n; ++a) col[a * TH_HANDS] = a == best ? 1.0 : 0.0;
+        return mn;
+    }
+    // TM_CFR: utility u = gsign * g, current strategy z, regrets r
+    double v = 0.0;
+    for (int a = 0; a < n; ++a) v += col[a * TH_HANDS] * cz[(size_t)(first + a) * Hp + h];
+    double S = 0.0;
+    for (int a = 0; a < n; ++a) {
+        const size_t ix = (size_t)(first + a) * Hp + h;
+        const double u = col[a * TH_HANDS], r0 = rg[ix];
+        double r = r0 + u - v;
+        if (C.cfr_plus) r = fmax(r, 0.0);
+        rg[ix] = r;
+        // DESIGN.md R15: regrets at the rounding-noise level of their own update count as 0
+        const double tol = 1e-13 * (fabs(r0) + fabs(u) + fabs(v));
+        const double pr = r > tol ? r : 0.0;
+        col[a * TH_HANDS] = pr;
+        S += pr;
+    }
+    for (int a = 0; a < n; ++a) {
+        const double z = S > 0.0 ? col[a * TH_HANDS] / S : 1.0 / n;
+        col[a * TH_HANDS] = z;
+        cz[(size_t)(first + a) * Hp + h] = z;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(TH_NT, 2) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
+    extern __shared__ __align__(16) double tile[];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (A.mask && A.mask[g] != A.want) return;
     const int Hp = G.H_pad, n_pub = P.n_pub, n_nodes = P.n_nodes, n_lv = P.n_levels;
-    const int h = blockIdx.x * TH_HANDS + lane;
-    const bool live = h < G.H;
+    const int h0 = blockIdx.x * TH_HANDS;
     const int mode = A.mode;
     const bool has_grad = mode == TM_SBR || mode == TM_PROX || mode == TM_BR || mode == TM_CFR;
-    double* val = tile + (size_t)n_pub * TH_HANDS;  // [n_nodes][TH_HANDS]
-    double* s_exptab = val + (size_t)n_nodes * TH_HANDS;  // [64] 2^(j/64)
-    double* s_logn = s_exptab + 64;                        // [n_nodes] log(number of actions)
+    double* rootv = tile + (size_t)n_pub * TH_HANDS;              // [n_root][64]
+    double* s_exptab = rootv + (size_t)P.n_root * TH_HANDS;       // [64] 2^(j/64)
+    double* s_logn = s_exptab + 64;                               // [n_nodes]
     int* s_first = reinterpret_cast<int*>(s_logn + n_nodes);
     int* s_nact = s_first + n_nodes;
     int* s_par = s_nact + n_nodes;
     int* s_bs = s_par + n_nodes;
-    int* s_lvn = s_bs + n_nodes;       // [n_nodes]
-    int* s_kidoff = s_lvn + n_nodes;   // [n_pub+1]
-    int* s_kids = s_kidoff + n_pub + 1; // [n_nodes]
-    int* s_lvoff = s_kids + n_nodes;   // [n_lv+1]
+    int* s_rslot = s_bs + n_nodes;
+    int* s_sn = s_rslot + n_nodes;                                // [n_nodes]
+    int* s_so = s_sn + n_nodes;                                   // [n_lv * TH_WARPS + 1]
     for (int i = tid; i < n_nodes; i += TH_NT) {
         s_first[i] = P.node_first[i];
         s_nact[i] = P.node_nact[i];
         s_par[i] = P.node_parent[i];
         s_bs[i] = P.node_bs[i];
-        s_lvn[i] = P.lvl_nodes[i];
-        s_kids[i] = P.kids[i];
+        s_rslot[i] = P.root_slot[i];
+        s_sn[i] = P.sched_nodes[i];
+        s_logn[i] = log((double)P.node_nact[i]);
     }
-    for (int i = tid; i <= n_pub; i += TH_NT) s_kidoff[i] = P.kid_off[i];
+    for (int i = tid; i <= n_lv * TH_WARPS; i += TH_NT) s_so[i] = P.sched_off[i];
     for (int i = tid; i < 64; i += TH_NT) s_exptab[i] = exp2((double)i / 64.0);
-    for (int i = tid; i < n_nodes; i += TH_NT) s_logn[i] = log((double)P.node_nact[i]);
-    for (int i = tid; i <= n_lv; i += TH_NT) s_lvoff[i] = P.lvl_off[i];
     const uint8_t* __restrict__ valid_g = G.tab_valid + (size_t)g * G.n_bs * Hp;
     const bool all_valid = G.all_valid != 0;
 
-    // ---- load the gradient tile: asynchronous 16-byte copies (LDGSTS), all rows in flight
-    // at once; the objective's scale sc = gsign (* step for prox) is applied when the
-    // bottom-up pass first reads an entry
-    double sc = A.gsign;
+    // ---- gradient tile: asynchronous 16-byte copies (LDGSTS), all rows in flight, then each
+    // thread scales the chunks it copied by sc = gsign (* step for prox)
     if (has_grad) {
+        double sc = A.gsign;
         if (mode == TM_PROX) sc *= A.mu[g];
-        const double* __restrict__ gp = A.g.at(g) + (size_t)blockIdx.x * TH_HANDS;
-        const int n_chunks = n_pub * (TH_HANDS / 2);
+        const double* __restrict__ gp = A.g.at(g) + h0;
+        const int per_row = TH_HANDS / 2, n_chunks = n_pub * per_row;
         for (int c = tid; c < n_chunks; c += TH_NT) {
-            const int r = c / (TH_HANDS / 2), k = c % (TH_HANDS / 2);
-            const unsigned dst = smem_u32(tile + r * TH_HANDS + 2 * k);
-            const double* src = gp + (size_t)r * Hp + 2 * k;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+            const int r = c / per_row, k = c % per_row;
+            if (h0 + 2 * k < Hp) {
+                const unsigned dst = smem_u32(tile + r * TH_HANDS + 2 * k);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gp + (size_t)r * Hp + 2 * k)
+                             : "memory");
+            }
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        if (sc != 1.0)
+            for (int c = tid; c < n_chunks; c += TH_NT) {
+                const int r = c / per_row, k = c % per_row;
+                double2* t2 = reinterpret_cast<double2*>(tile + r * TH_HANDS + 2 * k);
+                double2 v = *t2;
+                v.x *= sc;
+                v.y *= sc;
+                *t2 = v;
+            }
     }
     __syncthreads();
 
     // ---- bottom-up, deepest level first
-    const double mu = (mode == TM_SBR) ? A.mu[g] : 1.0;
+    TreeNodeCtx C;
+    C.mode = mode;
+    C.cfr_plus = A.cfr_plus;
+    C.mu = (mode == TM_SBR) ? A.mu[g] : 1.0;
+    C.exptab = s_exptab;
     double* __restrict__ cz = A.center.ok() ? A.center.at(g) : nullptr;
     double* __restrict__ rg = A.regret.ok() ? A.regret.at(g) : nullptr;
     if (has_grad) {
         for (int L = n_lv - 1; L >= 0; --L) {
-            for (int idx = s_lvoff[L] + wid; idx < s_lvoff[L + 1]; idx += TH_WARPS) {
-                const int m = s_lvn[idx];
-                const int first = s_first[m], n = s_nact[m];
-                double* col = tile + (size_t)first * TH_HANDS + lane;
-                const bool ok = live && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
-                if (!ok) {
-                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] = 0.0;
-                    val[m * TH_HANDS + lane] = 0.0;
-                    continue;
+            const int i0 = s_so[L * TH_WARPS + wid], i1 = s_so[L * TH_WARPS + wid + 1];
+            for (int idx = i0; idx < i1; ++idx) {
+                const int m = s_sn[idx];
+                const int first = s_first[m], n = s_nact[m], par = s_par[m], rs = s_rslot[m];
+                const double logn = s_logn[m];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int c = lane + 32 * j, h = h0 + c;
+                    double* col = tile + (size_t)first * TH_HANDS + c;
+                    double value = 0.0;
+                    if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]))
+                        value = tree_node_up(C, P, col, first, n, m, h, Hp, logn, cz, rg);
+                    else
+                        for (int a = 0; a < n; ++a) col[a * TH_HANDS] = 0.0;
+                    if (rs >= 0) rootv[rs * TH_HANDS + c] = value;
+                    else tile[par * TH_HANDS + c] += value;
                 }
-                // pull the child simplexes' values into this simplex's entries (D_j^i)
-                for (int a = 0; a < n; ++a) {
-                    const int s = first + a;
-                    double x = sc * col[a * TH_HANDS];
-                    for (int c = s_kidoff[s]; c < s_kidoff[s + 1]; ++c) x += val[s_kids[c] * TH_HANDS + lane];
-                    col[a * TH_HANDS] = x;
-                }
-                double value;
-                if (mode == TM_SBR) {
-                    // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
-                    // i* = argmax qbar, w = mu beta_j
-                    const double wgt = mu * P.beta[(size_t)m * Hp + h];
-                    const double iw = 1.0 / wgt;
-                    double mn = DBL_MAX;
-                    for (int a = 0; a < n; ++a) mn = fmin(mn, col[a * TH_HANDS]);
-                    double S = 0.0;
-                    for (int a = 0; a < n; ++a) {
-                        const double e = exp_nonpos((mn - col[a * TH_HANDS]) * iw, s_exptab);
-                        col[a * TH_HANDS] = e;
-                        S += e;
-                    }
-                    const double inv = 1.0 / S;
-                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
-                    value = mn - wgt * (log(S) - s_logn[m]);
-                } else if (mode == TM_PROX) {
-                    // shifted-gradient SBR in multiplicative form:
-                    // qbar_i ~ zbar_i exp(-g_i / beta), value = -beta log sum_i zbar_i exp(-g_i / beta)
-                    const double beta = P.beta[(size_t)m * Hp + h];
-                    const double ib = 1.0 / beta;
-                    const double* __restrict__ zr = cz + (size_t)first * Hp + h;
-                    double mn = DBL_MAX;
-                    for (int a = 0; a < n; ++a)
-                        if (zr[(size_t)a * Hp] > 0.0) mn = fmin(mn, col[a * TH_HANDS]);
-                    double S = 0.0;
-                    for (int a = 0; a < n; ++a) {
-                        const double za = zr[(size_t)a * Hp];
-                        const double e = za > 0.0 ? za * exp_nonpos((mn - col[a * TH_HANDS]) * ib, s_exptab) : 0.0;
-                        col[a * TH_HANDS] = e;
-                        S += e;
-                    }
-                    const double inv = 1.0 / S;
-                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
-                    value = mn - beta * log(S);
-                } else if (mode == TM_BR) {
-                    int best = 0;
-                    double mn = col[0];
-                    for (int a = 1; a < n; ++a) {
-                        const double v = col[a * TH_HANDS];
-                        if (v < mn) {
-                            mn = v;
-                            best = a;
-                        }
-                    }
-                    for (int a = 0; a < n; ++a) col[a * TH_HANDS] = a == best ? 1.0 : 0.0;
-                    value = mn;
-                } else {  // TM_CFR: utility u = gsign * g, current strategy z, regrets r
-                    double v = 0.0;
-                    for (int a = 0; a < n; ++a) v += col[a * TH_HANDS] * cz[(size_t)(first + a) * Hp + h];
-                    double S = 0.0;
-                    for (int a = 0; a < n; ++a) {
-                        const size_t ix = (size_t)(first + a) * Hp + h;
-                        const double u = col[a * TH_HANDS], r0 = rg[ix];
-                        double r = r0 + u - v;
-                        if (A.cfr_plus) r = fmax(r, 0.0);
-                        rg[ix] = r;
-                        // DESIGN.md R15: regrets at the rounding-noise level of their own update count as 0
-                        const double tol = 1e-13 * (fabs(r0) + fabs(u) + fabs(v));
-                        const double pr = r > tol ? r : 0.0;
-                        col[a * TH_HANDS] = pr;
-                        S += pr;
-                    }
-                    for (int a = 0; a < n; ++a) {
-                        const double z = S > 0.0 ? col[a * TH_HANDS] / S : 1.0 / n;
-                        col[a * TH_HANDS] = z;
-                        cz[(size_t)(first + a) * Hp + h] = z;
-                    }
-                    value = v;
-                }
-                val[m * TH_HANDS + lane] = value;
             }
             __syncthreads();
         }
@@ -729,9 +755,16 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
     // ---- per-game value: root entry + root simplexes' values, deterministic reductions
     if (A.value) {
         double v = 0.0;
-        if (wid == 0 && live) {
-            v = sc * tile[lane];
-            for (int c = s_kidoff[0]; c < s_kidoff[1]; ++c) v += val[s_kids[c] * TH_HANDS + lane];
+        if (wid == 0) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int c = lane + 32 * j;
+                if (h0 + c < G.H) {
+                    double u = tile[c];
+                    for (int r = 0; r < P.n_root; ++r) u += rootv[r * TH_HANDS + c];
+                    v += u;
+                }
+            }
         }
         v = warp_sum(v);
         __shared__ bool last;
@@ -767,35 +800,46 @@ __global__ void __launch_bounds__(TH_NT, 4) tree_kernel(DevGame G, DevPlayer P, 
         alpha = A.avg_linear ? 2.0 * t / (t * t + t) : 1.0 / t;
     }
     const double* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
-    const bool hvalid = h < Hp;
-    if (wid == 0 && hvalid) {
-        const double q0 = live ? 1.0 : 0.0;
-        if (ob) ob[h] = q0;
-        if (oq) oq[h] = q0;
-        if (co) co[h] = live ? (1.0 - tau) * ci[h] + tau : 0.0;
-        if (av) av[h] = q0;
+    if (wid == 0) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int h = h0 + lane + 32 * j;
+            if (h < Hp) {
+                const bool live = h < G.H;
+                const double q0 = live ? 1.0 : 0.0;
+                if (ob) ob[h] = q0;
+                if (oq) oq[h] = q0;
+                if (co) co[h] = live ? (1.0 - tau) * ci[h] + tau : 0.0;
+                if (av) av[h] = q0;
+            }
+        }
     }
     for (int L = 0; L < n_lv; ++L) {
-        for (int idx = s_lvoff[L] + wid; idx < s_lvoff[L + 1]; idx += TH_WARPS) {
-            const int m = s_lvn[idx];
+        const int i0 = s_so[L * TH_WARPS + wid], i1 = s_so[L * TH_WARPS + wid + 1];
+        for (int idx = i0; idx < i1; ++idx) {
+            const int m = s_sn[idx];
             const int first = s_first[m], n = s_nact[m], par = s_par[m];
-            const bool ok = live && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
-            const double qp = par == 0 ? (live ? 1.0 : 0.0) : tile[par * TH_HANDS + lane];
-            for (int a = 0; a < n; ++a) {
-                const int s = first + a;
-                double b;
-                if (!ok) b = 0.0;
-                else if (mode == TM_UNIFORM) b = 1.0 / n;
-                else if (mode == TM_COMBINE) b = bin[(size_t)s * Hp + h];
-                else b = tile[s * TH_HANDS + lane];
-                const double q = qp * b;
-                tile[s * TH_HANDS + lane] = q;
-                if (hvalid) {
-                    const size_t ix = (size_t)s * Hp + h;
-                    if (ob) ob[ix] = b;
-                    if (oq) oq[ix] = q;
-                    if (co) co[ix] = (1.0 - tau) * ci[ix] + tau * q;
-                    if (av) av[ix] = alpha * q + (1.0 - alpha) * av[ix];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int c = lane + 32 * j, h = h0 + c;
+                const bool ok = h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
+                const double qp = par == 0 ? (ok ? 1.0 : 0.0) : tile[par * TH_HANDS + c];
+                for (int a = 0; a < n; ++a) {
+                    const int s = first + a;
+                    double b;
+                    if (!ok) b = 0.0;
+                    else if (mode == TM_UNIFORM) b = 1.0 / n;
+                    else if (mode == TM_COMBINE) b = bin[(size_t)s * Hp + h];
+                    else b = tile[s * TH_HANDS + c];
+                    const double q = qp * b;
+                    tile[s * TH_HANDS + c] = q;
+                    if (h < Hp) {
+                        const size_t ix = (size_t)s * Hp + h;
+                        if (ob) ob[ix] = b;
+                        if (oq) oq[ix] = q;
+                        if (co) co[ix] = (1.0 - tau) * ci[ix] + tau * q;
+                        if (av) av[ix] = alpha * q + (1.0 - alpha) * av[ix];
+                    }
                 }
             }
         }

@@ -58,6 +58,10 @@ struct DevPlayer {
     const int* lvl_nodes;    // [n_nodes]
     const int* kid_off;      // [n_pub+1] child nodes of each sequence (D_j^i)
     const int* kids;         // [n_nodes]
+    const int* sched_off;    // [n_levels * TREE_WARPS + 1] treeplex-kernel warp schedule (game.h)
+    const int* sched_nodes;  // [n_nodes]
+    const int* root_slot;    // [n_nodes] slot of a root node's value, -1 otherwise
+    int n_root;
     const double* beta;      // [n_nodes][H_pad]
     const int* term_off;     // [n_pub+1] terminals grouped by this player's last sequence
     const int* term_idx;
