@@ -568,7 +568,7 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 // root simplexes keep their values apart.  Top-down (shallowest first) each entry becomes
 // q_i = q_{p_j} * qbar_i in place and the requested outputs (behavioural, sequence form,
 // EGT convex combinations, CFR average) are written row by row.
-static constexpr int TH_HANDS = 64, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
+static constexpr int TH_HPL = 1, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
 
 size_t tree_smem_bytes(const DevPlayer& P) {
     return sizeof(double) * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + 64 + P.n_nodes) +
@@ -660,7 +660,7 @@ __device__ __forceinline__ double tree_node_up(const TreeNodeCtx& C, const DevPl
     return v;
 }
 
-__global__ void __launch_bounds__(TH_NT, 2) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
+__global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
     extern __shared__ __align__(16) double tile[];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (A.mask && A.mask[g] != A.want) return;
@@ -698,7 +698,8 @@ __global__ void __launch_bounds__(TH_NT, 2) tree_kernel(DevGame G, DevPlayer P, 
         double sc = A.gsign;
         if (mode == TM_PROX) sc *= A.mu[g];
         const double* __restrict__ gp = A.g.at(g) + h0;
-        const int per_row = TH_HANDS / 2, n_chunks = n_pub * per_row;
+        constexpr int per_row = TH_HANDS / 2;
+        const int n_chunks = n_pub * per_row;
         for (int c = tid; c < n_chunks; c += TH_NT) {
             const int r = c / per_row, k = c % per_row;
             if (h0 + 2 * k < Hp) {
@@ -736,7 +737,7 @@ __global__ void __launch_bounds__(TH_NT, 2) tree_kernel(DevGame G, DevPlayer P, 
                 const int first = s_first[m], n = s_nact[m], par = s_par[m], rs = s_rslot[m];
                 const double logn = s_logn[m];
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < TH_HPL; ++j) {
                     const int c = lane + 32 * j, h = h0 + c;
                     double* col = tile + (size_t)first * TH_HANDS + c;
                     double value = 0.0;
@@ -757,7 +758,7 @@ __global__ void __launch_bounds__(TH_NT, 2) tree_kernel(DevGame G, DevPlayer P, 
         double v = 0.0;
         if (wid == 0) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < TH_HPL; ++j) {
                 const int c = lane + 32 * j;
                 if (h0 + c < G.H) {
                     double u = tile[c];
@@ -802,7 +803,7 @@ __global__ void __launch_bounds__(TH_NT, 2) tree_kernel(DevGame G, DevPlayer P, 
     const double* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
     if (wid == 0) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < TH_HPL; ++j) {
             const int h = h0 + lane + 32 * j;
             if (h < Hp) {
                 const bool live = h < G.H;
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(TH_NT, 2) tree_kernel(DevGame G, DevPlayer P, 
             const int m = s_sn[idx];
             const int first = s_first[m], n = s_nact[m], par = s_par[m];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < TH_HPL; ++j) {
                 const int c = lane + 32 * j, h = h0 + c;
                 const bool ok = h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
                 const double qp = par == 0 ? (ok ? 1.0 : 0.0) : tile[par * TH_HANDS + c];
