@@ -56,6 +56,9 @@ def parse():
                     help="also time EGT/as and CFR+ to eps_sad <= --eps-mbb on this many endgames (0: skip)")
     ap.add_argument("--eps-mbb", type=float, default=1.0, help="target saddle gap in milli-big-blinds")
     ap.add_argument("--converge-max-steps", type=int, default=4000)
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: every rank holds the same batch and computes a slice of each "
+                         "gradient's rows, NCCL all-reduce per gradient (DESIGN.md row 8)")
     return ap.parse_args()
 
 
@@ -84,9 +87,10 @@ def max_over_ranks(x, world, device="cpu"):
     return float(t.item())
 
 
-def throughput(games_per_rank, world, steps, ms):
-    """Whole-job gradient evaluations per second: every rank's games, every step."""
-    return GRADS_PER_STEP * games_per_rank * world * steps / (ms / 1e3)
+def throughput(games_per_rank, world, steps, ms, shard=False):
+    """Whole-job gradient evaluations per second: every rank's games, every step (sharded:
+    the ranks share one batch, so its games count once)."""
+    return GRADS_PER_STEP * games_per_rank * (1 if shard else world) * steps / (ms / 1e3)
 
 
 def time_to_gap(P, spec, boards, p1, p2, solver, eps_chips, max_steps, check_every=10):
@@ -140,7 +144,9 @@ def workload_config(args, game=None, world=1):
            "games_per_gpu": args.batch, "global_games": args.batch * world,
            "solver": "EGT/as (dilated entropy) + eps_sad per step", "pot": 2100, "stack": 18950,
            "bet_abstraction": "PAPER.md:673-685" if args.workload == "libratus" else "{0.5,1,all-in}",
-           "parallelism": "dp%d (independent endgames per rank)" % world}
+           "parallelism": ("shard%d (one batch; each gradient's terminal rows split over ranks, NCCL "
+                           "all-reduce per gradient)" % world) if getattr(args, "shard", False) else
+                          "dp%d (independent endgames per rank)" % world}
     if game is not None:
         cfg.update({"hands_per_player": game.H, "pub_seqs": list(game.n_pub),
                     "terminals": game.n_terminals,
@@ -325,10 +331,12 @@ def run_b200(args):
         dist.barrier()
     P.load_library()
 
-    spec, boards, p1, p2 = workload(args, rank)
+    spec, boards, p1, p2 = workload(args, 0 if args.shard else rank)
     game = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2)
     stream = torch.cuda.current_stream()
     game.set_stream(stream)
+    if args.shard:
+        game.shard(rank, world)
     game.egt_init(P.EGT_AS)  # practical mu (R14)
     gap = torch.zeros(args.batch, dtype=torch.float64, device="cuda")
 
@@ -355,7 +363,7 @@ def run_b200(args):
         dist.barrier()
     ck = clocks.stop()
     ms = max_over_ranks(ev0.elapsed_time(ev1), world, "cuda")
-    value = throughput(args.batch, world, args.steps, ms)
+    value = throughput(args.batch, world, args.steps, ms, args.shard)
     gaps = gap.cpu().numpy()
 
     # per-kernel event timing (same kernels, eager launches, events on the library stream)
@@ -393,7 +401,8 @@ def run_b200(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
                 "config": dict(workload_config(args, game, world),
                                l2="no flush: per-step working set %.0f MB > 126 MB L2" %
                                (args.batch * 2 * 7 * 8 * game.H_pad * max(game.n_pub) / 1e6)),
@@ -413,6 +422,8 @@ def run_b200(args):
         pinned = torch.zeros(args.batch, dtype=torch.float64).pin_memory()
         t0 = time.perf_counter()
         g2 = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2)
+        if args.shard:
+            g2.shard(rank, world)
         g2.egt_init(P.EGT_AS)
         for _ in range(args.steps):
             g2.egt_step(1)
@@ -421,7 +432,7 @@ def run_b200(args):
         grads_e2e = float(g2.egt_scalars()[0, 7])
         el = max_over_ranks(el, world, "cuda")
         if rank == 0:
-            line["e2e"] = {"value": grads_e2e * args.batch * world / el, "unit": UNIT,
+            line["e2e"] = {"value": grads_e2e * args.batch * (1 if args.shard else world) / el, "unit": UNIT,
                            "h2d_bytes_per_step": int(g2.h2d_bytes / args.steps),
                            "d2h_bytes_per_step": 8 * args.batch,
                            "what": "wall clock: egt_load_game from host arrays + egt_init (mu search) + "

@@ -201,6 +201,27 @@ int get_strategy_device(egt_game* game, int32_t player, int32_t which, double* d
  * last EGV, gradient evaluations (A y or A^T x, per game). */
 int egt_scalars(egt_game* game, double* host_out);
 
+/* ---- sharding one game over ranks (DESIGN.md row 8) -----------------------------
+ * Every rank loads the SAME game(s).  egt_shard gives rank `rank` of `world` a contiguous
+ * range of the sequences that end terminals (balanced by terminal count); every gradient
+ * the library evaluates (egt_gradient, the EGT / CFR solvers, saddle_gap) then computes only
+ * those rows and sums the other ranks' rows in with one in-place NCCL all-reduce on the
+ * game's stream (inside the solver's CUDA graph).  The rows are disjoint, so the sum is exact
+ * and every rank holds the full gradient and the same (replicated) iterates.
+ * id: HOST EGT_NCCL_ID_BYTES bytes from egt_nccl_unique_id on rank 0, distributed by the
+ * caller; NULL only for world == 1 (no communicator; with an id a 1-rank communicator is
+ * built and used).  Call before egt_init / cfr_init (EGT_E_STATE otherwise).
+ * NCCL is opened at run time (libnccl.so.2); EGT_E_CUDA if it cannot be. */
+#define EGT_NCCL_ID_BYTES 128
+int egt_nccl_unique_id(uint8_t* out);
+int egt_shard(egt_game* game, int32_t rank, int32_t world, const uint8_t* id);
+
+/* Rows of the gradient that shard `rank` of `world` computes, without communication:
+ * DEVICE dout receives those rows, every other row 0 (the sum over all ranks is
+ * egt_gradient's result).  Synchronous.  For tests and inspection. */
+int egt_gradient_rows(egt_game* game, int32_t player, int32_t rank, int32_t world, const double* dev_in,
+                      double* dev_out);
+
 /* ---- kernel timing (measurement only) -------------------------------------------
  * egt_timing(game, 1) switches egt_step / cfr_step / saddle_gap* to eager launches,
  * each bracketed by a pair of CUDA events on the library's stream (the stream the
@@ -212,7 +233,8 @@ int egt_scalars(egt_game* game, double* host_out);
 #define EGT_KERNEL_GRAD_ATX 1 /* gradient kernel, player 1: A^T x      */
 #define EGT_KERNEL_TREE 2     /* treeplex kernel (SBR / prox / BR / CFR / combine) */
 #define EGT_KERNEL_SCALAR 3   /* per-game scalar kernels (EGT stepsizes, EGC accept, gap) */
-#define EGT_N_KERNEL_KINDS 4
+#define EGT_KERNEL_COMM 4     /* NCCL all-reduce of a sharded gradient (egt_shard) */
+#define EGT_N_KERNEL_KINDS 5
 int egt_timing(egt_game* game, int32_t enable);
 int egt_timing_get(egt_game* game, double* host_out);
 

@@ -57,9 +57,10 @@ EXPORTS = [
     "egt_pub_history", "egt_gradient", "egt_smoothed_br", "egt_prox", "egt_best_response",
     "egt_init", "egt_step", "cfr_init", "cfr_step", "saddle_gap", "get_avg_strategy",
     "get_strategy_device", "egt_scalars", "egt_last_error", "saddle_gap_device",
-    "egt_timing", "egt_timing_get",
+    "egt_timing", "egt_timing_get", "egt_nccl_unique_id", "egt_shard", "egt_gradient_rows",
 ]
-KERNEL_KINDS = ("grad_Ay", "grad_ATx", "tree", "scalar")
+KERNEL_KINDS = ("grad_Ay", "grad_ATx", "tree", "scalar", "comm")
+NCCL_ID_BYTES = 128
 
 _lib = None
 
@@ -101,6 +102,9 @@ def load_library():
         "saddle_gap_device": ([P, I32, VP], I32),
         "egt_timing": ([P, I32], I32),
         "egt_timing_get": ([P, ctypes.POINTER(D)], I32),
+        "egt_nccl_unique_id": ([ctypes.c_char_p], I32),
+        "egt_shard": ([P, I32, I32, ctypes.c_char_p], I32),
+        "egt_gradient_rows": ([P, I32, I32, I32, VP, VP], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -245,6 +249,19 @@ class Game:
         """Per-game eps_sad into a DEVICE fp64 [n_games] buffer, stream-ordered."""
         _check(self._L.saddle_gap_device(self._h, which, _ptr(dout)))
 
+    def gradient_rows(self, player, rank, world, din, dout):
+        """Rows shard `rank` of `world` computes (others 0), no communication."""
+        _check(self._L.egt_gradient_rows(self._h, player, rank, world, _ptr(din), _ptr(dout)))
+
+    def shard(self, rank, world, uid=None):
+        """Shard every gradient of this game over `world` ranks (C ABI egt_shard).  `uid`: the
+        NCCL unique id bytes from rank 0 (``nccl_unique_id``); with torch.distributed
+        initialised and uid None, rank 0 makes it and broadcasts it (host-side plumbing)."""
+        if world > 1 and uid is None:
+            uid = broadcast_uid(nccl_unique_id() if rank == 0 else None)
+        buf = None if uid is None else ctypes.create_string_buffer(bytes(uid), NCCL_ID_BYTES)
+        _check(self._L.egt_shard(self._h, rank, world, buf))
+
     def timing(self, enable):
         _check(self._L.egt_timing(self._h, int(bool(enable))))
 
@@ -275,6 +292,23 @@ def _host_ptr(a):
         assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
         return a.ctypes.data
     return a.data_ptr()  # pinned torch CPU tensor
+
+
+def nccl_unique_id():
+    """C ABI egt_nccl_unique_id: NCCL_ID_BYTES bytes (rank 0 makes it, all ranks use it)."""
+    L = load_library()
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    _check(L.egt_nccl_unique_id(buf))
+    return buf.raw
+
+
+def broadcast_uid(uid):
+    """Rank 0's NCCL unique id to every rank over the initialised torch.distributed group."""
+    import torch.distributed as dist
+    box = [uid]
+    dist.broadcast_object_list(box, src=0)
+    assert box[0] is not None and len(box[0]) == NCCL_ID_BYTES
+    return box[0]
 
 
 def load_game(kind, **kw):

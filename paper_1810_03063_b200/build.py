@@ -49,7 +49,7 @@ def build(force=False, verbose=False):
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-Xcompiler", "-pthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl", "-Xcompiler", "-pthread"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     for o in objs:

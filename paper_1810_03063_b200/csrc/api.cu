@@ -1,7 +1,10 @@
 // C ABI (include/egt_b200.h): device layout upload, solver drivers, graphs.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only; the library is opened at run time (egt_shard)
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -32,7 +35,12 @@ enum SolverKind { SOLVER_NONE = 0, SOLVER_EGT = 1, SOLVER_CFR = 2 };
 struct egt_game {
     HostGame host;
     DevGame dg{};
-    DevPlayer dp[2]{};
+    DevPlayer dp[2]{};              // the view the solver launches (a row slice when sharded)
+    DevPlayer dp_full[2]{};         // all rows
+    // sharding (egt_shard): this rank computes a slice of every gradient's rows, then one
+    // NCCL all-reduce (sum) per gradient gives every rank the full gradient
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
     std::vector<void*> allocs;
     cudaStream_t st = nullptr;      // internal stream (graphs are captured here)
     cudaStream_t user = nullptr;    // caller's stream (nullptr = legacy default)
@@ -122,6 +130,93 @@ static int begin(egt_game* G) {
 static int end(egt_game* G) {
     CK(cudaEventRecord(G->ev_out, G->st));
     CK(cudaStreamWaitEvent(G->user, G->ev_out, 0));
+    return 0;
+}
+
+// ----------------------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+    void* lib = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* nccl_api(std::string& err) {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string load_err;
+    std::call_once(once, [] {
+        // an NCCL already in the process (e.g. torch's) is reused by soname
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            load_err = std::string("dlopen libnccl.so.2: ") + dlerror();
+            return;
+        }
+        api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+        api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+        api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+        api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
+        if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy || !api.errStr) {
+            load_err = "libnccl.so.2 lacks a required symbol";
+            return;
+        }
+        api.lib = h;
+    });
+    if (!api.lib) {
+        err = load_err;
+        return nullptr;
+    }
+    return &api;
+}
+
+static void nccl_destroy(ncclComm_t c) {
+    std::string e;
+    if (NcclApi* a = nccl_api(e)) a->commDestroy(c);
+}
+
+// Rows of player p's gradient that shard `rank` of `world` computes: a contiguous range of
+// the sequences that end a terminal, balanced by terminal count, split into chunks of
+// <= GRAD_CHUNK_TERMS terminals (relative to the range) for the staged kernel.
+static void shard_rows(const PlayerLayout& L, int rank, int world, int& r0, int& r1, std::vector<int>& chunks) {
+    const int n = (int)L.rows_term.size();
+    std::vector<long long> cum(n + 1, 0);
+    for (int r = 0; r < n; ++r) cum[r + 1] = cum[r] + (L.term_off[L.rows_term[r] + 1] - L.term_off[L.rows_term[r]]);
+    auto bound = [&](int k) {
+        const long long target = cum[n] * k / world;
+        return (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+    };
+    r0 = rank == 0 ? 0 : bound(rank);
+    r1 = rank + 1 == world ? n : bound(rank + 1);
+    chunks.assign(1, 0);
+    for (int r = r0, cnt = 0; r < r1; ++r) {
+        cnt += (int)(cum[r + 1] - cum[r]);
+        if (cnt >= GRAD_CHUNK_TERMS || r + 1 == r1) {
+            chunks.push_back(r + 1 - r0);
+            cnt = 0;
+        }
+    }
+}
+
+// A DevPlayer view restricted to shard `rank` of `world` (device chunk table allocated into allocs).
+static int make_slice(egt_game* G, int p, int rank, int world, DevPlayer& out, std::vector<void*>& allocs) {
+    int r0, r1;
+    std::vector<int> chunks;
+    shard_rows(G->host.pl[p], rank, world, r0, r1, chunks);
+    out = G->dp_full[p];
+    out.rows_term = G->dp_full[p].rows_term + r0;
+    out.n_rows_term = r1 - r0;
+    out.n_chunks = (int)chunks.size() - 1;
+    void* d = nullptr;
+    if (cudaMalloc(&d, sizeof(int) * chunks.size()) != cudaSuccess)
+        return fail(EGT_E_CUDA, "cudaMalloc (shard chunks)");
+    allocs.push_back(d);
+    if (cudaMemcpy(d, chunks.data(), sizeof(int) * chunks.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(EGT_E_CUDA, "cudaMemcpy (shard chunks)");
+    out.chunk_off = (const int*)d;
     return 0;
 }
 
@@ -274,6 +369,8 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         }
         G->V[p] = (long long)L.n_pub * Hp;
     }
+    G->dp_full[0] = G->dp[0];
+    G->dp_full[1] = G->dp[1];
     const int max_tiles = (H.H + 31) / 32;
     TRY(dalloc(G, &G->partial, (size_t)Gn * max_tiles));
     TRY(dalloc(G, &G->counter, (size_t)Gn));
@@ -327,6 +424,7 @@ extern "C" void egt_free_game(egt_game* G) {
         cudaEventDestroy(p.b);
     }
     for (cudaEvent_t e : G->ev_pool) cudaEventDestroy(e);
+    if (G->comm) nccl_destroy(G->comm);
     for (void* p : G->allocs) cudaFree(p);
     if (G->ev_in) cudaEventDestroy(G->ev_in);
     if (G->ev_out) cudaEventDestroy(G->ev_out);
@@ -390,12 +488,77 @@ extern "C" int egt_pub_history(const egt_game* G, int32_t player, int32_t s, cha
 }
 
 // ----------------------------------------------------------------------------- kernel-level
+static cudaError_t allreduce_grad(egt_game* G, int p, VecRef out);
+
 extern "C" int egt_gradient(egt_game* G, int32_t player, const double* din, double* dout) {
     if (!G || !din || !dout || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
     if (begin(G)) return EGT_E_CUDA;
-    CK(launch_gradient(G->dg, G->dp[player], player, vec(const_cast<double*>(din), G->V[1 - player]),
-                       vec(dout, G->V[player]), nullptr, 0, 1, G->st));
+    VecRef out = vec(dout, G->V[player]);
+    CK(launch_gradient(G->dg, G->dp[player], player, vec(const_cast<double*>(din), G->V[1 - player]), out,
+                       nullptr, 0, 1, G->st));
+    CK(allreduce_grad(G, player, out));
     return end(G);
+}
+
+extern "C" int egt_gradient_rows(egt_game* G, int32_t player, int32_t rank, int32_t world, const double* din,
+                                 double* dout) {
+    if (!G || !din || !dout || player < 0 || player > 1 || world < 1 || rank < 0 || rank >= world)
+        return fail(EGT_E_ARG, "bad argument");
+    std::vector<void*> tmp;
+    DevPlayer P;
+    int r = make_slice(G, player, rank, world, P, tmp);
+    if (!r && begin(G)) r = EGT_E_CUDA;
+    if (!r) {
+        cudaError_t e = launch_gradient(G->dg, P, player, vec(const_cast<double*>(din), G->V[1 - player]),
+                                        vec(dout, G->V[player]), nullptr, 0, 1, G->st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(G->st);
+        if (e != cudaSuccess) r = fail(EGT_E_CUDA, std::string("egt_gradient_rows: ") + cudaGetErrorString(e));
+    }
+    for (void* q : tmp) cudaFree(q);
+    if (r) return r;
+    return end(G);
+}
+
+extern "C" int egt_nccl_unique_id(uint8_t* out) {
+    if (!out) return fail(EGT_E_ARG, "null argument");
+    std::string err;
+    NcclApi* a = nccl_api(err);
+    if (!a) return fail(EGT_E_CUDA, err);
+    ncclUniqueId id;
+    ncclResult_t r = a->getUniqueId(&id);
+    if (r != ncclSuccess) return fail(EGT_E_CUDA, std::string("ncclGetUniqueId: ") + a->errStr(r));
+    static_assert(sizeof(ncclUniqueId) == EGT_NCCL_ID_BYTES, "NCCL unique id size");
+    memcpy(out, &id, sizeof(id));
+    return 0;
+}
+
+extern "C" int egt_shard(egt_game* G, int32_t rank, int32_t world, const uint8_t* id) {
+    if (!G || world < 1 || rank < 0 || rank >= world || (world > 1 && !id)) return fail(EGT_E_ARG, "bad argument");
+    if (G->solver != SOLVER_NONE) return fail(EGT_E_STATE, "egt_shard must precede egt_init / cfr_init");
+    if (G->comm) {
+        nccl_destroy(G->comm);
+        G->comm = nullptr;
+    }
+    G->rank = rank;
+    G->world = world;
+    for (int p = 0; p < 2; ++p) {
+        int r = make_slice(G, p, rank, world, G->dp[p], G->allocs);
+        if (r) return r;
+    }
+    if (id) {  // world == 1 with an id still builds a (1-rank) communicator: the same path
+        std::string err;
+        NcclApi* a = nccl_api(err);
+        if (!a) return fail(EGT_E_CUDA, err);
+        ncclUniqueId uid;
+        memcpy(&uid, id, sizeof(uid));
+        ncclResult_t r = a->commInitRank(&G->comm, world, uid, rank);
+        if (r != ncclSuccess) return fail(EGT_E_CUDA, std::string("ncclCommInitRank: ") + a->errStr(r));
+    }
+    if (G->graph) {
+        cudaGraphExecDestroy(G->graph);
+        G->graph = nullptr;
+    }
+    return 0;
 }
 
 static TreeArgs base_args() { return TreeArgs(); }
@@ -518,9 +681,25 @@ static cudaError_t tree(egt_game* G, int p, const TreeArgs& A) {
     return timed(G, EGT_KERNEL_TREE, active_games(G, A.mask, A.want),
                  [&] { return launch_tree(G->dg, G->dp[p], p, A, G->st); });
 }
+// the other ranks' rows of a sharded gradient, summed in by an in-place NCCL all-reduce
+static cudaError_t allreduce_grad(egt_game* G, int p, VecRef out) {
+    if (!G->comm) return cudaSuccess;
+    std::string err;
+    NcclApi* a = nccl_api(err);
+    if (!a || out.slot_sel) return cudaErrorInvalidValue;
+    const size_t count = (size_t)G->host.n_games * G->V[p];
+    return timed(G, EGT_KERNEL_COMM, G->host.n_games, [&] {
+        return a->allReduce(out.base, out.base, count, ncclDouble, ncclSum, G->comm, G->st) == ncclSuccess
+                   ? cudaSuccess
+                   : cudaErrorUnknown;
+    });
+}
+
 static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0) {
-    return timed(G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
-                 [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st); });
+    cudaError_t e = timed(G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
+                          [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st); });
+    if (e != cudaSuccess) return e;
+    return allreduce_grad(G, p, out);
 }
 template <class F>
 static cudaError_t scalar_k(egt_game* G, F&& launch) {

@@ -528,17 +528,20 @@ static bool staged_ok(const DevGame& G) {
 
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
                             const int* mask, int want, int all_rows, cudaStream_t st) {
-    const int rows = all_rows ? P.n_pub : P.n_rows_term;
-    if (rows == 0) return cudaSuccess;
-    if (staged_ok(G) && (!all_rows || gout.slot_sel == nullptr)) {
-        if (all_rows) {
-            // rows that end no terminal are 0; the staged kernel writes the others
-            for (int g = 0; g < G.n_games; ++g) {
-                cudaError_t e = cudaMemsetAsync(gout.base + (size_t)g * gout.game_stride, 0,
-                                                sizeof(double) * (size_t)P.n_pub * G.H_pad, st);
-                if (e != cudaSuccess) return e;
-            }
-        }
+    if (all_rows) {
+        // rows that end no terminal (or that another shard computes) are 0
+        if (gout.slot_sel) return cudaErrorInvalidValue;
+        cudaError_t e = cudaSuccess;
+        const size_t row_block = sizeof(double) * (size_t)P.n_pub * G.H_pad;
+        if (gout.game_stride == (long long)P.n_pub * G.H_pad)
+            e = cudaMemsetAsync(gout.base, 0, row_block * G.n_games, st);
+        else
+            for (int g = 0; g < G.n_games && e == cudaSuccess; ++g)
+                e = cudaMemsetAsync(gout.base + (size_t)g * gout.game_stride, 0, row_block, st);
+        if (e != cudaSuccess) return e;
+    }
+    if (P.n_rows_term == 0) return cudaSuccess;
+    if (staged_ok(G)) {
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
         const int gl = staged_gl_log2(G);
@@ -550,9 +553,9 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
                 <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
         return cudaGetLastError();
     }
-    dim3 grid(rows, G.n_games);
+    dim3 grid(P.n_rows_term, G.n_games);
     grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX><<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout,
-                                                                                         mask, want, all_rows);
+                                                                                         mask, want, 0);
     return cudaGetLastError();
 }
 

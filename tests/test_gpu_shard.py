@@ -1,0 +1,92 @@
+"""Row 8: one game sharded over ranks by terminal rows, NCCL all-reduce per gradient.
+
+On one GPU the ranks cannot run concurrently (B200_PROFILING.md), so the sharded
+arithmetic is checked by emulation -- every rank's slice computed on the same device
+(egt_gradient_rows) must sum, bit for bit, to the unsharded gradient -- and the NCCL path
+itself runs with a 1-rank communicator inside the solver's CUDA graph."""
+import numpy as np
+import pytest
+
+from paper_1810_03063_b200 import workloads
+from tests.paritylib import Pair
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _random_vec(G, p, seed):
+    rng = np.random.default_rng(seed)
+    v = rng.random((G.n_games, G.n_pub[p], G.H_pad))
+    v[:, :, G.H:] = 0.0
+    v[:, 0, :G.H] = 1.0
+    return torch.tensor(v, dtype=torch.float64, device="cuda")
+
+
+@pytest.mark.parametrize("kind,world", [("river", 2), ("river", 3), ("river", 8), ("leduc", 2), ("kuhn", 3),
+                                        ("libratus", 8)])
+def test_slices_sum_to_full_gradient(kind, world):
+    if kind == "libratus":
+        pair = Pair("river", n_games=4, spec=workloads.river_spec("libratus"), seed=5, sample=[])
+    elif kind == "river":
+        pair = Pair("river", n_games=3, seed=2, sample=[])
+    else:
+        pair = Pair(kind, n_games=2)
+    G = pair.game
+    for p in (0, 1):
+        din = _random_vec(G, 1 - p, 10 + p)
+        full = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
+        G.egt_gradient(p, din, full)
+        acc = torch.zeros_like(full)
+        touched = torch.zeros_like(full, dtype=torch.int32)
+        for r in range(world):
+            part = torch.full_like(full, np.nan)
+            G.gradient_rows(p, r, world, din, part)
+            assert torch.isfinite(part).all()
+            touched += (part != 0).int()
+            acc += part
+        assert torch.equal(acc, full)           # disjoint rows: the sum is exact
+        assert int(touched.max()) <= 1          # no row computed by two ranks
+
+
+def test_nccl_unique_id():
+    import paper_1810_03063_b200 as P
+    uid = P.binding.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == P.binding.NCCL_ID_BYTES
+
+
+@pytest.mark.parametrize("solver", ["egt_as", "cfr_plus"])
+def test_one_rank_nccl_solver_is_identical(solver):
+    """The sharded solver with a real (1-rank) NCCL communicator inside the CUDA graph
+    reproduces the unsharded solver exactly."""
+    import paper_1810_03063_b200 as P
+    spec = workloads.river_spec("simple")
+    boards = workloads.random_boards(4, 31)
+    p1, p2 = workloads.random_priors(boards, 31)
+    games = []
+    for sharded in (False, True):
+        G = P.Game(P.RIVER, n_games=4, river=spec, boards=boards, prior1=p1, prior2=p2)
+        if sharded:
+            G.shard(0, 1, uid=P.binding.nccl_unique_id())
+        if solver == "egt_as":
+            G.egt_init(P.EGT_AS, 50.0, 50.0)
+            G.egt_step(6)
+        else:
+            G.cfr_init(P.CFR_PLUS)
+            G.cfr_step(6)
+        games.append(G)
+    for p in (0, 1):
+        a = torch.zeros(games[0].vec_shape(p), dtype=torch.float64, device="cuda")
+        b = torch.zeros_like(a)
+        games[0].get_strategy_device(p, 1, a)
+        games[1].get_strategy_device(p, 1, b)
+        assert torch.equal(a, b)
+    assert np.array_equal(games[0].saddle_gap(1), games[1].saddle_gap(1))
+    kt = None
+    games[1].timing(True)
+    if solver == "egt_as":
+        games[1].egt_step(1)
+    else:
+        games[1].cfr_step(1)
+    kt = games[1].timing_get()
+    games[1].timing(False)
+    assert kt["comm"][1] >= 2                    # the all-reduces ran

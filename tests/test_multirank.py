@@ -60,3 +60,22 @@ def test_single_rank_defaults():
     import bench
     assert bench.max_over_ranks(3.5, 1) == 3.5
     assert bench.throughput(296, 1, 10, 1000.0) == 6 * 296 * 10
+
+
+def _uid_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1810_03063_b200 import binding
+    uid = bytes(range(128)) if rank == 0 else None
+    out[rank] = binding.broadcast_uid(uid)
+    dist.destroy_process_group()
+
+
+def test_nccl_uid_broadcast_gloo():
+    """Row 8's host plumbing: rank 0's NCCL unique id reaches every rank."""
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_uid_worker, args=(2, port, out), nprocs=2, join=True)
+        res = dict(out)
+    assert res[0] == res[1] == bytes(range(128))
