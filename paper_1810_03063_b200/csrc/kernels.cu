@@ -663,6 +663,112 @@ __device__ __forceinline__ double tree_node_up(const TreeNodeCtx& C, const DevPl
     return v;
 }
 
+// The same bottom-up work for a node with a compile-time number of actions N: the N
+// entries are read once into registers and written once.
+template <int N>
+__device__ __forceinline__ double tree_node_up_n(const TreeNodeCtx& C, const DevPlayer& P, double* col, int first,
+                                                 int m, int h, int Hp, double logn, double* __restrict__ cz,
+                                                 double* __restrict__ rg) {
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = col[a * TH_HANDS];
+    const int mode = C.mode;
+    double value;
+    if (mode == TM_SBR) {
+        const double wgt = C.mu * P.beta[(size_t)m * Hp + h];
+        const double iw = 1.0 / wgt;
+        double mn = x[0];
+#pragma unroll
+        for (int a = 1; a < N; ++a) mn = fmin(mn, x[a]);
+        double S = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            x[a] = exp_nonpos((mn - x[a]) * iw, C.exptab);
+            S += x[a];
+        }
+        const double inv = 1.0 / S;
+#pragma unroll
+        for (int a = 0; a < N; ++a) x[a] *= inv;
+        value = mn - wgt * (log(S) - logn);
+    } else if (mode == TM_PROX) {
+        const double beta = P.beta[(size_t)m * Hp + h];
+        const double ib = 1.0 / beta;
+        const double* __restrict__ zr = cz + (size_t)first * Hp + h;
+        double z[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) z[a] = zr[(size_t)a * Hp];
+        double mn = DBL_MAX;
+#pragma unroll
+        for (int a = 0; a < N; ++a)
+            if (z[a] > 0.0) mn = fmin(mn, x[a]);
+        double S = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            x[a] = z[a] > 0.0 ? z[a] * exp_nonpos((mn - x[a]) * ib, C.exptab) : 0.0;
+            S += x[a];
+        }
+        const double inv = 1.0 / S;
+#pragma unroll
+        for (int a = 0; a < N; ++a) x[a] *= inv;
+        value = mn - beta * log(S);
+    } else if (mode == TM_BR) {
+        int best = 0;
+        double mn = x[0];
+#pragma unroll
+        for (int a = 1; a < N; ++a)
+            if (x[a] < mn) {
+                mn = x[a];
+                best = a;
+            }
+#pragma unroll
+        for (int a = 0; a < N; ++a) x[a] = a == best ? 1.0 : 0.0;
+        value = mn;
+    } else {
+        double z[N], r[N];
+        const size_t ix0 = (size_t)first * Hp + h;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            z[a] = cz[ix0 + (size_t)a * Hp];
+            r[a] = rg[ix0 + (size_t)a * Hp];
+        }
+        double v = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) v += x[a] * z[a];
+        double S = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            const double u = x[a], r0 = r[a];
+            double rr = r0 + u - v;
+            if (C.cfr_plus) rr = fmax(rr, 0.0);
+            rg[ix0 + (size_t)a * Hp] = rr;
+            const double tol = 1e-13 * (fabs(r0) + fabs(u) + fabs(v));  // DESIGN.md R15
+            x[a] = rr > tol ? rr : 0.0;
+            S += x[a];
+        }
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            x[a] = S > 0.0 ? x[a] / S : 1.0 / N;
+            cz[ix0 + (size_t)a * Hp] = x[a];
+        }
+        value = v;
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a) col[a * TH_HANDS] = x[a];
+    return value;
+}
+
+__device__ __forceinline__ double tree_node_up_any(const TreeNodeCtx& C, const DevPlayer& P, double* col, int first,
+                                                   int n, int m, int h, int Hp, double logn, double* __restrict__ cz,
+                                                   double* __restrict__ rg) {
+    switch (n) {  // warp-uniform: every lane works on the same node
+#define EGT_NODE_CASE(K) \
+    case K: return tree_node_up_n<K>(C, P, col, first, m, h, Hp, logn, cz, rg);
+        EGT_NODE_CASE(1) EGT_NODE_CASE(2) EGT_NODE_CASE(3) EGT_NODE_CASE(4)
+#undef EGT_NODE_CASE
+        default: return tree_node_up(C, P, col, first, n, m, h, Hp, logn, cz, rg);
+    }
+}
+
 __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
     extern __shared__ __align__(16) double tile[];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -745,7 +851,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
                     double* col = tile + (size_t)first * TH_HANDS + c;
                     double value = 0.0;
                     if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]))
-                        value = tree_node_up(C, P, col, first, n, m, h, Hp, logn, cz, rg);
+                        value = tree_node_up_any(C, P, col, first, n, m, h, Hp, logn, cz, rg);
                     else
                         for (int a = 0; a < n; ++a) col[a * TH_HANDS] = 0.0;
                     if (rs >= 0) rootv[rs * TH_HANDS + c] = value;
