@@ -769,6 +769,65 @@ __device__ __forceinline__ double tree_node_up_any(const TreeNodeCtx& C, const D
     }
 }
 
+// Top-down work of simplex (node, hand): q_i = q_{p_j} * qbar_i and the requested output rows.
+// All global reads of the node are issued before any use (one round trip per node).
+struct TreeDownCtx {
+    int mode;
+    double tau, alpha;
+    const double* __restrict__ bin;
+    const double* __restrict__ ci;
+    double* __restrict__ ob;
+    double* __restrict__ oq;
+    double* __restrict__ co;
+    double* __restrict__ av;
+};
+
+template <int N>
+__device__ __forceinline__ void tree_node_down_n(const TreeDownCtx& D, bool ok, double qp, double unif, int first,
+                                                 double* col, int h, int Hp) {
+    const size_t ix0 = (size_t)first * Hp + h;
+    double b[N], cv[N], avv[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+        if (!ok) b[a] = 0.0;
+        else if (D.mode == TM_UNIFORM) b[a] = unif;
+        else if (D.mode == TM_COMBINE) b[a] = D.bin[ix0 + (size_t)a * Hp];
+        else b[a] = col[a * TH_HANDS];
+        cv[a] = D.co ? D.ci[ix0 + (size_t)a * Hp] : 0.0;
+        avv[a] = D.av ? D.av[ix0 + (size_t)a * Hp] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+        const double q = qp * b[a];
+        col[a * TH_HANDS] = q;
+        const size_t ix = ix0 + (size_t)a * Hp;
+        if (D.ob) D.ob[ix] = b[a];
+        if (D.oq) D.oq[ix] = q;
+        if (D.co) D.co[ix] = (1.0 - D.tau) * cv[a] + D.tau * q;
+        if (D.av) D.av[ix] = D.alpha * q + (1.0 - D.alpha) * avv[a];
+    }
+}
+
+__device__ __forceinline__ void tree_node_down_any(const TreeDownCtx& D, bool ok, double qp, int first, int n,
+                                                   double* col, int h, int Hp) {
+    const double unif = 1.0 / n;
+    switch (n) {
+        case 1: tree_node_down_n<1>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 2: tree_node_down_n<2>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 3: tree_node_down_n<3>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 4: tree_node_down_n<4>(D, ok, qp, unif, first, col, h, Hp); return;
+        default: break;
+    }
+    for (int a0 = 0; a0 < n; a0 += 4) {  // wider nodes: four actions per round trip
+        const int k = min(4, n - a0);
+        double* c0 = col + a0 * TH_HANDS;
+        if (k == 4) tree_node_down_n<4>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 3) tree_node_down_n<3>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 2) tree_node_down_n<2>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else tree_node_down_n<1>(D, ok, qp, unif, first + a0, c0, h, Hp);
+    }
+}
+
 __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
     extern __shared__ __align__(16) double tile[];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -910,6 +969,16 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
         alpha = A.avg_linear ? 2.0 * t / (t * t + t) : 1.0 / t;
     }
     const double* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
+    TreeDownCtx Dn;
+    Dn.mode = mode;
+    Dn.tau = tau;
+    Dn.alpha = alpha;
+    Dn.bin = bin;
+    Dn.ci = ci;
+    Dn.ob = ob;
+    Dn.oq = oq;
+    Dn.co = co;
+    Dn.av = av;
     if (wid == 0) {
 #pragma unroll
         for (int j = 0; j < TH_HPL; ++j) {
@@ -934,23 +1003,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
                 const int c = lane + 32 * j, h = h0 + c;
                 const bool ok = h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
                 const double qp = par == 0 ? (ok ? 1.0 : 0.0) : tile[par * TH_HANDS + c];
-                for (int a = 0; a < n; ++a) {
-                    const int s = first + a;
-                    double b;
-                    if (!ok) b = 0.0;
-                    else if (mode == TM_UNIFORM) b = 1.0 / n;
-                    else if (mode == TM_COMBINE) b = bin[(size_t)s * Hp + h];
-                    else b = tile[s * TH_HANDS + c];
-                    const double q = qp * b;
-                    tile[s * TH_HANDS + c] = q;
-                    if (h < Hp) {
-                        const size_t ix = (size_t)s * Hp + h;
-                        if (ob) ob[ix] = b;
-                        if (oq) oq[ix] = q;
-                        if (co) co[ix] = (1.0 - tau) * ci[ix] + tau * q;
-                        if (av) av[ix] = alpha * q + (1.0 - alpha) * av[ix];
-                    }
-                }
+                tree_node_down_any(Dn, ok, qp, first, n, tile + (size_t)first * TH_HANDS + c, h, Hp);
             }
         }
         __syncthreads();
