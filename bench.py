@@ -56,6 +56,8 @@ def parse():
                     help="also time EGT/as and CFR+ to eps_sad <= --eps-mbb on this many endgames (0: skip)")
     ap.add_argument("--eps-mbb", type=float, default=1.0, help="target saddle gap in milli-big-blinds")
     ap.add_argument("--converge-max-steps", type=int, default=4000)
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                    help="f32: the optional fp32 mode (fp32 vectors and arithmetic, DESIGN.md row 9)")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: every rank holds the same batch and computes a slice of each "
                          "gradient's rows, NCCL all-reduce per gradient (DESIGN.md row 8)")
@@ -199,12 +201,13 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- roofline
-def grad_bytes_per_game(game, player):
+def grad_bytes_per_game(game, player, esz=8):
     """Compulsory HBM bytes of one gradient evaluation of one game: read
     the rows of the other player's vector that terminals end on, write the rows of this
     player's gradient that can be nonzero (sequences ending a terminal; the others are
     identically 0), read both hand priors -- H hands, fp64."""
-    return 8 * game.H * (game.grad_rows_read[player] + game.grad_rows_written[player] + 2)
+    esz = 4 if getattr(game, "precision", "f64") == "f32" else 8
+    return esz * game.H * (game.grad_rows_read[player] + game.grad_rows_written[player] + 2)
 
 
 def measured_peak():
@@ -332,7 +335,8 @@ def run_b200(args):
     P.load_library()
 
     spec, boards, p1, p2 = workload(args, 0 if args.shard else rank)
-    game = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2)
+    game = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2,
+                  precision=args.precision)
     stream = torch.cuda.current_stream()
     game.set_stream(stream)
     if args.shard:
@@ -401,7 +405,7 @@ def run_b200(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f64",
+                "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": args.precision,
                 "data": "synthetic",
                 "config": dict(workload_config(args, game, world),
                                l2="no flush: per-step working set %.0f MB > 126 MB L2" %
@@ -421,7 +425,8 @@ def run_b200(args):
             dist.barrier()
         pinned = torch.zeros(args.batch, dtype=torch.float64).pin_memory()
         t0 = time.perf_counter()
-        g2 = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2)
+        g2 = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2,
+                    precision=args.precision)
         if args.shard:
             g2.shard(rank, world)
         g2.egt_init(P.EGT_AS)

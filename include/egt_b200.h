@@ -8,7 +8,9 @@
  * its own board and hand priors).  x is player 1 (moves first, "Libratus",
  * minimises), y is player 2.  A is player 2's payoff.  A is never materialised.
  *
- * Vector layout (device, fp64): for player p, a vector holds, per game g, a
+ * Vector layout (device; elements fp64, or fp32 for games loaded with precision EGT_F32 --
+ * every device vector argument below is then a float buffer, while per-game scalars such
+ * as mu, step sizes and values stay fp64): for player p, a vector holds, per game g, a
  * row-major [n_pub[p]][H_pad] block; row 0 is the empty sequence (value 1 in a
  * strategy, the value/constant term in a gradient; R1), row s >= 1 is
  * public sequence s (a decision node of p and one of its actions) for every
@@ -75,7 +77,11 @@ typedef struct {
     const int32_t* boards;    /* HOST [n_games][5] card ids (rank_pos*n_suits + suit) */
     const double* prior1;     /* HOST [n_games][n_combos] canonical combos (c1<c2 lexicographic), >= 0; NULL = uniform */
     const double* prior2;     /* as prior1, for player 2 */
+    int32_t precision;        /* EGT_F64 (0, default) or EGT_F32: element type of every vector */
 } egt_game_spec;
+
+#define EGT_F64 0 /* fp64 vectors and arithmetic (parity 1e-9 with the oracle) */
+#define EGT_F32 1 /* optional fp32 mode: fp32 vectors and arithmetic, fp64 per-game scalars (1e-5) */
 
 typedef struct egt_game egt_game; /* opaque */
 
@@ -96,6 +102,7 @@ typedef struct {
      * nonzero (sequences that end a terminal) -- the compulsory traffic */
     int32_t grad_rows_read[2];
     int32_t grad_rows_written[2];
+    int32_t precision;     /* EGT_F64 or EGT_F32 */
 } egt_game_info;
 
 /* ---- game ---------------------------------------------------------------- */

@@ -38,6 +38,7 @@ class Spec(ctypes.Structure):
         ("boards", ctypes.POINTER(ctypes.c_int32)),
         ("prior1", ctypes.POINTER(ctypes.c_double)),
         ("prior2", ctypes.POINTER(ctypes.c_double)),
+        ("precision", ctypes.c_int32),
     ]
 
 
@@ -49,6 +50,7 @@ class Info(ctypes.Structure):
         ("vec_stride", ctypes.c_int64 * 2), ("max_abs_A", ctypes.c_double * 1),
         ("h2d_bytes", ctypes.c_int64),
         ("grad_rows_read", ctypes.c_int32 * 2), ("grad_rows_written", ctypes.c_int32 * 2),
+        ("precision", ctypes.c_int32),
     ]
 
 
@@ -128,10 +130,14 @@ def _ptr(x):
     return x.data_ptr()
 
 
-def _spec_from(kind, n_games, river, boards, prior1, prior2, n_ranks, n_suits):
+F64, F32 = 0, 1
+
+
+def _spec_from(kind, n_games, river, boards, prior1, prior2, n_ranks, n_suits, precision=F64):
     s = Spec()
     s.kind = kind
     s.n_games = n_games
+    s.precision = {"f64": F64, "f32": F32}.get(precision, precision)
     keep = []
     if kind == RIVER:
         s.pot, s.stack = river["pot"], river["stack"]
@@ -159,9 +165,11 @@ class Game:
     """A batch of games sharing one public tree (C ABI handle ``egt_game``)."""
 
     def __init__(self, kind, n_games=1, river=None, boards=None, prior1=None, prior2=None,
-                 n_ranks=13, n_suits=4):
+                 n_ranks=13, n_suits=4, precision="f64"):
+        """precision: "f64" (default) or "f32" (the optional fp32 mode): element type of every
+        device vector of this game."""
         L = load_library()
-        spec, keep = _spec_from(kind, n_games, river, boards, prior1, prior2, n_ranks, n_suits)
+        spec, keep = _spec_from(kind, n_games, river, boards, prior1, prior2, n_ranks, n_suits, precision)
         h = ctypes.c_void_p()
         _check(L.egt_load_game(ctypes.byref(spec), ctypes.byref(h)))
         del keep
@@ -179,6 +187,8 @@ class Game:
         self.h2d_bytes = info.h2d_bytes
         self.grad_rows_read = (info.grad_rows_read[0], info.grad_rows_read[1])
         self.grad_rows_written = (info.grad_rows_written[0], info.grad_rows_written[1])
+        self.precision = "f32" if info.precision == F32 else "f64"
+        self.np_dtype = np.float32 if self.precision == "f32" else np.float64
 
     def close(self):
         if self._h:
@@ -210,6 +220,11 @@ class Game:
 
     def vec_shape(self, player):
         return (self.n_games, self.n_pub[player], self.H_pad)
+
+    @property
+    def torch_dtype(self):
+        import torch
+        return torch.float32 if self.precision == "f32" else torch.float64
 
     # ---- kernel-level calls (device buffers)
     def egt_gradient(self, player, din, dout):

@@ -41,6 +41,7 @@ struct egt_game {
     // NCCL all-reduce (sum) per gradient gives every rank the full gradient
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    int esz = 8;                    // bytes per vector element (8: fp64, 4: fp32 mode)
     std::vector<void*> allocs;
     cudaStream_t st = nullptr;      // internal stream (graphs are captured here)
     cudaStream_t user = nullptr;    // caller's stream (nullptr = legacy default)
@@ -91,6 +92,17 @@ static int dalloc(egt_game* G, T** p, size_t n) {
     if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     G->allocs.push_back(q);
     *p = (T*)q;
+    return 0;
+}
+
+// a per-game vector buffer of n elements in the game's precision (base address only)
+static int dalloc_vec(egt_game* G, double** p, size_t n) {
+    void* q = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&q, n * (size_t)G->esz);
+    if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    G->allocs.push_back(q);
+    *p = (double*)q;
     return 0;
 }
 
@@ -226,7 +238,9 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     *out = nullptr;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EGT_E_CUDA, "no CUDA device");
+    if (spec->precision != EGT_F64 && spec->precision != EGT_F32) return fail(EGT_E_ARG, "bad precision");
     egt_game* G = new egt_game();
+    G->esz = spec->precision == EGT_F32 ? 4 : 8;
     std::string err = build_host_game(*spec, G->host);
     if (!err.empty()) {
         delete G;
@@ -279,8 +293,17 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(upload(G, &d_pcard, pcard));
     TRY(upload(G, &d_valid, valid));
     double *d_p0, *d_p1, *d_kg;
-    TRY(upload(G, &d_p0, H.prior[0]));
-    TRY(upload(G, &d_p1, H.prior[1]));
+    if (G->esz == 8) {
+        TRY(upload(G, &d_p0, H.prior[0]));
+        TRY(upload(G, &d_p1, H.prior[1]));
+    } else {  // fp32 mode: priors in the vectors' precision
+        std::vector<float> f0(H.prior[0].begin(), H.prior[0].end()), f1(H.prior[1].begin(), H.prior[1].end());
+        float *q0, *q1;
+        TRY(upload(G, &q0, f0));
+        TRY(upload(G, &q1, f1));
+        d_p0 = (double*)q0;
+        d_p1 = (double*)q1;
+    }
     TRY(upload(G, &d_kg, H.kappa_game));
     std::vector<DevTerm> terms;
     for (const Terminal& t : H.terms) {
@@ -301,6 +324,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     G->dg.hand_size = H.hand_size;
     G->dg.n_bs = nbs;
     G->dg.n_cards = H.n_cards;
+    G->dg.esz = G->esz;
     G->dg.all_valid = H.all_valid;
     G->dg.tab_nvalid = d_nvalid;
     G->dg.tab_order = d_order;
@@ -363,7 +387,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         P.kid_off = ko;
         P.kids = kd;
         P.rows_term = rt;
-        if (tree_smem_bytes(P) > 200 * 1024) {
+        if (tree_smem_bytes(P, G->esz) > 200 * 1024) {
             egt_free_game(G);
             return fail(EGT_E_ARG, "public tree too large for the treeplex kernel's shared-memory tile");
         }
@@ -398,10 +422,10 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(dalloc(G, &G->gapout, (size_t)Gn));
     for (int p = 0; p < 2; ++p) {
         const size_t n = (size_t)Gn * G->V[p];
-        TRY(dalloc(G, &G->GR[p], n));
-        TRY(dalloc(G, &G->HAT[p], n));
+        TRY(dalloc_vec(G, &G->GR[p], n));
+        TRY(dalloc_vec(G, &G->HAT[p], n));
         // rows that end no terminal are never written by the solver's gradient launches
-        if (cudaMemset(G->GR[p], 0, n * sizeof(double)) != cudaSuccess) {
+        if (cudaMemset(G->GR[p], 0, n * G->esz) != cudaSuccess) {
             egt_free_game(G);
             return fail(EGT_E_CUDA, "memset");
         }
@@ -455,6 +479,7 @@ extern "C" int egt_game_info_get(const egt_game* G, egt_game_info* o) {
     o->n_terminals = (int)H.terms.size();
     o->max_abs_A[0] = 0.0;
     o->h2d_bytes = G->h2d_bytes;
+    o->precision = G->esz == 4 ? EGT_F32 : EGT_F64;
     for (int p = 0; p < 2; ++p) {
         std::vector<char> seen(H.pl[1 - p].n_pub, 0);
         for (const Terminal& t : H.terms)
@@ -617,9 +642,9 @@ static int ensure_egt_buffers(egt_game* G) {
     const int Gn = G->host.n_games;
     for (int p = 0; p < 2; ++p) {
         const size_t n = (size_t)Gn * G->V[p];
-        if (!G->S[p] && dalloc(G, &G->S[p], 2 * n)) return EGT_E_CUDA;
-        if (!G->C[p] && dalloc(G, &G->C[p], 2 * n)) return EGT_E_CUDA;
-        if (!G->RESP[p] && dalloc(G, &G->RESP[p], n)) return EGT_E_CUDA;
+        if (!G->S[p] && dalloc_vec(G, &G->S[p], 2 * n)) return EGT_E_CUDA;
+        if (!G->C[p] && dalloc_vec(G, &G->C[p], 2 * n)) return EGT_E_CUDA;
+        if (!G->RESP[p] && dalloc_vec(G, &G->RESP[p], n)) return EGT_E_CUDA;
     }
     return 0;
 }
@@ -689,7 +714,8 @@ static cudaError_t allreduce_grad(egt_game* G, int p, VecRef out) {
     if (!a || out.slot_sel) return cudaErrorInvalidValue;
     const size_t count = (size_t)G->host.n_games * G->V[p];
     return timed(G, EGT_KERNEL_COMM, G->host.n_games, [&] {
-        return a->allReduce(out.base, out.base, count, ncclDouble, ncclSum, G->comm, G->st) == ncclSuccess
+        return a->allReduce(out.base, out.base, count, G->esz == 8 ? ncclDouble : ncclFloat, ncclSum, G->comm,
+                            G->st) == ncclSuccess
                    ? cudaSuccess
                    : cudaErrorUnknown;
     });
@@ -977,10 +1003,10 @@ extern "C" int cfr_init(egt_game* G, int32_t variant) {
     const int Gn = G->host.n_games;
     for (int p = 0; p < 2; ++p) {
         const size_t n = (size_t)Gn * G->V[p];
-        if (!G->R[p] && dalloc(G, &G->R[p], n)) return EGT_E_CUDA;
-        if (!G->Z[p] && dalloc(G, &G->Z[p], n)) return EGT_E_CUDA;
-        if (!G->Q[p] && dalloc(G, &G->Q[p], n)) return EGT_E_CUDA;
-        if (!G->AVG[p] && dalloc(G, &G->AVG[p], n)) return EGT_E_CUDA;
+        if (!G->R[p] && dalloc_vec(G, &G->R[p], n)) return EGT_E_CUDA;
+        if (!G->Z[p] && dalloc_vec(G, &G->Z[p], n)) return EGT_E_CUDA;
+        if (!G->Q[p] && dalloc_vec(G, &G->Q[p], n)) return EGT_E_CUDA;
+        if (!G->AVG[p] && dalloc_vec(G, &G->AVG[p], n)) return EGT_E_CUDA;
     }
     if (begin(G)) return EGT_E_CUDA;
     if (zero_scalars(G)) return EGT_E_CUDA;
@@ -996,8 +1022,8 @@ extern "C" int cfr_init(egt_game* G, int32_t variant) {
     CK(cudaMemcpyAsync(G->sc.t, one.data(), sizeof(int) * Gn, cudaMemcpyHostToDevice, G->st));
     for (int p = 0; p < 2; ++p) {
         const size_t n = (size_t)Gn * G->V[p];
-        CK(cudaMemsetAsync(G->R[p], 0, n * sizeof(double), G->st));
-        CK(cudaMemsetAsync(G->AVG[p], 0, n * sizeof(double), G->st));
+        CK(cudaMemsetAsync(G->R[p], 0, n * G->esz, G->st));
+        CK(cudaMemsetAsync(G->AVG[p], 0, n * G->esz, G->st));
         TreeArgs U = base_args();
         U.mode = TM_UNIFORM;  // x^0 uniform at every simplex (Gen-CFR line 1)
         U.out_b = vec(G->Z[p], G->V[p]);
@@ -1114,11 +1140,13 @@ extern "C" int get_strategy_device(egt_game* G, int32_t player, int32_t which, d
         CK(cudaMemcpyAsync(cur.data(), G->sc.cur, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
         CK(cudaStreamSynchronize(G->st));
     }
+    const size_t es = (size_t)G->esz;
     for (int g = 0; g < Gn; ++g) {
-        const double* src = s[player].base + (size_t)g * G->V[player] +
-                            (s[player].slot_sel ? (size_t)(cur[g] & 1) * s[player].slot_stride : 0);
-        CK(cudaMemcpyAsync(dev_out + (size_t)g * G->V[player], src, sizeof(double) * G->V[player],
-                           cudaMemcpyDeviceToDevice, G->st));
+        const char* src = reinterpret_cast<const char*>(s[player].base) +
+                          es * ((size_t)g * G->V[player] +
+                                (s[player].slot_sel ? (size_t)(cur[g] & 1) * s[player].slot_stride : 0));
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(dev_out) + es * (size_t)g * G->V[player], src,
+                           es * G->V[player], cudaMemcpyDeviceToDevice, G->st));
     }
     return end(G);
 }
@@ -1128,16 +1156,21 @@ extern "C" int get_avg_strategy(egt_game* G, int32_t player, double* host_out) {
     const HostGame& H = G->host;
     const int Gn = H.n_games, Hp = H.H_pad, np = H.pl[player].n_pub;
     double* tmp = nullptr;
-    CK(cudaMalloc(&tmp, sizeof(double) * (size_t)Gn * G->V[player]));
+    const size_t ne = (size_t)Gn * G->V[player];
+    CK(cudaMalloc(&tmp, (size_t)G->esz * ne));
     int r = get_strategy_device(G, player, 1, tmp);
-    std::vector<double> h((size_t)Gn * G->V[player]);
+    std::vector<double> h(ne);
+    std::vector<float> hf(G->esz == 4 ? ne : 0);
     if (!r) {
-        cudaError_t e = cudaMemcpyAsync(h.data(), tmp, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, G->user);
+        cudaError_t e = G->esz == 8
+                            ? cudaMemcpyAsync(h.data(), tmp, sizeof(double) * ne, cudaMemcpyDeviceToHost, G->user)
+                            : cudaMemcpyAsync(hf.data(), tmp, sizeof(float) * ne, cudaMemcpyDeviceToHost, G->user);
         if (e == cudaSuccess) e = cudaStreamSynchronize(G->user);
         if (e != cudaSuccess) r = fail(EGT_E_CUDA, cudaGetErrorString(e));
     }
     cudaFree(tmp);
     if (r) return r;
+    if (G->esz == 4) std::copy(hf.begin(), hf.end(), h.begin());
     const int nc = H.n_combos;
     for (int g = 0; g < Gn; ++g)
         for (int s = 0; s < np; ++s) {

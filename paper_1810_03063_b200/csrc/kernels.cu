@@ -1,4 +1,4 @@
-// sm_100a kernels of the EGT / CFR hot path (fp64).
+// sm_100a kernels of the EGT / CFR hot path (fp64, or fp32 in the optional fp32 mode).
 //
 //  grad_kernel  : g = A y (player 0) or g = A^T x (player 1) without materialising A
 //                 (PAPER.md:299 gradient operators; Gen-CFR lines 29/35).
@@ -16,10 +16,11 @@
 namespace egt {
 
 // ------------------------------------------------------------------ warp helpers
-__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const double u = __shfl_up_sync(0xffffffffu, v, o);
+        const T u = __shfl_up_sync(0xffffffffu, v, o);
         if (lane >= o) v += u;
     }
     return v;
@@ -45,7 +46,18 @@ __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict_
     return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
+// fp32 mode: the library exp on non-positive arguments (<= 2 ulp)
+__device__ __forceinline__ float exp_nonpos(float x, const double* __restrict__) { return expf(x); }
+
+template <class T>
+__device__ __forceinline__ T big_value() { return sizeof(T) == 8 ? (T)DBL_MAX : (T)FLT_MAX; }
+
+// DESIGN.md R15: a regret at the rounding-noise level of its own update counts as 0
+template <class T>
+__device__ __forceinline__ T cfr_noise() { return sizeof(T) == 8 ? (T)1e-13 : (T)2e-6f; }
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
@@ -68,68 +80,69 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Pc: one segmented block scan over the card array (EPT consecutive slots per thread,
 // reset at each segment's first slot); each segment's end slot receives its total S_c.
 // Hands that do not share their tie group read their own P / Pc from registers.
-template <int NT, int KMAX, int EMAX>
+template <int NT, int KMAX, int EMAX, typename T>
 __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
                                                      const int* __restrict__ mask, int want, int all_rows) {
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    T* sm = reinterpret_cast<T*>(sm_raw);
     constexpr int NW = NT / 32;
-    __shared__ double wtot[NW];
-    __shared__ double segv[NW];
+    __shared__ T wtot[NW];
+    __shared__ T segv[NW];
     __shared__ int segf[NW];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
     const int s = all_rows ? (int)blockIdx.x : P.rows_term[blockIdx.x];
     const int Hp = G.H_pad, hs = G.hand_size, H = G.H, n_ce = G.n_ce;
     const bool fast = G.ident && G.all_valid;  // positions are hands and every hand is valid
-    double* w = sm;               // [Hp]   by position
-    double* Pf = w + Hp;          // [Hp+1] by position
-    double* Ex = Pf + Hp + 1;     // [n_ce] card array
-    double* acc = Ex + n_ce;      // [Hp]   by hand (general path only)
+    T* w = sm;               // [Hp]   by position
+    T* Pf = w + Hp;          // [Hp+1] by position
+    T* Ex = Pf + Hp + 1;     // [n_ce] card array
+    T* acc = Ex + n_ce;      // [Hp]   by hand (general path only)
     if (!fast)
-        for (int i = tid; i < Hp; i += NT) acc[i] = 0.0;
-    double racc[KMAX];
+        for (int i = tid; i < Hp; i += NT) acc[i] = T(0);
+    T racc[KMAX];
 #pragma unroll
-    for (int j = 0; j < KMAX; ++j) racc[j] = 0.0;
+    for (int j = 0; j < KMAX; ++j) racc[j] = T(0);
     const int t0 = P.term_off[s], t1 = P.term_off[s + 1];
-    const double* __restrict__ popp = (player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp;
-    const double* __restrict__ vo = vin.at(g);
-    const double kg = G.kappa_game[g];
-    const double sd_sign = player == 0 ? 1.0 : -1.0;
+    const T* __restrict__ popp = static_cast<const T*>(player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp;
+    const T* __restrict__ vo = vin.at<T>(g);
+    const T kg = (T)G.kappa_game[g];
+    const T sd_sign = player == 0 ? T(1) : T(-1);
     const int EPT = (n_ce + NT - 1) / NT;
     const int ebase = tid * EPT;
     for (int ti = t0; ti < t1; ++ti) {
-        const DevTerm T = G.terms[P.term_idx[ti]];
-        const int k = g * G.n_bs + T.bs;
+        const DevTerm tm = G.terms[P.term_idx[ti]];
+        const int k = g * G.n_bs + tm.bs;
         const int nv = G.tab_nvalid[k];
         const int16_t* __restrict__ order = G.tab_order + (size_t)k * Hp;
         const uint32_t* __restrict__ lohi = G.tab_lohi + (size_t)k * Hp;
         const uint16_t* __restrict__ cent = G.tab_cent + (size_t)k * n_ce;
         const uint2* __restrict__ pcard = G.tab_pcard + (size_t)k * Hp;
-        const int so = player ? T.seq[0] : T.seq[1];
-        const double* __restrict__ vrow = vo + (size_t)so * Hp;
-        const bool sd = T.kind == 2;
+        const int so = player ? tm.seq[0] : tm.seq[1];
+        const T* __restrict__ vrow = vo + (size_t)so * Hp;
+        const bool sd = tm.kind == 2;
         const int K = (nv + NT - 1) / NT;
         const int base = tid * K;
         __syncthreads();  // the previous terminal is done with w / Pf / Ex
         // ---- phase A: w (coalesced), then per-thread chunks of K positions, block scan
         for (int i = tid; i < nv; i += NT) {
             const int h = fast ? i : order[i];
-            w[i] = popp[h] * (so ? vrow[h] : 1.0);
+            w[i] = popp[h] * (so ? vrow[h] : T(1));
         }
         __syncthreads();
-        double x[KMAX];
-        double run = 0.0;
+        T x[KMAX];
+        T run = T(0);
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
             const int i = base + j;
-            x[j] = (j < K && i < nv) ? w[i] : 0.0;
+            x[j] = (j < K && i < nv) ? w[i] : T(0);
             run += x[j];
         }
-        const double incl = warp_incl_scan(run, lane);
+        const T incl = warp_incl_scan(run, lane);
         if (lane == 31) wtot[wid] = incl;
         // ---- phase B (local part): card-array chunk, segmented scan inside the thread
-        double ex[EMAX];
-        double srun = 0.0;
+        T ex[EMAX];
+        T srun = T(0);
         bool sflag = false;
         int first_flag = EMAX;
         unsigned endmask = 0u;
@@ -139,22 +152,22 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
             const bool in = j < EPT && e < n_ce;
             const unsigned c = in ? cent[e] : CE_END;
             if (in && (c & CE_FIRST)) {
-                srun = 0.0;
+                srun = T(0);
                 if (!sflag) first_flag = j;
                 sflag = true;
             }
             const unsigned pos = c & CE_END;
             if (pos == CE_END) endmask |= 1u << j;
-            const double y = pos != CE_END ? w[pos] : 0.0;
+            const T y = pos != CE_END ? w[pos] : T(0);
             ex[j] = srun;
             srun += y;
         }
         // segmented inclusive scan of (srun, sflag) over the warp
-        double sv = srun;
+        T sv = srun;
         int sf = sflag;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const double uv = __shfl_up_sync(0xffffffffu, sv, o);
+            const T uv = __shfl_up_sync(0xffffffffu, sv, o);
             const int uf = __shfl_up_sync(0xffffffffu, sf, o);
             if (lane >= o) {
                 if (!sf) sv += uv;
@@ -167,16 +180,16 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
         }
         __syncthreads();
         // block prefix of P
-        double wpre = 0.0, total = 0.0;
+        T wpre = T(0), total = T(0);
 #pragma unroll
         for (int q = 0; q < NW; ++q) {
-            const double v = wtot[q];
-            wpre += q < wid ? v : 0.0;
+            const T v = wtot[q];
+            wpre += q < wid ? v : T(0);
             total += v;
         }
-        const double pbase = wpre + incl - run;
+        const T pbase = wpre + incl - run;
         if (sd) {
-            double p = pbase;
+            T p = pbase;
 #pragma unroll
             for (int j = 0; j < KMAX; ++j) {
                 const int i = base + j;
@@ -187,40 +200,40 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
         }
         // carry into this thread's first segment: segmented exclusive prefix over threads
         {
-            double carry = 0.0;
+            T carry = T(0);
             for (int q = 0; q < wid; ++q) carry = segf[q] ? segv[q] : carry + segv[q];
-            const double pv = __shfl_up_sync(0xffffffffu, sv, 1);
+            const T pv = __shfl_up_sync(0xffffffffu, sv, 1);
             const int pf = __shfl_up_sync(0xffffffffu, sf, 1);
             if (lane > 0) carry = pf ? pv : carry + pv;
 #pragma unroll
             for (int j = 0; j < EMAX; ++j) {
                 const int e = ebase + j;
                 if (j < EPT && e < n_ce) {
-                    const double v = j < first_flag ? carry + ex[j] : ex[j];
+                    const T v = j < first_flag ? carry + ex[j] : ex[j];
                     if (sd || ((endmask >> j) & 1u)) Ex[e] = v;
                 }
             }
         }
         __syncthreads();
         // ---- phase C: per position
-        const double scale = T.kappa * kg * T.amount;
-        double pre = pbase;
+        const T scale = (T)(tm.kappa * G.kappa_game[g] * tm.amount);
+        T pre = pbase;
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
             const int i = base + j;
             if (j < K && i < nv) {
                 const uint2 pc = pcard[i];
-                double v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
+                T v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
                 if (hs == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
                 if (sd) {
                     const uint32_t lh = lohi[i];
                     const int lo = lh & 0xFFFFu, hi = lh >> 16;
                     if (lo == i && hi == i + 1) {
                         // alone in its tie group: its own prefixes
-                        const double ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
+                        const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
                         v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
                         if (hs == 2) {
-                            const double cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
+                            const T cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
                             v += cb + (cb + x[j]);
                         }
                     } else {
@@ -238,8 +251,8 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
             pre += x[j];
         }
     }
-    const double* __restrict__ pself = (player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
-    double* __restrict__ out = gout.at(g) + (size_t)s * Hp;
+    const T* __restrict__ pself = static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
+    T* __restrict__ out = gout.at<T>(g) + (size_t)s * Hp;
     __syncthreads();
     if (fast) {
         const int K = (H + NT - 1) / NT;
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
             if (j < K && i < H) w[i] = racc[j];
         }
         __syncthreads();
-        for (int i = tid; i < Hp; i += NT) out[i] = i < H ? pself[i] * w[i] : 0.0;
+        for (int i = tid; i < Hp; i += NT) out[i] = i < H ? pself[i] * w[i] : T(0);
     } else {
         for (int i = tid; i < Hp; i += NT) out[i] = pself[i] * acc[i];
     }
@@ -296,31 +309,32 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 // Card sums: every card's segment (seg_w slots) is scanned by one group of GL lanes (CH
 // slots each, GL * CH >= seg_w), so segments never straddle groups or warps.
-template <int NT, int K, int CH, int HS>
+template <int NT, int K, int CH, int HS, typename T>
 __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
                                                             VecRef gout, const int* __restrict__ mask, int want,
                                                             int gl_log2) {
-    extern __shared__ __align__(16) double sm[];
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    T* sm = reinterpret_cast<T*>(sm_raw);
     constexpr int NW = NT / 32, NP = NT * K;  // positions padded to NP
-    __shared__ double wtot[NW];
+    __shared__ T wtot[NW];
     __shared__ __align__(8) uint64_t bar[3];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
     const int Hp = G.H_pad, H = G.H, n_ce = G.n_ce, W = G.seg_w;
-    double* popp = sm;                 // [NP] (0 beyond H)
-    double* pself = popp + NP;         // [Hp]
-    double* vb = pself + Hp;           // [2][NP] opponent rows (0 beyond Hp)
-    double* w = vb + 2 * NP;           // [NP]
-    double* ob = w + NP;               // [Hp] output row staging
-    double* Pf = ob + Hp;              // [NP + 2]
-    double* Ex = Pf + NP + 2;          // [n_ce]
+    T* popp = sm;                 // [NP] (0 beyond H)
+    T* pself = popp + NP;         // [Hp]
+    T* vb = pself + Hp;           // [2][NP] opponent rows (0 beyond Hp)
+    T* w = vb + 2 * NP;           // [NP]
+    T* ob = w + NP;               // [Hp] output row staging
+    T* Pf = ob + Hp;              // [NP + 2]
+    T* Ex = Pf + NP + 2;          // [n_ce]
     uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [NP]
     uint32_t* lohi = reinterpret_cast<uint32_t*>(pcard + NP);        // [NP]
     uint16_t* cent = reinterpret_cast<uint16_t*>(lohi + NP);         // [n_ce]
     const int r0 = P.chunk_off[blockIdx.x], r1 = P.chunk_off[blockIdx.x + 1];
     const int T0 = P.term_off[P.rows_term[r0]], T1 = P.term_off[P.rows_term[r1 - 1] + 1];
-    const double* __restrict__ vo = vin.at(g);
-    double* __restrict__ outg = gout.at(g);
+    const T* __restrict__ vo = vin.at<T>(g);
+    T* __restrict__ outg = gout.at<T>(g);
     const int* __restrict__ tidx = P.term_idx;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -330,34 +344,34 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     }
     // padding beyond the copied ranges (never overwritten by the bulk copies)
     for (int i = Hp + tid; i < NP; i += NT) {
-        popp[i] = 0.0;
-        vb[i] = 0.0;
-        vb[NP + i] = 0.0;
+        popp[i] = T(0);
+        vb[i] = T(0);
+        vb[NP + i] = T(0);
         pcard[i] = make_uint2(0u, 0u);
         lohi[i] = 0u;
     }
-    for (int i = H + tid; i < Hp; i += NT) ob[i] = 0.0;
+    for (int i = H + tid; i < Hp; i += NT) ob[i] = T(0);
     __syncthreads();
     if (tid == 0) {
-        const unsigned bD = Hp * sizeof(double), bU2 = Hp * sizeof(uint2), bU = Hp * sizeof(uint32_t),
+        const unsigned bD = Hp * sizeof(T), bU2 = Hp * sizeof(uint2), bU = Hp * sizeof(uint32_t),
                        bC = n_ce * sizeof(uint16_t);
         mbar_expect_tx(&bar[0], 2 * bD + bU2 + bU + bC);
-        bulk_g2s(popp, (player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp, bD, &bar[0]);
-        bulk_g2s(pself, (player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp, bD, &bar[0]);
+        bulk_g2s(popp, static_cast<const T*>(player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp, bD, &bar[0]);
+        bulk_g2s(pself, static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp, bD, &bar[0]);
         bulk_g2s(pcard, G.tab_pcard + (size_t)g * Hp, bU2, &bar[0]);
         bulk_g2s(lohi, G.tab_lohi + (size_t)g * Hp, bU, &bar[0]);
         bulk_g2s(cent, G.tab_cent + (size_t)g * n_ce, bC, &bar[0]);
         for (int q = 0; q < 2 && T0 + q < T1; ++q) {
-            const DevTerm& T = G.terms[tidx[T0 + q]];
-            const int so = player ? T.seq[0] : T.seq[1];
+            const DevTerm& tm = G.terms[tidx[T0 + q]];
+            const int so = player ? tm.seq[0] : tm.seq[1];
             if (so) {
                 mbar_expect_tx(&bar[1 + q], bD);
                 bulk_g2s(vb + q * NP, vo + (size_t)so * Hp, bD, &bar[1 + q]);
             }
         }
     }
-    const double kg = G.kappa_game[g];
-    const double sd_sign = player == 0 ? 1.0 : -1.0;
+    
+    const T sd_sign = player == 0 ? T(1) : T(-1);
     const int base = tid * K;
     // card-array role: segment sgi, part of it [sbeg, sbeg + CH)
     const int GL = 1 << gl_log2;
@@ -365,17 +379,17 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     const bool has_seg = sgi < G.n_cards;
     const int sbeg = sgi * W + part * CH;
     const int send = has_seg ? min(sgi * W + W, sbeg + CH) : sbeg;
-    double racc[K];
+    T racc[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) racc[j] = 0.0;
+    for (int j = 0; j < K; ++j) racc[j] = T(0);
     unsigned par[2] = {0u, 0u};
     mbar_wait(&bar[0], 0);
     int r = r0;
     for (int ti = T0; ti < T1; ++ti) {
         const int q = (ti - T0) & 1;
-        const DevTerm T = G.terms[tidx[ti]];
-        const int so = player ? T.seq[0] : T.seq[1];
-        const bool sd = T.kind == 2;
+        const DevTerm tm = G.terms[tidx[ti]];
+        const int so = player ? tm.seq[0] : tm.seq[1];
+        const bool sd = tm.kind == 2;
         // prefetch terminal ti+1's row into the other buffer (its previous reader, terminal
         // ti-1, finished phase A before that terminal's first barrier)
         if (tid == 0 && ti > T0 && ti + 1 < T1) {
@@ -383,46 +397,46 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             const int so1 = player ? T1n.seq[0] : T1n.seq[1];
             if (so1) {
                 fence_proxy_async();
-                mbar_expect_tx(&bar[1 + (q ^ 1)], Hp * sizeof(double));
-                bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)so1 * Hp, Hp * sizeof(double), &bar[1 + (q ^ 1)]);
+                mbar_expect_tx(&bar[1 + (q ^ 1)], Hp * sizeof(T));
+                bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)so1 * Hp, Hp * sizeof(T), &bar[1 + (q ^ 1)]);
             }
         }
         if (so) {
             mbar_wait(&bar[1 + q], par[q]);
             par[q] ^= 1u;
         }
-        const double* vrow = vb + q * NP;
+        const T* vrow = vb + q * NP;
         // ---- phase A: w = prior_opp * v_opp in chunks of K positions, warp scan of the chunk sums
-        double x[K];
-        double run = 0.0;
+        T x[K];
+        T run = T(0);
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             x[j] = so ? popp[base + j] * vrow[base + j] : popp[base + j];
             w[base + j] = x[j];
             run += x[j];
         }
-        const double incl = warp_incl_scan(run, lane);
+        const T incl = warp_incl_scan(run, lane);
         if (lane == 31) wtot[wid] = incl;
         __syncthreads();
         // ---- phase B: card sums (segment scans inside lane groups) and the block prefix of w
         {
-            double y[CH];
-            double ssum = 0.0;
+            T y[CH];
+            T ssum = T(0);
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
                 const int e = sbeg + j;
                 const unsigned pos = e < send ? (cent[e] & CE_END) : CE_END;
-                y[j] = pos != CE_END ? w[pos] : 0.0;
+                y[j] = pos != CE_END ? w[pos] : T(0);
                 ssum += y[j];
             }
             // exclusive scan of the part sums inside the segment's lane group
-            double inc = ssum;
+            T inc = ssum;
             for (int o = 1; o < GL; o <<= 1) {
-                const double u = __shfl_up_sync(0xffffffffu, inc, o, GL);
+                const T u = __shfl_up_sync(0xffffffffu, inc, o, GL);
                 if (part >= o) inc += u;
             }
             if (has_seg) {
-                double run2 = inc - ssum;
+                T run2 = inc - ssum;
                 if (sd) {
 #pragma unroll
                     for (int j = 0; j < CH; ++j) {
@@ -434,16 +448,16 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
                 }
             }
         }
-        double wpre = 0.0, total = 0.0;
+        T wpre = T(0), total = T(0);
 #pragma unroll
         for (int qq = 0; qq < NW; ++qq) {
-            const double v = wtot[qq];
-            wpre += qq < wid ? v : 0.0;
+            const T v = wtot[qq];
+            wpre += qq < wid ? v : T(0);
             total += v;
         }
-        const double pbase = wpre + incl - run;
+        const T pbase = wpre + incl - run;
         if (sd) {
-            double p = pbase;
+            T p = pbase;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
                 Pf[base + j] = p;
@@ -452,22 +466,22 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         }
         __syncthreads();
         // ---- phase C (positions beyond H compute on padding and are never stored)
-        const double scale = T.kappa * kg * T.amount;
-        double pre = pbase;
+        const T scale = (T)(tm.kappa * G.kappa_game[g] * tm.amount);
+        T pre = pbase;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const int i = base + j;
             const uint2 pc = pcard[i];
-            double v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
+            T v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
             if (HS == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
             if (sd) {
                 const uint32_t lh = lohi[i];
                 const int lo = lh & 0xFFFFu, hi = lh >> 16;
                 if (lo == i && hi == i + 1) {
-                    const double ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
+                    const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
                     v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
                     if (HS == 2) {
-                        const double cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
+                        const T cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
                         v += cb + (cb + x[j]);
                     }
                 } else {
@@ -490,11 +504,11 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             for (int j = 0; j < K; ++j) {
                 const int i = base + j;
                 if (i < H) ob[i] = pself[i] * racc[j];
-                racc[j] = 0.0;
+                racc[j] = T(0);
             }
             fence_proxy_async();
             __syncthreads();
-            if (tid == 0) bulk_s2g(outg + (size_t)srow * Hp, ob, Hp * sizeof(double));
+            if (tid == 0) bulk_s2g(outg + (size_t)srow * Hp, ob, Hp * sizeof(T));
             ++r;
         }
     }
@@ -504,15 +518,15 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
 static constexpr int GRAD_NT = 512, GRAD_KMAX = 3, GRAD_EMAX = 6;  // H <= 1536, card array <= 3072
 
 static size_t grad_smem_bytes(const DevGame& G) {
-    return sizeof(double) * (size_t)(3 * G.H_pad + 1 + G.n_ce);
+    return (size_t)G.esz * (size_t)(3 * G.H_pad + 1 + G.n_ce);
 }
 
 static constexpr int STG_NT = 416, STG_K = 3, STG_CH = 6;  // positions <= 1248, 52 cards x 8 lanes
 
 static size_t grad_staged_smem_bytes(const DevGame& G) {
     const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
-    return sizeof(double) * (2 * Hp + 5 * NP + 2 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
-           sizeof(uint16_t) * G.n_ce;
+    return (size_t)G.esz * (2 * Hp + 5 * NP + 2 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
+           sizeof(uint16_t) * G.n_ce + 16;
 }
 
 static int staged_gl_log2(const DevGame& G) {
@@ -526,37 +540,45 @@ static bool staged_ok(const DevGame& G) {
            (G.n_cards << staged_gl_log2(G)) <= STG_NT && (1 << staged_gl_log2(G)) <= 32;
 }
 
+template <class T>
+static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
+                                     const int* mask, int want, cudaStream_t st) {
+    if (staged_ok(G)) {
+        if (P.n_chunks == 0) return cudaSuccess;
+        dim3 grid(P.n_chunks, G.n_games);
+        const int gl = staged_gl_log2(G);
+        if (G.hand_size == 2)
+            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, T>
+                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
+        else
+            grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, T>
+                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
+        return cudaGetLastError();
+    }
+    dim3 grid(P.n_rows_term, G.n_games);
+    grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>
+        <<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, 0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
                             const int* mask, int want, int all_rows, cudaStream_t st) {
     if (all_rows) {
         // rows that end no terminal (or that another shard computes) are 0
         if (gout.slot_sel) return cudaErrorInvalidValue;
         cudaError_t e = cudaSuccess;
-        const size_t row_block = sizeof(double) * (size_t)P.n_pub * G.H_pad;
+        const size_t row_block = (size_t)G.esz * (size_t)P.n_pub * G.H_pad;
+        char* base = reinterpret_cast<char*>(gout.base);
         if (gout.game_stride == (long long)P.n_pub * G.H_pad)
-            e = cudaMemsetAsync(gout.base, 0, row_block * G.n_games, st);
+            e = cudaMemsetAsync(base, 0, row_block * G.n_games, st);
         else
             for (int g = 0; g < G.n_games && e == cudaSuccess; ++g)
-                e = cudaMemsetAsync(gout.base + (size_t)g * gout.game_stride, 0, row_block, st);
+                e = cudaMemsetAsync(base + (size_t)g * gout.game_stride * G.esz, 0, row_block, st);
         if (e != cudaSuccess) return e;
     }
     if (P.n_rows_term == 0) return cudaSuccess;
-    if (staged_ok(G)) {
-        if (P.n_chunks == 0) return cudaSuccess;
-        dim3 grid(P.n_chunks, G.n_games);
-        const int gl = staged_gl_log2(G);
-        if (G.hand_size == 2)
-            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2>
-                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
-        else
-            grad_staged_kernel<STG_NT, STG_K, STG_CH, 1>
-                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
-        return cudaGetLastError();
-    }
-    dim3 grid(P.n_rows_term, G.n_games);
-    grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX><<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout,
-                                                                                         mask, want, 0);
-    return cudaGetLastError();
+    return G.esz == 4 ? launch_gradient_t<float>(G, P, player, vin, gout, mask, want, st)
+                      : launch_gradient_t<double>(G, P, player, vin, gout, mask, want, st);
 }
 
 // ------------------------------------------------------------------ treeplex pass
@@ -573,90 +595,92 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 // EGT convex combinations, CFR average) are written row by row.
 static constexpr int TH_HPL = 1, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
 
-size_t tree_smem_bytes(const DevPlayer& P) {
-    return sizeof(double) * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + 64 + P.n_nodes) +
+size_t tree_smem_bytes(const DevPlayer& P, int esz) {
+    return sizeof(double) * 64 + (size_t)esz * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + P.n_nodes) +
            sizeof(int) * (size_t)(6 * P.n_nodes + P.n_levels * TH_WARPS + 1);
 }
 
+template <class T>
 struct TreeNodeCtx {
     int mode, cfr_plus;
-    double mu;
+    T mu;
     const double* __restrict__ exptab;
 };
 
 // Bottom-up work of simplex (node m, hand h) on its column; returns the simplex value.
-__device__ __forceinline__ double tree_node_up(const TreeNodeCtx& C, const DevPlayer& P, double* col, int first,
-                                               int n, int m, int h, int Hp, double logn, double* __restrict__ cz,
-                                               double* __restrict__ rg) {
+template <class T>
+__device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
+                                               int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
+                                               T* __restrict__ rg) {
     const int mode = C.mode;
     if (mode == TM_SBR) {
         // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
         // i* = argmax qbar, w = mu beta_j
-        const double wgt = C.mu * P.beta[(size_t)m * Hp + h];
-        const double iw = 1.0 / wgt;
-        double mn = DBL_MAX;
+        const T wgt = C.mu * (T)P.beta[(size_t)m * Hp + h];
+        const T iw = T(1) / wgt;
+        T mn = big_value<T>();
         for (int a = 0; a < n; ++a) mn = fmin(mn, col[a * TH_HANDS]);
-        double S = 0.0;
+        T S = T(0);
         for (int a = 0; a < n; ++a) {
-            const double e = exp_nonpos((mn - col[a * TH_HANDS]) * iw, C.exptab);
+            const T e = exp_nonpos((mn - col[a * TH_HANDS]) * iw, C.exptab);
             col[a * TH_HANDS] = e;
             S += e;
         }
-        const double inv = 1.0 / S;
+        const T inv = T(1) / S;
         for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
         return mn - wgt * (log(S) - logn);
     }
     if (mode == TM_PROX) {
         // shifted-gradient SBR in multiplicative form (R16):
         // qbar_i ~ zbar_i exp(-g_i / beta), value = -beta log sum_i zbar_i exp(-g_i / beta)
-        const double beta = P.beta[(size_t)m * Hp + h];
-        const double ib = 1.0 / beta;
-        const double* __restrict__ zr = cz + (size_t)first * Hp + h;
-        double mn = DBL_MAX;
+        const T beta = (T)P.beta[(size_t)m * Hp + h];
+        const T ib = T(1) / beta;
+        const T* __restrict__ zr = cz + (size_t)first * Hp + h;
+        T mn = big_value<T>();
         for (int a = 0; a < n; ++a)
-            if (zr[(size_t)a * Hp] > 0.0) mn = fmin(mn, col[a * TH_HANDS]);
-        double S = 0.0;
+            if (zr[(size_t)a * Hp] > T(0)) mn = fmin(mn, col[a * TH_HANDS]);
+        T S = T(0);
         for (int a = 0; a < n; ++a) {
-            const double za = zr[(size_t)a * Hp];
-            const double e = za > 0.0 ? za * exp_nonpos((mn - col[a * TH_HANDS]) * ib, C.exptab) : 0.0;
+            const T za = zr[(size_t)a * Hp];
+            const T e = za > T(0) ? za * exp_nonpos((mn - col[a * TH_HANDS]) * ib, C.exptab) : T(0);
             col[a * TH_HANDS] = e;
             S += e;
         }
-        const double inv = 1.0 / S;
+        const T inv = T(1) / S;
         for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
         return mn - beta * log(S);
     }
     if (mode == TM_BR) {
         int best = 0;
-        double mn = col[0];
+        T mn = col[0];
         for (int a = 1; a < n; ++a) {
-            const double v = col[a * TH_HANDS];
+            const T v = col[a * TH_HANDS];
             if (v < mn) {
                 mn = v;
                 best = a;
             }
         }
-        for (int a = 0; a < n; ++a) col[a * TH_HANDS] = a == best ? 1.0 : 0.0;
+        for (int a = 0; a < n; ++a) col[a * TH_HANDS] = a == best ? T(1) : T(0);
         return mn;
     }
     // TM_CFR: utility u = gsign * g, current strategy z, regrets r
-    double v = 0.0;
+    T v = T(0);
     for (int a = 0; a < n; ++a) v += col[a * TH_HANDS] * cz[(size_t)(first + a) * Hp + h];
-    double S = 0.0;
+    T S = T(0);
     for (int a = 0; a < n; ++a) {
         const size_t ix = (size_t)(first + a) * Hp + h;
-        const double u = col[a * TH_HANDS], r0 = rg[ix];
-        double r = r0 + u - v;
-        if (C.cfr_plus) r = fmax(r, 0.0);
+        const T u = col[a * TH_HANDS], r0 = rg[ix];
+        T r = r0 + u - v;
+        if (C.cfr_plus) r = fmax(r, T(0));
         rg[ix] = r;
         // DESIGN.md R15: regrets at the rounding-noise level of their own update count as 0
-        const double tol = 1e-13 * (fabs(r0) + fabs(u) + fabs(v));
-        const double pr = r > tol ? r : 0.0;
+        const T tol = cfr_noise<T>() * (fabs(r0) + fabs(u) + fabs(v));
+        const T pr = r > tol ? r : T(0);
         col[a * TH_HANDS] = pr;
         S += pr;
     }
     for (int a = 0; a < n; ++a) {
-        const double z = S > 0.0 ? col[a * TH_HANDS] / S : 1.0 / n;
+        const T z = S > T(0) ? col[a * TH_HANDS] / S : T(1) / n;
         col[a * TH_HANDS] = z;
         cz[(size_t)(first + a) * Hp + h] = z;
     }
@@ -665,55 +689,55 @@ __device__ __forceinline__ double tree_node_up(const TreeNodeCtx& C, const DevPl
 
 // The same bottom-up work for a node with a compile-time number of actions N: the N
 // entries are read once into registers and written once.
-template <int N>
-__device__ __forceinline__ double tree_node_up_n(const TreeNodeCtx& C, const DevPlayer& P, double* col, int first,
-                                                 int m, int h, int Hp, double logn, double* __restrict__ cz,
-                                                 double* __restrict__ rg) {
-    double x[N];
+template <int N, class T>
+__device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
+                                                 int m, int h, int Hp, T logn, T* __restrict__ cz,
+                                                 T* __restrict__ rg) {
+    T x[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) x[a] = col[a * TH_HANDS];
     const int mode = C.mode;
-    double value;
+    T value;
     if (mode == TM_SBR) {
-        const double wgt = C.mu * P.beta[(size_t)m * Hp + h];
-        const double iw = 1.0 / wgt;
-        double mn = x[0];
+        const T wgt = C.mu * (T)P.beta[(size_t)m * Hp + h];
+        const T iw = T(1) / wgt;
+        T mn = x[0];
 #pragma unroll
         for (int a = 1; a < N; ++a) mn = fmin(mn, x[a]);
-        double S = 0.0;
+        T S = T(0);
 #pragma unroll
         for (int a = 0; a < N; ++a) {
             x[a] = exp_nonpos((mn - x[a]) * iw, C.exptab);
             S += x[a];
         }
-        const double inv = 1.0 / S;
+        const T inv = T(1) / S;
 #pragma unroll
         for (int a = 0; a < N; ++a) x[a] *= inv;
         value = mn - wgt * (log(S) - logn);
     } else if (mode == TM_PROX) {
-        const double beta = P.beta[(size_t)m * Hp + h];
-        const double ib = 1.0 / beta;
-        const double* __restrict__ zr = cz + (size_t)first * Hp + h;
-        double z[N];
+        const T beta = (T)P.beta[(size_t)m * Hp + h];
+        const T ib = T(1) / beta;
+        const T* __restrict__ zr = cz + (size_t)first * Hp + h;
+        T z[N];
 #pragma unroll
         for (int a = 0; a < N; ++a) z[a] = zr[(size_t)a * Hp];
-        double mn = DBL_MAX;
+        T mn = big_value<T>();
 #pragma unroll
         for (int a = 0; a < N; ++a)
-            if (z[a] > 0.0) mn = fmin(mn, x[a]);
-        double S = 0.0;
+            if (z[a] > T(0)) mn = fmin(mn, x[a]);
+        T S = T(0);
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            x[a] = z[a] > 0.0 ? z[a] * exp_nonpos((mn - x[a]) * ib, C.exptab) : 0.0;
+            x[a] = z[a] > T(0) ? z[a] * exp_nonpos((mn - x[a]) * ib, C.exptab) : T(0);
             S += x[a];
         }
-        const double inv = 1.0 / S;
+        const T inv = T(1) / S;
 #pragma unroll
         for (int a = 0; a < N; ++a) x[a] *= inv;
         value = mn - beta * log(S);
     } else if (mode == TM_BR) {
         int best = 0;
-        double mn = x[0];
+        T mn = x[0];
 #pragma unroll
         for (int a = 1; a < N; ++a)
             if (x[a] < mn) {
@@ -721,33 +745,33 @@ __device__ __forceinline__ double tree_node_up_n(const TreeNodeCtx& C, const Dev
                 best = a;
             }
 #pragma unroll
-        for (int a = 0; a < N; ++a) x[a] = a == best ? 1.0 : 0.0;
+        for (int a = 0; a < N; ++a) x[a] = a == best ? T(1) : T(0);
         value = mn;
     } else {
-        double z[N], r[N];
+        T z[N], r[N];
         const size_t ix0 = (size_t)first * Hp + h;
 #pragma unroll
         for (int a = 0; a < N; ++a) {
             z[a] = cz[ix0 + (size_t)a * Hp];
             r[a] = rg[ix0 + (size_t)a * Hp];
         }
-        double v = 0.0;
+        T v = T(0);
 #pragma unroll
         for (int a = 0; a < N; ++a) v += x[a] * z[a];
-        double S = 0.0;
+        T S = T(0);
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            const double u = x[a], r0 = r[a];
-            double rr = r0 + u - v;
-            if (C.cfr_plus) rr = fmax(rr, 0.0);
+            const T u = x[a], r0 = r[a];
+            T rr = r0 + u - v;
+            if (C.cfr_plus) rr = fmax(rr, T(0));
             rg[ix0 + (size_t)a * Hp] = rr;
-            const double tol = 1e-13 * (fabs(r0) + fabs(u) + fabs(v));  // DESIGN.md R15
-            x[a] = rr > tol ? rr : 0.0;
+            const T tol = cfr_noise<T>() * (fabs(r0) + fabs(u) + fabs(v));  // DESIGN.md R15
+            x[a] = rr > tol ? rr : T(0);
             S += x[a];
         }
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            x[a] = S > 0.0 ? x[a] / S : 1.0 / N;
+            x[a] = S > T(0) ? x[a] / S : T(1) / N;
             cz[ix0 + (size_t)a * Hp] = x[a];
         }
         value = v;
@@ -757,12 +781,13 @@ __device__ __forceinline__ double tree_node_up_n(const TreeNodeCtx& C, const Dev
     return value;
 }
 
-__device__ __forceinline__ double tree_node_up_any(const TreeNodeCtx& C, const DevPlayer& P, double* col, int first,
-                                                   int n, int m, int h, int Hp, double logn, double* __restrict__ cz,
-                                                   double* __restrict__ rg) {
+template <class T>
+__device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
+                                                   int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
+                                                   T* __restrict__ rg) {
     switch (n) {  // warp-uniform: every lane works on the same node
 #define EGT_NODE_CASE(K) \
-    case K: return tree_node_up_n<K>(C, P, col, first, m, h, Hp, logn, cz, rg);
+    case K: return tree_node_up_n<K, T>(C, P, col, first, m, h, Hp, logn, cz, rg);
         EGT_NODE_CASE(1) EGT_NODE_CASE(2) EGT_NODE_CASE(3) EGT_NODE_CASE(4)
 #undef EGT_NODE_CASE
         default: return tree_node_up(C, P, col, first, n, m, h, Hp, logn, cz, rg);
@@ -771,74 +796,78 @@ __device__ __forceinline__ double tree_node_up_any(const TreeNodeCtx& C, const D
 
 // Top-down work of simplex (node, hand): q_i = q_{p_j} * qbar_i and the requested output rows.
 // All global reads of the node are issued before any use (one round trip per node).
+template <class T>
 struct TreeDownCtx {
     int mode;
-    double tau, alpha;
-    const double* __restrict__ bin;
-    const double* __restrict__ ci;
-    double* __restrict__ ob;
-    double* __restrict__ oq;
-    double* __restrict__ co;
-    double* __restrict__ av;
+    T tau, alpha;
+    const T* __restrict__ bin;
+    const T* __restrict__ ci;
+    T* __restrict__ ob;
+    T* __restrict__ oq;
+    T* __restrict__ co;
+    T* __restrict__ av;
 };
 
-template <int N>
-__device__ __forceinline__ void tree_node_down_n(const TreeDownCtx& D, bool ok, double qp, double unif, int first,
-                                                 double* col, int h, int Hp) {
+template <int N, class T>
+__device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool ok, T qp, T unif, int first,
+                                                 T* col, int h, int Hp) {
     const size_t ix0 = (size_t)first * Hp + h;
-    double b[N], cv[N], avv[N];
+    T b[N], cv[N], avv[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) {
-        if (!ok) b[a] = 0.0;
+        if (!ok) b[a] = T(0);
         else if (D.mode == TM_UNIFORM) b[a] = unif;
         else if (D.mode == TM_COMBINE) b[a] = D.bin[ix0 + (size_t)a * Hp];
         else b[a] = col[a * TH_HANDS];
-        cv[a] = D.co ? D.ci[ix0 + (size_t)a * Hp] : 0.0;
-        avv[a] = D.av ? D.av[ix0 + (size_t)a * Hp] : 0.0;
+        cv[a] = D.co ? D.ci[ix0 + (size_t)a * Hp] : T(0);
+        avv[a] = D.av ? D.av[ix0 + (size_t)a * Hp] : T(0);
     }
 #pragma unroll
     for (int a = 0; a < N; ++a) {
-        const double q = qp * b[a];
+        const T q = qp * b[a];
         col[a * TH_HANDS] = q;
         const size_t ix = ix0 + (size_t)a * Hp;
         if (D.ob) D.ob[ix] = b[a];
         if (D.oq) D.oq[ix] = q;
-        if (D.co) D.co[ix] = (1.0 - D.tau) * cv[a] + D.tau * q;
-        if (D.av) D.av[ix] = D.alpha * q + (1.0 - D.alpha) * avv[a];
+        if (D.co) D.co[ix] = (T(1) - D.tau) * cv[a] + D.tau * q;
+        if (D.av) D.av[ix] = D.alpha * q + (T(1) - D.alpha) * avv[a];
     }
 }
 
-__device__ __forceinline__ void tree_node_down_any(const TreeDownCtx& D, bool ok, double qp, int first, int n,
-                                                   double* col, int h, int Hp) {
-    const double unif = 1.0 / n;
+template <class T>
+__device__ __forceinline__ void tree_node_down_any(const TreeDownCtx<T>& D, bool ok, T qp, int first, int n,
+                                                   T* col, int h, int Hp) {
+    const T unif = T(1) / n;
     switch (n) {
-        case 1: tree_node_down_n<1>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 2: tree_node_down_n<2>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 3: tree_node_down_n<3>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 4: tree_node_down_n<4>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 1: tree_node_down_n<1, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 2: tree_node_down_n<2, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 3: tree_node_down_n<3, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 4: tree_node_down_n<4, T>(D, ok, qp, unif, first, col, h, Hp); return;
         default: break;
     }
     for (int a0 = 0; a0 < n; a0 += 4) {  // wider nodes: four actions per round trip
         const int k = min(4, n - a0);
-        double* c0 = col + a0 * TH_HANDS;
-        if (k == 4) tree_node_down_n<4>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else if (k == 3) tree_node_down_n<3>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else if (k == 2) tree_node_down_n<2>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else tree_node_down_n<1>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        T* c0 = col + a0 * TH_HANDS;
+        if (k == 4) tree_node_down_n<4, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 3) tree_node_down_n<3, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 2) tree_node_down_n<2, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else tree_node_down_n<1, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
     }
 }
 
+template <class T>
 __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
-    extern __shared__ __align__(16) double tile[];
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    double* s_exptab = reinterpret_cast<double*>(sm_raw);        // [64] 2^(j/64) (fp64 exp only)
+    T* tile = reinterpret_cast<T*>(s_exptab + 64);                // [n_pub][TH_HANDS]
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (A.mask && A.mask[g] != A.want) return;
     const int Hp = G.H_pad, n_pub = P.n_pub, n_nodes = P.n_nodes, n_lv = P.n_levels;
     const int h0 = blockIdx.x * TH_HANDS;
     const int mode = A.mode;
     const bool has_grad = mode == TM_SBR || mode == TM_PROX || mode == TM_BR || mode == TM_CFR;
-    double* rootv = tile + (size_t)n_pub * TH_HANDS;              // [n_root][64]
-    double* s_exptab = rootv + (size_t)P.n_root * TH_HANDS;       // [64] 2^(j/64)
-    double* s_logn = s_exptab + 64;                               // [n_nodes]
+    T* rootv = tile + (size_t)n_pub * TH_HANDS;                   // [n_root][TH_HANDS]
+    T* s_logn = rootv + (size_t)P.n_root * TH_HANDS;              // [n_nodes]
     int* s_first = reinterpret_cast<int*>(s_logn + n_nodes);
     int* s_nact = s_first + n_nodes;
     int* s_par = s_nact + n_nodes;
@@ -853,7 +882,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
         s_bs[i] = P.node_bs[i];
         s_rslot[i] = P.root_slot[i];
         s_sn[i] = P.sched_nodes[i];
-        s_logn[i] = log((double)P.node_nact[i]);
+        s_logn[i] = log((T)P.node_nact[i]);
     }
     for (int i = tid; i <= n_lv * TH_WARPS; i += TH_NT) s_so[i] = P.sched_off[i];
     for (int i = tid; i < 64; i += TH_NT) s_exptab[i] = exp2((double)i / 64.0);
@@ -863,56 +892,53 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
     // ---- gradient tile: asynchronous 16-byte copies (LDGSTS), all rows in flight, then each
     // thread scales the chunks it copied by sc = gsign (* step for prox)
     if (has_grad) {
-        double sc = A.gsign;
-        if (mode == TM_PROX) sc *= A.mu[g];
-        const double* __restrict__ gp = A.g.at(g) + h0;
-        constexpr int per_row = TH_HANDS / 2;
+        const T sc = (T)(mode == TM_PROX ? A.gsign * A.mu[g] : A.gsign);
+        const T* __restrict__ gp = A.g.at<T>(g) + h0;
+        constexpr int EPC = 16 / sizeof(T);  // elements per 16-byte chunk
+        constexpr int per_row = TH_HANDS / EPC;
         const int n_chunks = n_pub * per_row;
         for (int c = tid; c < n_chunks; c += TH_NT) {
             const int r = c / per_row, k = c % per_row;
-            if (h0 + 2 * k < Hp) {
-                const unsigned dst = smem_u32(tile + r * TH_HANDS + 2 * k);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gp + (size_t)r * Hp + 2 * k)
+            if (h0 + EPC * k < Hp) {
+                const unsigned dst = smem_u32(tile + r * TH_HANDS + EPC * k);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gp + (size_t)r * Hp + EPC * k)
                              : "memory");
             }
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        if (sc != 1.0)
+        if (sc != T(1))
             for (int c = tid; c < n_chunks; c += TH_NT) {
-                const int r = c / per_row, k = c % per_row;
-                double2* t2 = reinterpret_cast<double2*>(tile + r * TH_HANDS + 2 * k);
-                double2 v = *t2;
-                v.x *= sc;
-                v.y *= sc;
-                *t2 = v;
+                T* t = tile + (c / per_row) * TH_HANDS + EPC * (c % per_row);
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) t[e] *= sc;
             }
     }
     __syncthreads();
 
     // ---- bottom-up, deepest level first
-    TreeNodeCtx C;
+    TreeNodeCtx<T> C;
     C.mode = mode;
     C.cfr_plus = A.cfr_plus;
-    C.mu = (mode == TM_SBR) ? A.mu[g] : 1.0;
+    C.mu = (mode == TM_SBR) ? (T)A.mu[g] : T(1);
     C.exptab = s_exptab;
-    double* __restrict__ cz = A.center.ok() ? A.center.at(g) : nullptr;
-    double* __restrict__ rg = A.regret.ok() ? A.regret.at(g) : nullptr;
+    T* __restrict__ cz = A.center.ok() ? A.center.at<T>(g) : nullptr;
+    T* __restrict__ rg = A.regret.ok() ? A.regret.at<T>(g) : nullptr;
     if (has_grad) {
         for (int L = n_lv - 1; L >= 0; --L) {
             const int i0 = s_so[L * TH_WARPS + wid], i1 = s_so[L * TH_WARPS + wid + 1];
             for (int idx = i0; idx < i1; ++idx) {
                 const int m = s_sn[idx];
                 const int first = s_first[m], n = s_nact[m], par = s_par[m], rs = s_rslot[m];
-                const double logn = s_logn[m];
+                const T logn = s_logn[m];
 #pragma unroll
                 for (int j = 0; j < TH_HPL; ++j) {
                     const int c = lane + 32 * j, h = h0 + c;
-                    double* col = tile + (size_t)first * TH_HANDS + c;
-                    double value = 0.0;
+                    T* col = tile + (size_t)first * TH_HANDS + c;
+                    T value = T(0);
                     if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]))
                         value = tree_node_up_any(C, P, col, first, n, m, h, Hp, logn, cz, rg);
                     else
-                        for (int a = 0; a < n; ++a) col[a * TH_HANDS] = 0.0;
+                        for (int a = 0; a < n; ++a) col[a * TH_HANDS] = T(0);
                     if (rs >= 0) rootv[rs * TH_HANDS + c] = value;
                     else tile[par * TH_HANDS + c] += value;
                 }
@@ -929,8 +955,8 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
             for (int j = 0; j < TH_HPL; ++j) {
                 const int c = lane + 32 * j;
                 if (h0 + c < G.H) {
-                    double u = tile[c];
-                    for (int r = 0; r < P.n_root; ++r) u += rootv[r * TH_HANDS + c];
+                    double u = (double)tile[c];
+                    for (int r = 0; r < P.n_root; ++r) u += (double)rootv[r * TH_HANDS + c];
                     v += u;
                 }
             }
@@ -957,19 +983,19 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
     // ---- top-down, shallowest level first
     const bool want_td = A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR;
     if (!want_td) return;
-    double* __restrict__ ob = A.out_b.ok() ? A.out_b.at(g) : nullptr;
-    double* __restrict__ oq = A.out_q.ok() ? A.out_q.at(g) : nullptr;
-    const double* __restrict__ ci = A.comb_in.ok() ? A.comb_in.at(g) : nullptr;
-    double* __restrict__ co = A.comb_out.ok() ? A.comb_out.at(g) : nullptr;
-    double* __restrict__ av = A.avg.ok() ? A.avg.at(g) : nullptr;
-    const double tau = A.tau ? A.tau[g] : 0.0;
-    double alpha = 0.0;
+    T* __restrict__ ob = A.out_b.ok() ? A.out_b.at<T>(g) : nullptr;
+    T* __restrict__ oq = A.out_q.ok() ? A.out_q.at<T>(g) : nullptr;
+    const T* __restrict__ ci = A.comb_in.ok() ? A.comb_in.at<T>(g) : nullptr;
+    T* __restrict__ co = A.comb_out.ok() ? A.comb_out.at<T>(g) : nullptr;
+    T* __restrict__ av = A.avg.ok() ? A.avg.at<T>(g) : nullptr;
+    const T tau = A.tau ? (T)A.tau[g] : T(0);
+    T alpha = T(0);
     if (av) {
         const double t = (double)A.iter[g];
-        alpha = A.avg_linear ? 2.0 * t / (t * t + t) : 1.0 / t;
+        alpha = (T)(A.avg_linear ? 2.0 * t / (t * t + t) : 1.0 / t);
     }
-    const double* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
-    TreeDownCtx Dn;
+    const T* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
+    TreeDownCtx<T> Dn;
     Dn.mode = mode;
     Dn.tau = tau;
     Dn.alpha = alpha;
@@ -985,10 +1011,10 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
             const int h = h0 + lane + 32 * j;
             if (h < Hp) {
                 const bool live = h < G.H;
-                const double q0 = live ? 1.0 : 0.0;
+                const T q0 = live ? T(1) : T(0);
                 if (ob) ob[h] = q0;
                 if (oq) oq[h] = q0;
-                if (co) co[h] = live ? (1.0 - tau) * ci[h] + tau : 0.0;
+                if (co) co[h] = live ? (T(1) - tau) * ci[h] + tau : T(0);
                 if (av) av[h] = q0;
             }
         }
@@ -1002,7 +1028,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
             for (int j = 0; j < TH_HPL; ++j) {
                 const int c = lane + 32 * j, h = h0 + c;
                 const bool ok = h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
-                const double qp = par == 0 ? (ok ? 1.0 : 0.0) : tile[par * TH_HANDS + c];
+                const T qp = par == 0 ? (ok ? T(1) : T(0)) : tile[par * TH_HANDS + c];
                 tree_node_down_any(Dn, ok, qp, first, n, tile + (size_t)first * TH_HANDS + c, h, Hp);
             }
         }
@@ -1012,21 +1038,29 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
 
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st) {
     dim3 grid((G.H_pad + TH_HANDS - 1) / TH_HANDS, G.n_games);
-    tree_kernel<<<grid, TH_NT, tree_smem_bytes(P), st>>>(G, P, player, A);
+    if (G.esz == 4) tree_kernel<float><<<grid, TH_NT, tree_smem_bytes(P, 4), st>>>(G, P, player, A);
+    else tree_kernel<double><<<grid, TH_NT, tree_smem_bytes(P, 8), st>>>(G, P, player, A);
     return cudaGetLastError();
 }
 
+template <class T>
+static cudaError_t prepare_t() {
+    const int lim = 200 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, T>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, T>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    return e;
+}
+
 cudaError_t kernels_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = prepare_t<double>();
+    return e == cudaSuccess ? prepare_t<float>() : e;
 }
 
 // ------------------------------------------------------------------ per-game scalars

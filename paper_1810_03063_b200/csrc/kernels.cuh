@@ -14,10 +14,12 @@ struct VecRef {
     int slot_xor = 0;               // 0: current slot, 1: the other one
     __host__ __device__ bool ok() const { return base != nullptr; }
 #ifdef __CUDACC__
-    __device__ __forceinline__ double* at(int g) const {
+    // strides count elements of the game's precision T (base only carries the address)
+    template <class T = double>
+    __device__ __forceinline__ T* at(int g) const {
         long long off = (long long)g * game_stride;
         if (slot_sel) off += (long long)((slot_sel[g] ^ slot_xor) & 1) * slot_stride;
-        return base + off;
+        return reinterpret_cast<T*>(base) + off;
     }
 #endif
 };
@@ -32,6 +34,7 @@ struct DevTerm {
 
 struct DevGame {
     int n_games, H, H_pad, hand_size, n_bs, n_cards;
+    int esz;                  // bytes per vector element: 8 (fp64) or 4 (fp32 mode)
     int all_valid;            // 1: every hand is valid at every board state (river endgames)
     int ident;                // 1: position order = hand order at every board state (river endgames)
     int n_ce;                 // card-array slots per table (n_cards * seg_w, padded to 8)
@@ -42,7 +45,7 @@ struct DevGame {
     const uint16_t* tab_cent; // [G*n_bs][n_ce]      card array (CE_* packing, game.h)
     const uint2* tab_pcard;   // [G*n_bs][H_pad]     per position, per card: segment info (PC_*)
     const uint8_t* tab_valid; // [G*n_bs][H_pad]
-    const double* prior[2];   // [G][H_pad]
+    const void* prior[2];     // [G][H_pad] in the game's precision
     const double* kappa_game; // [G]
     const DevTerm* terms;
 };
@@ -116,7 +119,7 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
                             const int* mask, int want, int all_rows, cudaStream_t st);
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st);
 cudaError_t kernels_prepare();
-size_t tree_smem_bytes(const DevPlayer& P);
+size_t tree_smem_bytes(const DevPlayer& P, int esz);
 
 cudaError_t launch_egt_prepare(int variant, int n_games, DevScalars S, cudaStream_t st);
 cudaError_t launch_egt_accept(int variant, int n_games, DevScalars S, cudaStream_t st);
