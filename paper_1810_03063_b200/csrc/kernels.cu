@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     T* w = vb + 2 * NP;           // [NP]
     T* ob = w + NP;               // [Hp] output row staging
     T* Pf = ob + Hp;              // [NP + 2]
-    T* Ex = Pf + NP + 2;          // [n_ce]
+    T* Ex = Pf + NP + 4;          // [n_ce] (Pf padded to keep 16-byte alignment)
     uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [NP]
     uint32_t* lohi = reinterpret_cast<uint32_t*>(pcard + NP);        // [NP]
     uint16_t* cent = reinterpret_cast<uint16_t*>(lohi + NP);         // [n_ce]
@@ -525,7 +525,7 @@ static constexpr int STG_NT = 416, STG_K = 3, STG_CH = 6;  // positions <= 1248,
 
 static size_t grad_staged_smem_bytes(const DevGame& G) {
     const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
-    return (size_t)G.esz * (2 * Hp + 5 * NP + 2 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
+    return (size_t)G.esz * (2 * Hp + 5 * NP + 4 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
            sizeof(uint16_t) * G.n_ce + 16;
 }
 
