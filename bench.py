@@ -12,9 +12,10 @@ boards and hand priors seeded per rank).  Units are shared out across ranks with
 data-path collective ("scaling": "weak").
 
 One step = one pass of the whole hot path for every game of the batch: one EGT/as
-iteration (Alg. 3 body with Alg. 4's excessive-gap check: 4 gradient evaluations)
-followed by the stopping test eps_sad(x^t, y^t) (Alg. 3 line 5: 2 more gradient
-evaluations + 2 best-response passes) -- 6 gradient evaluations per game per step.
+iteration (Alg. 3 body with Alg. 4's excessive-gap check: 4 gradient evaluations, the
+count PAPER.md:726-731 uses) including the stopping test eps_sad(x^t, y^t) (Alg. 3 line 5),
+which the library takes from the excessive-gap check's gradients (2 best-response passes,
+no extra gradient), read back with ``saddle_gap_device``.
 ``value`` = gradient evaluations of all games on all ranks / max-over-ranks device time.
 
 ``--impl reference`` times the CPU oracle (``oracle/``) as it stands on the host cores,
@@ -35,9 +36,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-METRIC = "gradient evals/sec (EGT/as + eps_sad stopping test, HUNL river endgames)"
+METRIC = ("EGT/as gradient evaluations/sec (4 per iteration as PAPER.md:726-731 counts them; "
+          "eps_sad stopping test inside the timed step), HUNL river endgames")
 UNIT = "grad_evals/s"
-GRADS_PER_STEP = 6  # EGT/as: 4 (Alg. 2 + EGC check); eps_sad: 2
+GRADS_PER_STEP = 4  # EGT/as: y_mu(x_hat), the prox gradient, the two excessive-gap responses (R17)
 
 
 def parse():

@@ -58,6 +58,7 @@ struct egt_game {
     int* search_mask = nullptr;     // [G]
     double* gapval = nullptr;       // [2][G]
     double* gapout = nullptr;       // [G]
+    double* gapcur = nullptr;       // [G] eps_sad of the current EGT/as iterate (maintained)
     double* S[2] = {nullptr, nullptr};   // EGT state, 2 slots
     double* C[2] = {nullptr, nullptr};   // EGT cache (behavioural smoothed BR), 2 slots
     double* HAT[2] = {nullptr, nullptr};
@@ -419,6 +420,9 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(dalloc(G, &G->mu_base, 2 * (size_t)Gn));
     TRY(dalloc(G, &G->search_mask, (size_t)Gn));
     TRY(dalloc(G, &G->gapval, 2 * (size_t)Gn));
+    TRY(dalloc(G, &G->gapcur, (size_t)Gn));
+    S.brval = G->gapval;
+    S.gap = G->gapcur;
     TRY(dalloc(G, &G->gapout, (size_t)Gn));
     for (int p = 0; p < 2; ++p) {
         const size_t n = (size_t)Gn * G->V[p];
@@ -860,6 +864,17 @@ static int record_egt_iteration(egt_game* G) {
             A.counter = G->counter;
             CK(tree(G, p, A));
         }
+        // stopping test (Alg. 3 line 5) at the candidate from the same gradients: A y+ and A^T x+
+        for (int p = 0; p < 2; ++p) {
+            TreeArgs A = base_args();
+            A.mode = TM_BR;
+            A.g = vec(G->GR[p], G->V[p]);
+            A.gsign = GSIGN[p];
+            A.value = G->gapval + (size_t)p * Gn;
+            A.partial = G->partial;
+            A.counter = G->counter;
+            CK(tree(G, p, A));
+        }
     }
     CK(scalar_k(G, [&] { return launch_egt_accept(var, Gn, S, G->st); }));
     return 0;
@@ -896,6 +911,8 @@ static int zero_scalars(egt_game* G) {
     CK(cudaStreamSynchronize(G->st));
     return 0;
 }
+
+static int enqueue_gap(egt_game* G, int which, double* dev_out);
 
 extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) {
     if (!G || variant < EGT_THEORY || variant > EGT_AS) return fail(EGT_E_ARG, "bad argument");
@@ -953,6 +970,10 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
     if (egt_initial_point(G)) return EGT_E_CUDA;
     G->grads += 3;
     G->grads_per_iter = variant == EGT_AS ? 4 : 3;
+    if (variant == EGT_AS) {
+        int r = enqueue_gap(G, 0, G->gapcur);  // eps_sad(x0, y0); steps keep it current
+        if (r) return r;
+    }
     return end(G);
 }
 
@@ -1090,11 +1111,21 @@ static int enqueue_gap(egt_game* G, int which, double* dev_out) {
     return 0;
 }
 
+// EGT/as keeps eps_sad of its current iterate up to date (from the excessive-gap check's
+// gradients); other solvers and the CFR averages evaluate it (2 gradients + 2 best responses).
+static int gap_into(egt_game* G, int which, double* dev_out) {
+    if (G->solver == SOLVER_EGT && G->variant == EGT_AS && which == 0) {
+        CK(cudaMemcpyAsync(dev_out, G->gapcur, sizeof(double) * G->host.n_games, cudaMemcpyDeviceToDevice, G->st));
+        return 0;
+    }
+    return enqueue_gap(G, which, dev_out);
+}
+
 extern "C" int saddle_gap(egt_game* G, int32_t which, double* host_out) {
     if (!G || !host_out) return fail(EGT_E_ARG, "bad argument");
     const int Gn = G->host.n_games;
     if (begin(G)) return EGT_E_CUDA;
-    int r = enqueue_gap(G, which, G->gapout);
+    int r = gap_into(G, which, G->gapout);
     if (r) return r;
     CK(cudaMemcpyAsync(host_out, G->gapout, sizeof(double) * Gn, cudaMemcpyDeviceToHost, G->st));
     CK(cudaStreamSynchronize(G->st));
@@ -1104,7 +1135,7 @@ extern "C" int saddle_gap(egt_game* G, int32_t which, double* host_out) {
 extern "C" int saddle_gap_device(egt_game* G, int32_t which, double* dev_out) {
     if (!G || !dev_out) return fail(EGT_E_ARG, "bad argument");
     if (begin(G)) return EGT_E_CUDA;
-    int r = enqueue_gap(G, which, dev_out);
+    int r = gap_into(G, which, dev_out);
     if (r) return r;
     return end(G);
 }

@@ -1096,6 +1096,9 @@ __global__ void egt_accept_kernel(int variant, int n, DevScalars S) {
         S.mu[g] = S.mu_cand[g];
         S.mu[n + g] = S.mu_cand[n + g];
         S.t[g] += 1;
+        // eps_sad of the accepted candidate from the best responses to the check's gradients
+        // (PAPER.md:311); a rejected attempt leaves the iterate, and its gap, unchanged
+        if (variant == 2) S.gap[g] = -S.brval[n + g] - S.brval[g];
     } else {
         S.tau[g] *= 0.5;                              // Alg. 4 line 3
         S.backtracks[g] += 1;

@@ -110,6 +110,8 @@ struct DevScalars {
     int* attempts;    // [G]
     int* backtracks;  // [G]
     int* fail;        // [G]
+    const double* brval;  // [2][G] best-response values at the EGT/as candidate (gap)
+    double* gap;      // [G] eps_sad of the current iterate (EGT/as maintains it)
 };
 
 // Launchers (return cudaGetLastError()).

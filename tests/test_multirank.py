@@ -39,6 +39,11 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
+def bench_grads():
+    import bench
+    return bench.GRADS_PER_STEP
+
+
 def test_two_ranks_gloo():
     world = 2
     port = _free_port()
@@ -49,7 +54,7 @@ def test_two_ranks_gloo():
     for rank in range(world):
         assert res[rank]["env"] == (rank, rank, world)
         assert res[rank]["ms"] == 15.0                      # max over ranks
-        assert res[rank]["value"] == pytest.approx(6 * 4 * 2 * 7 / 0.015)
+        assert res[rank]["value"] == pytest.approx(bench_grads() * 4 * 2 * 7 / 0.015)
     b0, b1 = (np.array(b) for b in res[0]["boards"])
     assert b0.shape == b1.shape == (4, 5)
     assert not np.array_equal(b0, b1)                         # independent endgames per rank
@@ -59,7 +64,7 @@ def test_two_ranks_gloo():
 def test_single_rank_defaults():
     import bench
     assert bench.max_over_ranks(3.5, 1) == 3.5
-    assert bench.throughput(296, 1, 10, 1000.0) == 6 * 296 * 10
+    assert bench.throughput(296, 1, 10, 1000.0) == bench.GRADS_PER_STEP * 296 * 10
 
 
 def _uid_worker(rank, world, port, out):
