@@ -233,9 +233,10 @@ int egt_gradient_rows(egt_game* game, int32_t player, int32_t rank, int32_t worl
  * egt_timing(game, 1) switches egt_step / cfr_step / saddle_gap* to eager launches,
  * each bracketed by a pair of CUDA events on the library's stream (the stream the
  * kernels run on), and clears the accumulators; egt_timing(game, 0) switches back to
- * CUDA-graph replay.  egt_timing_get writes HOST out[EGT_N_KERNEL_KINDS][3]:
- * total device ms, launches, and game-launches that did work (a masked EGT launch
- * only works on the games whose step focuses on that player), per kernel kind. */
+ * CUDA-graph replay.  egt_timing_get writes HOST out[EGT_N_KERNEL_KINDS][4]:
+ * total device ms, launches, game-launches that did work (a masked EGT launch only works
+ * on the games whose step focuses on that player), and the compulsory HBM bytes of that
+ * work, per kernel kind. */
 #define EGT_KERNEL_GRAD_AY 0  /* gradient kernel, player 0: A y        */
 #define EGT_KERNEL_GRAD_ATX 1 /* gradient kernel, player 1: A^T x      */
 #define EGT_KERNEL_TREE 2     /* treeplex kernel (SBR / prox / BR / CFR / combine) */

@@ -281,10 +281,10 @@ class Game:
         _check(self._L.egt_timing(self._h, int(bool(enable))))
 
     def timing_get(self):
-        """{kind: (ms, launches, active game-launches)} since the last timing(True)."""
-        out = np.zeros(3 * len(KERNEL_KINDS))
+        """{kind: (ms, launches, active game-launches, algorithmic bytes)} since timing(True)."""
+        out = np.zeros(4 * len(KERNEL_KINDS))
         _check(self._L.egt_timing_get(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
-        return {k: tuple(out[3 * i:3 * i + 3]) for i, k in enumerate(KERNEL_KINDS)}
+        return {k: tuple(out[4 * i:4 * i + 4]) for i, k in enumerate(KERNEL_KINDS)}
 
     def get_avg_strategy(self, player, out=None):
         if out is None:

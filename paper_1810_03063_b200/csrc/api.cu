@@ -75,12 +75,13 @@ struct egt_game {
     // kernel timing mode (egt_timing): eager launches bracketed by CUDA events
     int timing = 0;
     std::vector<int> focus_host;    // per-game focus of the current EGT iteration (timing mode)
-    struct Pending { int kind; long long active; cudaEvent_t a, b; };
+    struct Pending { int kind; long long active; double bytes; cudaEvent_t a, b; };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> ev_pool;
     double t_ms[EGT_N_KERNEL_KINDS] = {0};
     double t_launch[EGT_N_KERNEL_KINDS] = {0};
     double t_active[EGT_N_KERNEL_KINDS] = {0};
+    double t_bytes[EGT_N_KERNEL_KINDS] = {0};
 };
 
 const char* egt_last_error(void) { return g_err.c_str(); }
@@ -676,6 +677,7 @@ static cudaError_t timing_flush(egt_game* G) {
         G->t_ms[p.kind] += ms;
         G->t_launch[p.kind] += 1;
         G->t_active[p.kind] += (double)p.active;
+        G->t_bytes[p.kind] += p.bytes;
         G->ev_pool.push_back(p.a);
         G->ev_pool.push_back(p.b);
     }
@@ -694,21 +696,48 @@ static long long active_games(egt_game* G, const int* mask, int want) {
 }
 
 template <class F>
-static cudaError_t timed(egt_game* G, int kind, long long active, F&& launch) {
+static cudaError_t timed(egt_game* G, int kind, long long active, F&& launch, double bytes_per_game = 0.0) {
     if (!G->timing) return launch();
     cudaEvent_t a = pool_event(G), b = pool_event(G);
     cudaError_t e = cudaEventRecord(a, G->st);
     if (e == cudaSuccess) e = launch();
     if (e == cudaSuccess) e = cudaEventRecord(b, G->st);
     if (e != cudaSuccess) return e;
-    G->pending.push_back({kind, active, a, b});
+    G->pending.push_back({kind, active, bytes_per_game * (double)active, a, b});
     if (G->pending.size() >= 1024) return timing_flush(G);
     return cudaSuccess;
 }
 
+// compulsory HBM bytes of one treeplex pass of one game: every vector the
+// pass reads or writes, n_pub x H elements each (read-modify-write vectors count twice)
+static double tree_bytes_per_game(const egt_game* G, int p, const TreeArgs& A) {
+    int n = 0;
+    const bool has_grad = A.mode == TM_SBR || A.mode == TM_PROX || A.mode == TM_BR || A.mode == TM_CFR;
+    n += has_grad;
+    if (A.center.ok()) n += A.mode == TM_CFR ? 2 : 1;
+    n += A.regret.ok() ? 2 : 0;
+    n += A.avg.ok() ? 2 : 0;
+    n += A.out_b.ok() + A.out_q.ok() + A.comb_in.ok() + A.comb_out.ok();
+    return (double)n * G->host.pl[p].n_pub * G->host.H * G->esz;
+}
+
+// compulsory HBM bytes of one gradient of one game
+static double grad_bytes_per_game(const egt_game* G, int p) {
+    const HostGame& H = G->host;
+    std::vector<char> seen(H.pl[1 - p].n_pub, 0);
+    int rd = 0;
+    for (const Terminal& t : H.terms)
+        if (t.last_seq[1 - p] != 0 && !seen[t.last_seq[1 - p]]) {
+            seen[t.last_seq[1 - p]] = 1;
+            ++rd;
+        }
+    return (double)(rd + (int)H.pl[p].rows_term.size() + 2) * H.H * G->esz;
+}
+
 static cudaError_t tree(egt_game* G, int p, const TreeArgs& A) {
-    return timed(G, EGT_KERNEL_TREE, active_games(G, A.mask, A.want),
-                 [&] { return launch_tree(G->dg, G->dp[p], p, A, G->st); });
+    return timed(
+        G, EGT_KERNEL_TREE, active_games(G, A.mask, A.want),
+        [&] { return launch_tree(G->dg, G->dp[p], p, A, G->st); }, G->timing ? tree_bytes_per_game(G, p, A) : 0.0);
 }
 // the other ranks' rows of a sharded gradient, summed in by an in-place NCCL all-reduce
 static cudaError_t allreduce_grad(egt_game* G, int p, VecRef out) {
@@ -726,8 +755,10 @@ static cudaError_t allreduce_grad(egt_game* G, int p, VecRef out) {
 }
 
 static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0) {
-    cudaError_t e = timed(G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
-                          [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st); });
+    cudaError_t e = timed(
+        G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
+        [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st); },
+        G->timing ? grad_bytes_per_game(G, p) : 0.0);
     if (e != cudaSuccess) return e;
     return allreduce_grad(G, p, out);
 }
@@ -1143,7 +1174,7 @@ extern "C" int saddle_gap_device(egt_game* G, int32_t which, double* dev_out) {
 extern "C" int egt_timing(egt_game* G, int32_t enable) {
     if (!G) return fail(EGT_E_ARG, "null game");
     CK(timing_flush(G));
-    for (int k = 0; k < EGT_N_KERNEL_KINDS; ++k) G->t_ms[k] = G->t_launch[k] = G->t_active[k] = 0.0;
+    for (int k = 0; k < EGT_N_KERNEL_KINDS; ++k) G->t_ms[k] = G->t_launch[k] = G->t_active[k] = G->t_bytes[k] = 0.0;
     G->timing = enable != 0;
     if (!G->timing) G->focus_host.clear();
     return 0;
@@ -1153,9 +1184,10 @@ extern "C" int egt_timing_get(egt_game* G, double* host_out) {
     if (!G || !host_out) return fail(EGT_E_ARG, "bad argument");
     CK(timing_flush(G));
     for (int k = 0; k < EGT_N_KERNEL_KINDS; ++k) {
-        host_out[3 * k + 0] = G->t_ms[k];
-        host_out[3 * k + 1] = G->t_launch[k];
-        host_out[3 * k + 2] = G->t_active[k];
+        host_out[4 * k + 0] = G->t_ms[k];
+        host_out[4 * k + 1] = G->t_launch[k];
+        host_out[4 * k + 2] = G->t_active[k];
+        host_out[4 * k + 3] = G->t_bytes[k];
     }
     return 0;
 }
