@@ -596,7 +596,7 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 static constexpr int TH_HPL = 1, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
 
 size_t tree_smem_bytes(const DevPlayer& P, int esz) {
-    return sizeof(double) * 64 + (size_t)esz * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + P.n_nodes) +
+    return sizeof(double) * 64 + (size_t)esz * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + 3 * P.n_nodes) +
            sizeof(int) * (size_t)(6 * P.n_nodes + P.n_levels * TH_WARPS + 1);
 }
 
@@ -611,13 +611,12 @@ struct TreeNodeCtx {
 template <class T>
 __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
-                                               T* __restrict__ rg) {
+                                               T* __restrict__ rg, T sc, T wgt, T iw) {
     const int mode = C.mode;
+    for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= sc;  // the objective's scale (see tree_kernel)
     if (mode == TM_SBR) {
         // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
         // i* = argmax qbar, w = mu beta_j
-        const T wgt = C.mu * (T)P.beta[(size_t)m * Hp + h];
-        const T iw = T(1) / wgt;
         T mn = big_value<T>();
         for (int a = 0; a < n; ++a) mn = fmin(mn, col[a * TH_HANDS]);
         T S = T(0);
@@ -633,8 +632,7 @@ __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlay
     if (mode == TM_PROX) {
         // shifted-gradient SBR in multiplicative form (R16):
         // qbar_i ~ zbar_i exp(-g_i / beta), value = -beta log sum_i zbar_i exp(-g_i / beta)
-        const T beta = (T)P.beta[(size_t)m * Hp + h];
-        const T ib = T(1) / beta;
+        const T beta = wgt, ib = iw;
         const T* __restrict__ zr = cz + (size_t)first * Hp + h;
         T mn = big_value<T>();
         for (int a = 0; a < n; ++a)
@@ -692,15 +690,13 @@ __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlay
 template <int N, class T>
 __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                  int m, int h, int Hp, T logn, T* __restrict__ cz,
-                                                 T* __restrict__ rg) {
+                                                 T* __restrict__ rg, T sc, T wgt, T iw) {
     T x[N];
 #pragma unroll
-    for (int a = 0; a < N; ++a) x[a] = col[a * TH_HANDS];
+    for (int a = 0; a < N; ++a) x[a] = sc * col[a * TH_HANDS];
     const int mode = C.mode;
     T value;
     if (mode == TM_SBR) {
-        const T wgt = C.mu * (T)P.beta[(size_t)m * Hp + h];
-        const T iw = T(1) / wgt;
         T mn = x[0];
 #pragma unroll
         for (int a = 1; a < N; ++a) mn = fmin(mn, x[a]);
@@ -715,8 +711,7 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
         for (int a = 0; a < N; ++a) x[a] *= inv;
         value = mn - wgt * (log(S) - logn);
     } else if (mode == TM_PROX) {
-        const T beta = (T)P.beta[(size_t)m * Hp + h];
-        const T ib = T(1) / beta;
+        const T beta = wgt, ib = iw;
         const T* __restrict__ zr = cz + (size_t)first * Hp + h;
         T z[N];
 #pragma unroll
@@ -784,13 +779,13 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
 template <class T>
 __device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                    int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
-                                                   T* __restrict__ rg) {
+                                                   T* __restrict__ rg, T sc, T wgt, T iw) {
     switch (n) {  // warp-uniform: every lane works on the same node
 #define EGT_NODE_CASE(K) \
-    case K: return tree_node_up_n<K, T>(C, P, col, first, m, h, Hp, logn, cz, rg);
+    case K: return tree_node_up_n<K, T>(C, P, col, first, m, h, Hp, logn, cz, rg, sc, wgt, iw);
         EGT_NODE_CASE(1) EGT_NODE_CASE(2) EGT_NODE_CASE(3) EGT_NODE_CASE(4)
 #undef EGT_NODE_CASE
-        default: return tree_node_up(C, P, col, first, n, m, h, Hp, logn, cz, rg);
+        default: return tree_node_up(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
     }
 }
 
@@ -868,7 +863,9 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
     const bool has_grad = mode == TM_SBR || mode == TM_PROX || mode == TM_BR || mode == TM_CFR;
     T* rootv = tile + (size_t)n_pub * TH_HANDS;                   // [n_root][TH_HANDS]
     T* s_logn = rootv + (size_t)P.n_root * TH_HANDS;              // [n_nodes]
-    int* s_first = reinterpret_cast<int*>(s_logn + n_nodes);
+    T* s_wgt = s_logn + n_nodes;                                  // [n_nodes] (mu) beta_j (all-valid games)
+    T* s_iw = s_wgt + n_nodes;                                    // [n_nodes] its reciprocal
+    int* s_first = reinterpret_cast<int*>(s_iw + n_nodes);
     int* s_nact = s_first + n_nodes;
     int* s_par = s_nact + n_nodes;
     int* s_bs = s_par + n_nodes;
@@ -888,11 +885,22 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
     for (int i = tid; i < 64; i += TH_NT) s_exptab[i] = exp2((double)i / 64.0);
     const uint8_t* __restrict__ valid_g = G.tab_valid + (size_t)g * G.n_bs * Hp;
     const bool all_valid = G.all_valid != 0;
+    // simplex weights: w_j = mu beta_j (SBR) or beta_j (prox); beta_j depends on the hand only
+    // through board validity, so for all-valid games one value per node serves every hand
+    const double wmu = mode == TM_SBR ? A.mu[g] : 1.0;
+    if (all_valid)
+        for (int i = tid; i < n_nodes; i += TH_NT) {
+            const double w = wmu * P.beta[(size_t)i * Hp];
+            s_wgt[i] = (T)w;
+            s_iw[i] = (T)(1.0 / w);
+        }
 
-    // ---- gradient tile: asynchronous 16-byte copies (LDGSTS), all rows in flight, then each
-    // thread scales the chunks it copied by sc = gsign (* step for prox)
+    // ---- gradient tile: asynchronous 16-byte copies (LDGSTS), all rows in flight.  The tile
+    // keeps the raw gradient; the objective's scale sc = gsign (* step for prox) multiplies an
+    // entry when a node reads it, and child values are pushed divided by sc.
+    const double scd = mode == TM_PROX ? A.gsign * A.mu[g] : A.gsign;
+    const T sc = (T)scd, inv_sc = (T)(1.0 / scd);
     if (has_grad) {
-        const T sc = (T)(mode == TM_PROX ? A.gsign * A.mu[g] : A.gsign);
         const T* __restrict__ gp = A.g.at<T>(g) + h0;
         constexpr int EPC = 16 / sizeof(T);  // elements per 16-byte chunk
         constexpr int per_row = TH_HANDS / EPC;
@@ -906,12 +914,6 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
             }
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        if (sc != T(1))
-            for (int c = tid; c < n_chunks; c += TH_NT) {
-                T* t = tile + (c / per_row) * TH_HANDS + EPC * (c % per_row);
-#pragma unroll
-                for (int e = 0; e < EPC; ++e) t[e] *= sc;
-            }
     }
     __syncthreads();
 
@@ -935,12 +937,21 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
                     const int c = lane + 32 * j, h = h0 + c;
                     T* col = tile + (size_t)first * TH_HANDS + c;
                     T value = T(0);
-                    if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]))
-                        value = tree_node_up_any(C, P, col, first, n, m, h, Hp, logn, cz, rg);
-                    else
+                    if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h])) {
+                        T wgt, iw;
+                        if (all_valid) {
+                            wgt = s_wgt[m];
+                            iw = s_iw[m];
+                        } else {
+                            wgt = (T)(wmu * P.beta[(size_t)m * Hp + h]);
+                            iw = T(1) / wgt;
+                        }
+                        value = tree_node_up_any(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
+                    } else {
                         for (int a = 0; a < n; ++a) col[a * TH_HANDS] = T(0);
+                    }
                     if (rs >= 0) rootv[rs * TH_HANDS + c] = value;
-                    else tile[par * TH_HANDS + c] += value;
+                    else tile[par * TH_HANDS + c] += value * inv_sc;
                 }
             }
             __syncthreads();
@@ -955,7 +966,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
             for (int j = 0; j < TH_HPL; ++j) {
                 const int c = lane + 32 * j;
                 if (h0 + c < G.H) {
-                    double u = (double)tile[c];
+                    double u = scd * (double)tile[c];
                     for (int r = 0; r < P.n_root; ++r) u += (double)rootv[r * TH_HANDS + c];
                     v += u;
                 }
