@@ -44,6 +44,7 @@ def build(force=False, verbose=False):
                "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
+            cmd[1:1] = os.environ.get("EGT_EXTRA_NVCC", "").split()  # experiments only
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

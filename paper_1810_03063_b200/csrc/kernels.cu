@@ -49,6 +49,25 @@ __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict_
 // fp32 mode: the library exp on non-positive arguments (<= 2 ulp)
 __device__ __forceinline__ float exp_nonpos(float x, const double* __restrict__) { return expf(x); }
 
+// log(S) for S >= 1 (a softmax normaliser): fp32 hardware log as the start, one Newton step
+// y <- y - 1 + S exp(-y) (error ~1e-14 relative; two steps would be exact to rounding)
+__device__ __forceinline__ double log_ge1(double S, const double* __restrict__ tab) {
+    const double y0 = (double)__logf((float)S);
+    return y0 - 1.0 + S * exp_nonpos(-y0, tab);
+}
+__device__ __forceinline__ float log_ge1(float S, const double* __restrict__) { return logf(S); }
+
+// 1/x for x > 0 normal: hardware approximation + two Newton steps (~1 ulp)
+__device__ __forceinline__ double rcp_pos(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ float rcp_pos(float x) { return __frcp_rn(x); }
+
 template <class T>
 __device__ __forceinline__ T big_value() { return sizeof(T) == 8 ? (T)DBL_MAX : (T)FLT_MAX; }
 
@@ -594,6 +613,9 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 // q_i = q_{p_j} * qbar_i in place and the requested outputs (behavioural, sequence form,
 // EGT convex combinations, CFR average) are written row by row.
 static constexpr int TH_HPL = 1, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
+#ifndef TREE_MIN_CTAS
+#define TREE_MIN_CTAS 4
+#endif
 
 size_t tree_smem_bytes(const DevPlayer& P, int esz) {
     return sizeof(double) * 64 + (size_t)esz * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + 3 * P.n_nodes) +
@@ -602,17 +624,17 @@ size_t tree_smem_bytes(const DevPlayer& P, int esz) {
 
 template <class T>
 struct TreeNodeCtx {
-    int mode, cfr_plus;
+    int cfr_plus;
     T mu;
     const double* __restrict__ exptab;
 };
 
 // Bottom-up work of simplex (node m, hand h) on its column; returns the simplex value.
-template <class T>
+template <int MODE, class T>
 __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
                                                T* __restrict__ rg, T sc, T wgt, T iw) {
-    const int mode = C.mode;
+    constexpr int mode = MODE;
     for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= sc;  // the objective's scale (see tree_kernel)
     if (mode == TM_SBR) {
         // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
@@ -687,14 +709,14 @@ __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlay
 
 // The same bottom-up work for a node with a compile-time number of actions N: the N
 // entries are read once into registers and written once.
-template <int N, class T>
+template <int N, int MODE, class T>
 __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                  int m, int h, int Hp, T logn, T* __restrict__ cz,
                                                  T* __restrict__ rg, T sc, T wgt, T iw) {
     T x[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) x[a] = sc * col[a * TH_HANDS];
-    const int mode = C.mode;
+    constexpr int mode = MODE;
     T value;
     if (mode == TM_SBR) {
         T mn = x[0];
@@ -706,10 +728,10 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
             x[a] = exp_nonpos((mn - x[a]) * iw, C.exptab);
             S += x[a];
         }
-        const T inv = T(1) / S;
+        const T inv = rcp_pos(S);
 #pragma unroll
         for (int a = 0; a < N; ++a) x[a] *= inv;
-        value = mn - wgt * (log(S) - logn);
+        value = mn - wgt * (log_ge1(S, C.exptab) - logn);
     } else if (mode == TM_PROX) {
         const T beta = wgt, ib = iw;
         const T* __restrict__ zr = cz + (size_t)first * Hp + h;
@@ -726,7 +748,7 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
             x[a] = z[a] > T(0) ? z[a] * exp_nonpos((mn - x[a]) * ib, C.exptab) : T(0);
             S += x[a];
         }
-        const T inv = T(1) / S;
+        const T inv = rcp_pos(S);
 #pragma unroll
         for (int a = 0; a < N; ++a) x[a] *= inv;
         value = mn - beta * log(S);
@@ -776,16 +798,16 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
     return value;
 }
 
-template <class T>
+template <int MODE, class T>
 __device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                    int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
                                                    T* __restrict__ rg, T sc, T wgt, T iw) {
     switch (n) {  // warp-uniform: every lane works on the same node
 #define EGT_NODE_CASE(K) \
-    case K: return tree_node_up_n<K, T>(C, P, col, first, m, h, Hp, logn, cz, rg, sc, wgt, iw);
+    case K: return tree_node_up_n<K, MODE, T>(C, P, col, first, m, h, Hp, logn, cz, rg, sc, wgt, iw);
         EGT_NODE_CASE(1) EGT_NODE_CASE(2) EGT_NODE_CASE(3) EGT_NODE_CASE(4)
 #undef EGT_NODE_CASE
-        default: return tree_node_up(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
+        default: return tree_node_up<MODE, T>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
     }
 }
 
@@ -793,7 +815,6 @@ __device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const Dev
 // All global reads of the node are issued before any use (one round trip per node).
 template <class T>
 struct TreeDownCtx {
-    int mode;
     T tau, alpha;
     const T* __restrict__ bin;
     const T* __restrict__ ci;
@@ -803,7 +824,7 @@ struct TreeDownCtx {
     T* __restrict__ av;
 };
 
-template <int N, class T>
+template <int N, int MODE, class T>
 __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool ok, T qp, T unif, int first,
                                                  T* col, int h, int Hp) {
     const size_t ix0 = (size_t)first * Hp + h;
@@ -811,8 +832,8 @@ __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool o
 #pragma unroll
     for (int a = 0; a < N; ++a) {
         if (!ok) b[a] = T(0);
-        else if (D.mode == TM_UNIFORM) b[a] = unif;
-        else if (D.mode == TM_COMBINE) b[a] = D.bin[ix0 + (size_t)a * Hp];
+        else if (MODE == TM_UNIFORM) b[a] = unif;
+        else if (MODE == TM_COMBINE) b[a] = D.bin[ix0 + (size_t)a * Hp];
         else b[a] = col[a * TH_HANDS];
         cv[a] = D.co ? D.ci[ix0 + (size_t)a * Hp] : T(0);
         avv[a] = D.av ? D.av[ix0 + (size_t)a * Hp] : T(0);
@@ -829,29 +850,29 @@ __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool o
     }
 }
 
-template <class T>
+template <int MODE, class T>
 __device__ __forceinline__ void tree_node_down_any(const TreeDownCtx<T>& D, bool ok, T qp, int first, int n,
                                                    T* col, int h, int Hp) {
     const T unif = T(1) / n;
     switch (n) {
-        case 1: tree_node_down_n<1, T>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 2: tree_node_down_n<2, T>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 3: tree_node_down_n<3, T>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 4: tree_node_down_n<4, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 1: tree_node_down_n<1, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 2: tree_node_down_n<2, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 3: tree_node_down_n<3, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 4: tree_node_down_n<4, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
         default: break;
     }
     for (int a0 = 0; a0 < n; a0 += 4) {  // wider nodes: four actions per round trip
         const int k = min(4, n - a0);
         T* c0 = col + a0 * TH_HANDS;
-        if (k == 4) tree_node_down_n<4, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else if (k == 3) tree_node_down_n<3, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else if (k == 2) tree_node_down_n<2, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else tree_node_down_n<1, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        if (k == 4) tree_node_down_n<4, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 3) tree_node_down_n<3, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 2) tree_node_down_n<2, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else tree_node_down_n<1, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
     }
 }
 
-template <class T>
-__global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
+template <class T, int MODE>
+__global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     double* s_exptab = reinterpret_cast<double*>(sm_raw);        // [64] 2^(j/64) (fp64 exp only)
     T* tile = reinterpret_cast<T*>(s_exptab + 64);                // [n_pub][TH_HANDS]
@@ -859,7 +880,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
     if (A.mask && A.mask[g] != A.want) return;
     const int Hp = G.H_pad, n_pub = P.n_pub, n_nodes = P.n_nodes, n_lv = P.n_levels;
     const int h0 = blockIdx.x * TH_HANDS;
-    const int mode = A.mode;
+    constexpr int mode = MODE;
     const bool has_grad = mode == TM_SBR || mode == TM_PROX || mode == TM_BR || mode == TM_CFR;
     T* rootv = tile + (size_t)n_pub * TH_HANDS;                   // [n_root][TH_HANDS]
     T* s_logn = rootv + (size_t)P.n_root * TH_HANDS;              // [n_nodes]
@@ -919,7 +940,6 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
 
     // ---- bottom-up, deepest level first
     TreeNodeCtx<T> C;
-    C.mode = mode;
     C.cfr_plus = A.cfr_plus;
     C.mu = (mode == TM_SBR) ? (T)A.mu[g] : T(1);
     C.exptab = s_exptab;
@@ -946,7 +966,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
                             wgt = (T)(wmu * P.beta[(size_t)m * Hp + h]);
                             iw = T(1) / wgt;
                         }
-                        value = tree_node_up_any(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
+                        value = tree_node_up_any<MODE, T>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
                     } else {
                         for (int a = 0; a < n; ++a) col[a * TH_HANDS] = T(0);
                     }
@@ -1007,7 +1027,6 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
     }
     const T* __restrict__ bin = (mode == TM_COMBINE) ? cz : nullptr;
     TreeDownCtx<T> Dn;
-    Dn.mode = mode;
     Dn.tau = tau;
     Dn.alpha = alpha;
     Dn.bin = bin;
@@ -1040,7 +1059,7 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
                 const int c = lane + 32 * j, h = h0 + c;
                 const bool ok = h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
                 const T qp = par == 0 ? (ok ? T(1) : T(0)) : tile[par * TH_HANDS + c];
-                tree_node_down_any(Dn, ok, qp, first, n, tile + (size_t)first * TH_HANDS + c, h, Hp);
+                tree_node_down_any<MODE, T>(Dn, ok, qp, first, n, tile + (size_t)first * TH_HANDS + c, h, Hp);
             }
         }
         __syncthreads();
@@ -1049,8 +1068,22 @@ __global__ void __launch_bounds__(TH_NT, 4 / TH_HPL) tree_kernel(DevGame G, DevP
 
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st) {
     dim3 grid((G.H_pad + TH_HANDS - 1) / TH_HANDS, G.n_games);
-    if (G.esz == 4) tree_kernel<float><<<grid, TH_NT, tree_smem_bytes(P, 4), st>>>(G, P, player, A);
-    else tree_kernel<double><<<grid, TH_NT, tree_smem_bytes(P, 8), st>>>(G, P, player, A);
+    const size_t sm = tree_smem_bytes(P, G.esz);
+#define EGT_TREE_LAUNCH(M)                                                                            \
+    case M:                                                                                           \
+        if (G.esz == 4) tree_kernel<float, M><<<grid, TH_NT, sm, st>>>(G, P, player, A);              \
+        else tree_kernel<double, M><<<grid, TH_NT, sm, st>>>(G, P, player, A);                        \
+        break;
+    switch (A.mode) {  // one specialised kernel per mode: no mode branches, fewer live registers
+        EGT_TREE_LAUNCH(TM_SBR)
+        EGT_TREE_LAUNCH(TM_PROX)
+        EGT_TREE_LAUNCH(TM_BR)
+        EGT_TREE_LAUNCH(TM_CFR)
+        EGT_TREE_LAUNCH(TM_UNIFORM)
+        EGT_TREE_LAUNCH(TM_COMBINE)
+        default: return cudaErrorInvalidValue;
+    }
+#undef EGT_TREE_LAUNCH
     return cudaGetLastError();
 }
 
@@ -1065,7 +1098,11 @@ static cudaError_t prepare_t() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, T>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(tree_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    const void* tk[] = {(const void*)tree_kernel<T, TM_SBR>,     (const void*)tree_kernel<T, TM_PROX>,
+                        (const void*)tree_kernel<T, TM_BR>,      (const void*)tree_kernel<T, TM_CFR>,
+                        (const void*)tree_kernel<T, TM_UNIFORM>, (const void*)tree_kernel<T, TM_COMBINE>};
+    for (const void* f : tk)
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     return e;
 }
 
