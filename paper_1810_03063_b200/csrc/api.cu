@@ -215,6 +215,15 @@ static void shard_rows(const PlayerLayout& L, int rank, int world, int& r0, int&
     }
 }
 
+static int max_chunk_terms(const PlayerLayout& L, int r0, const std::vector<int>& chunks) {
+    int mx = 0;
+    for (size_t c = 0; c + 1 < chunks.size(); ++c) {
+        const int a = L.rows_term[r0 + chunks[c]], b = L.rows_term[r0 + chunks[c + 1] - 1];
+        mx = std::max(mx, L.term_off[b + 1] - L.term_off[a]);
+    }
+    return mx;
+}
+
 // A DevPlayer view restricted to shard `rank` of `world` (device chunk table allocated into allocs).
 static int make_slice(egt_game* G, int p, int rank, int world, DevPlayer& out, std::vector<void*>& allocs) {
     int r0, r1;
@@ -224,6 +233,7 @@ static int make_slice(egt_game* G, int p, int rank, int world, DevPlayer& out, s
     out.rows_term = G->dp_full[p].rows_term + r0;
     out.n_rows_term = r1 - r0;
     out.n_chunks = (int)chunks.size() - 1;
+    out.max_chunk_terms = max_chunk_terms(G->host.pl[p], r0, chunks);
     void* d = nullptr;
     if (cudaMalloc(&d, sizeof(int) * chunks.size()) != cudaSuccess)
         return fail(EGT_E_CUDA, "cudaMalloc (shard chunks)");
@@ -377,6 +387,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         P.n_root = L.n_root;
         P.n_chunks = (int)L.chunk_off.size() - 1;
         P.chunk_off = co;
+        P.max_chunk_terms = max_chunk_terms(L, 0, L.chunk_off);
         P.node_first = a;
         P.node_nact = b;
         P.node_parent = c;

@@ -19,6 +19,7 @@ constexpr int EGT_MAX_HANDS = 1280;
 constexpr int TREE_WARPS = 8;
 // terminals per CTA of the staged river gradient kernel (rows are never split)
 constexpr int GRAD_CHUNK_TERMS = 32;
+constexpr int GRAD_CHUNK_MAX_TERMS = 64;  // a chunk never exceeds this (rows are small)
 
 enum NodeKind { ND_DECISION = 0, ND_CHANCE = 1, ND_TERMINAL = 2 };
 enum TermKind { T_FOLD_P1 = 0, T_FOLD_P2 = 1, T_SHOWDOWN = 2 };

@@ -337,6 +337,10 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     constexpr int NW = NT / 32, NP = NT * K;  // positions padded to NP
     __shared__ T wtot[NW];
     __shared__ __align__(8) uint64_t bar[3];
+    // the chunk's terminals (<= GRAD_CHUNK_MAX_TERMS): opponent row, kind, weight, and the
+    // row each one completes (-1: more terminals of its row follow)
+    __shared__ int t_so[GRAD_CHUNK_MAX_TERMS], t_kind[GRAD_CHUNK_MAX_TERMS], t_end[GRAD_CHUNK_MAX_TERMS];
+    __shared__ double t_w[GRAD_CHUNK_MAX_TERMS];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
     const int Hp = G.H_pad, H = G.H, n_ce = G.n_ce, W = G.seg_w;
@@ -355,6 +359,14 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     const T* __restrict__ vo = vin.at<T>(g);
     T* __restrict__ outg = gout.at<T>(g);
     const int* __restrict__ tidx = P.term_idx;
+    const int nT = T1 - T0;
+    for (int i = tid; i < nT; i += NT) {
+        const DevTerm tm = G.terms[tidx[T0 + i]];
+        t_so[i] = player ? tm.seq[0] : tm.seq[1];
+        t_kind[i] = tm.kind;
+        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
+        t_end[i] = -1;
+    }
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -371,6 +383,10 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     }
     for (int i = H + tid; i < Hp; i += NT) ob[i] = T(0);
     __syncthreads();
+    for (int r = r0 + tid; r < r1; r += NT) {
+        const int srow = P.rows_term[r];
+        t_end[P.term_off[srow + 1] - 1 - T0] = srow;
+    }
     if (tid == 0) {
         const unsigned bD = Hp * sizeof(T), bU2 = Hp * sizeof(uint2), bU = Hp * sizeof(uint32_t),
                        bC = n_ce * sizeof(uint16_t);
@@ -381,8 +397,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         bulk_g2s(lohi, G.tab_lohi + (size_t)g * Hp, bU, &bar[0]);
         bulk_g2s(cent, G.tab_cent + (size_t)g * n_ce, bC, &bar[0]);
         for (int q = 0; q < 2 && T0 + q < T1; ++q) {
-            const DevTerm& tm = G.terms[tidx[T0 + q]];
-            const int so = player ? tm.seq[0] : tm.seq[1];
+            const int so = t_so[q];
             if (so) {
                 mbar_expect_tx(&bar[1 + q], bD);
                 bulk_g2s(vb + q * NP, vo + (size_t)so * Hp, bD, &bar[1 + q]);
@@ -403,17 +418,15 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     for (int j = 0; j < K; ++j) racc[j] = T(0);
     unsigned par[2] = {0u, 0u};
     mbar_wait(&bar[0], 0);
-    int r = r0;
+    __syncthreads();  // t_end
     for (int ti = T0; ti < T1; ++ti) {
-        const int q = (ti - T0) & 1;
-        const DevTerm tm = G.terms[tidx[ti]];
-        const int so = player ? tm.seq[0] : tm.seq[1];
-        const bool sd = tm.kind == 2;
+        const int q = (ti - T0) & 1, li = ti - T0;
+        const int so = t_so[li];
+        const bool sd = t_kind[li] == 2;
         // prefetch terminal ti+1's row into the other buffer (its previous reader, terminal
         // ti-1, finished phase A before that terminal's first barrier)
         if (tid == 0 && ti > T0 && ti + 1 < T1) {
-            const DevTerm& T1n = G.terms[tidx[ti + 1]];
-            const int so1 = player ? T1n.seq[0] : T1n.seq[1];
+            const int so1 = t_so[li + 1];
             if (so1) {
                 fence_proxy_async();
                 mbar_expect_tx(&bar[1 + (q ^ 1)], Hp * sizeof(T));
@@ -485,7 +498,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         }
         __syncthreads();
         // ---- phase C (positions beyond H compute on padding and are never stored)
-        const T scale = (T)(tm.kappa * G.kappa_game[g] * tm.amount);
+        const T scale = (T)t_w[li];
         T pre = pbase;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
@@ -515,8 +528,8 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             pre += x[j];
         }
         // ---- row end: stage prior_self * acc, one bulk store per row
-        const int srow = P.rows_term[r];
-        if (ti + 1 == P.term_off[srow + 1]) {
+        const int srow = t_end[li];
+        if (srow >= 0) {
             if (tid == 0) bulk_wait_read0();  // the previous row's store has left ob
             __syncthreads();
 #pragma unroll
@@ -528,7 +541,6 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             fence_proxy_async();
             __syncthreads();
             if (tid == 0) bulk_s2g(outg + (size_t)srow * Hp, ob, Hp * sizeof(T));
-            ++r;
         }
     }
     if (tid == 0) bulk_wait0();
@@ -562,7 +574,7 @@ static bool staged_ok(const DevGame& G) {
 template <class T>
 static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
                                      const int* mask, int want, cudaStream_t st) {
-    if (staged_ok(G)) {
+    if (staged_ok(G) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
         const int gl = staged_gl_log2(G);

@@ -71,6 +71,7 @@ struct DevPlayer {
     const int* rows_term;    // [n_rows_term]
     int n_chunks;
     const int* chunk_off;    // [n_chunks+1] ranges of rows_term, one CTA each (staged gradient kernel)
+    int max_chunk_terms;     // most terminals in one chunk (the staged kernel takes <= GRAD_CHUNK_MAX_TERMS)
 };
 
 enum TreeMode { TM_SBR = 0, TM_PROX = 1, TM_BR = 2, TM_CFR = 3, TM_UNIFORM = 4, TM_COMBINE = 5 };
