@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--timing-steps", type=int, default=3, help="steps of the per-kernel event-timing pass")
     ap.add_argument("--converge-games", type=int, default=16,
                     help="also time EGT/as and CFR+ to eps_sad <= --eps-mbb on this many endgames (0: skip)")
-    ap.add_argument("--eps-mbb", type=float, default=1.0, help="target saddle gap in milli-big-blinds")
+    ap.add_argument("--eps-mbb", type=float, nargs="+", default=[100.0, 10.0, 1.0],
+                    help="saddle-gap targets in milli-big-blinds (time to each, median game)")
     ap.add_argument("--converge-max-steps", type=int, default=4000)
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="f32: the optional fp32 mode (fp32 vectors and arithmetic, DESIGN.md row 9)")
@@ -97,13 +98,14 @@ def throughput(games_per_rank, world, steps, ms, shard=False):
     return GRADS_PER_STEP * games_per_rank * (1 if shard else world) * steps / (ms / 1e3)
 
 
-def time_to_gap(P, spec, boards, p1, p2, solver, eps_chips, max_steps, check_every=10):
-    """Wall time (CUDA events) for every game of the batch to reach eps_sad <= eps_chips:
-    graph-launched solver steps, eps_sad on the device after each step, read back every
-    `check_every` steps (sum of regrets in mbb; 1 mbb = big blind / 1000)."""
+def time_to_gap(P, spec, boards, p1, p2, solver, eps_mbb, max_steps, check_every=10, precision="f64"):
+    """Device time (CUDA events) until the median game of the batch reaches eps_sad <= each
+    target in eps_mbb (sum of regrets in milli-big-blinds, 1 mbb = big blind
+    / 1000 chips): graph-launched solver steps, eps_sad on the device after each step, read
+    back every `check_every` steps (an event is recorded at every check)."""
     import torch
     n = len(boards)
-    game = P.Game(P.RIVER, n_games=n, river=spec, boards=boards, prior1=p1, prior2=p2)
+    game = P.Game(P.RIVER, n_games=n, river=spec, boards=boards, prior1=p1, prior2=p2, precision=precision)
     st = torch.cuda.current_stream()
     game.set_stream(st)
     gap = torch.zeros(n, dtype=torch.float64, device="cuda")
@@ -115,32 +117,36 @@ def time_to_gap(P, spec, boards, p1, p2, solver, eps_chips, max_steps, check_eve
         game.cfr_init(P.CFR_PLUS)
         step = lambda: game.cfr_step(1)  # noqa: E731
         which = 1
-    done_at = np.full(n, -1)
+    mbb = spec["big_blind"] / 1000.0
+    targets = sorted(eps_mbb, reverse=True)
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0 = torch.cuda.Event(enable_timing=True)
     ev0.record(st)
+    checks = []  # (steps, event, median gap, max gap)
     steps = 0
     while steps < max_steps:
         for _ in range(check_every):
             step()
             game.saddle_gap_device(which, gap)
             steps += 1
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(st)
         g = gap.cpu().numpy()
-        newly = (done_at < 0) & (g <= eps_chips)
-        done_at[newly] = steps
-        if (done_at >= 0).all():
+        checks.append((steps, ev, float(np.median(g)), float(np.max(g))))
+        if checks[-1][3] <= targets[-1] * mbb:
             break
-    ev1.record(st)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
     sc = game.egt_scalars()
     game.close()
-    reached = done_at >= 0
-    return {"solver": solver, "games": n, "eps_chips": eps_chips, "reached": int(reached.sum()),
-            "steps_median": float(np.median(done_at[reached])) if reached.any() else None,
-            "steps_max": int(done_at.max()) if reached.all() else None, "steps_run": steps,
-            "seconds": ms / 1e3, "final_gap_median": float(np.median(g)),
-            "grad_evals_per_game": float(sc[0, 7])}
+    out = {"solver": solver, "games": n, "precision": precision, "steps_run": steps,
+           "seconds_run": ev0.elapsed_time(checks[-1][1]) / 1e3,
+           "final_gap_mbb": {"median": checks[-1][2] / mbb, "max": checks[-1][3] / mbb},
+           "grad_evals_per_game": float(sc[0, 7]), "to_eps": []}
+    for e in targets:
+        hit = next((c for c in checks if c[2] <= e * mbb), None)
+        out["to_eps"].append({"eps_mbb": e, "median_game_steps": hit[0] if hit else None,
+                              "seconds": ev0.elapsed_time(hit[1]) / 1e3 if hit else None})
+    return out
 
 
 def workload_config(args, game=None, world=1):
@@ -444,11 +450,9 @@ def run_b200(args):
         g2.close()
 
     if args.converge_games > 0:
-        from paper_1810_03063_b200 import workloads as W
-        eps = args.eps_mbb * W.river_spec(args.workload)["big_blind"] / 1000.0
         n = args.converge_games
-        conv = [time_to_gap(P, spec, boards[:n], p1[:n], p2[:n], sv, eps, args.converge_max_steps)
-                for sv in ("egt_as", "cfr_plus")]
+        conv = [time_to_gap(P, spec, boards[:n], p1[:n], p2[:n], sv, args.eps_mbb, args.converge_max_steps,
+                            precision=args.precision) for sv in ("egt_as", "cfr_plus")]
         if rank == 0:
             line["time_to_gap"] = conv
 

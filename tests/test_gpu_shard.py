@@ -90,3 +90,28 @@ def test_one_rank_nccl_solver_is_identical(solver):
     kt = games[1].timing_get()
     games[1].timing(False)
     assert kt["comm"][1] >= 2                    # the all-reduces ran
+
+
+def test_kernel_timing_accounting():
+    """egt_timing: eager launches bracketed by events; per kind the launches, the game-launches
+    that did work and the algorithmic bytes add up for one EGT/as iteration."""
+    import paper_1810_03063_b200 as P
+    spec = workloads.river_spec("simple")
+    boards = workloads.random_boards(3, 41)
+    p1, p2 = workloads.random_priors(boards, 41)
+    G = P.Game(P.RIVER, n_games=3, river=spec, boards=boards, prior1=p1, prior2=p2)
+    G.egt_init(P.EGT_AS, 30.0, 30.0)
+    G.timing(True)
+    G.egt_step(1)
+    kt = G.timing_get()
+    G.timing(False)
+    # per game: 4 gradients (2 on the focused player's launches, 2 in the excessive-gap check)
+    grads = kt["grad_Ay"][2] + kt["grad_ATx"][2]
+    assert grads == 4 * 3
+    assert kt["grad_Ay"][1] + kt["grad_ATx"][1] == 6          # 4 masked + 2 full launches
+    per_game = [8 * G.H * (G.grad_rows_read[p] + G.grad_rows_written[p] + 2) for p in (0, 1)]
+    assert abs(kt["grad_Ay"][3] - per_game[0] * kt["grad_Ay"][2]) < 1e-6 * kt["grad_Ay"][3]
+    assert kt["tree"][1] == 10 and kt["tree"][0] > 0 and kt["tree"][3] > 0
+    assert kt["scalar"][1] == 2 and kt["comm"][1] == 0
+    G.egt_step(2)  # back on the CUDA graph
+    assert np.isfinite(G.saddle_gap(0)).all()
