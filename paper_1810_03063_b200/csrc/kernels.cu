@@ -480,13 +480,11 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
                 }
             }
         }
-        T wpre = T(0), total = T(0);
-#pragma unroll
-        for (int qq = 0; qq < NW; ++qq) {
-            const T v = wtot[qq];
-            wpre += qq < wid ? v : T(0);
-            total += v;
-        }
+        // block prefix of the warp totals: one load per lane, a warp scan, two shuffles
+        const T wsc = warp_incl_scan(lane < NW ? wtot[lane] : T(0), lane);
+        const T wpre_incl = __shfl_sync(0xffffffffu, wsc, (wid + 31) & 31);
+        const T wpre = wid ? wpre_incl : T(0);
+        const T total = __shfl_sync(0xffffffffu, wsc, NW - 1);
         const T pbase = wpre + incl - run;
         if (sd) {
             T p = pbase;
