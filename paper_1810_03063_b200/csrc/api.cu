@@ -46,10 +46,14 @@ struct egt_game {
     cudaStream_t st = nullptr;      // internal stream (graphs are captured here)
     cudaStream_t user = nullptr;    // caller's stream (nullptr = legacy default)
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaStream_t st2 = nullptr;     // second stream for independent chains inside the graph
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     long long V[2] = {0, 0};        // doubles per game per player vector
     // scratch
     double* partial = nullptr;
     unsigned* counter = nullptr;
+    double* partial2 = nullptr;     // reduction scratch of the second stream
+    unsigned* counter2 = nullptr;
     // solver state
     int solver = SOLVER_NONE;
     int variant = 0;
@@ -273,6 +277,9 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         cudaError_t e = cudaStreamCreateWithFlags(&G->st, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_in, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_out, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&G->st2, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&G->ev_join, cudaEventDisableTiming);
         if (e == cudaSuccess) e = kernels_prepare();
         if (e != cudaSuccess) {
             egt_free_game(G);
@@ -411,7 +418,10 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     const int max_tiles = (H.H + 31) / 32;
     TRY(dalloc(G, &G->partial, (size_t)Gn * max_tiles));
     TRY(dalloc(G, &G->counter, (size_t)Gn));
-    if (cudaMemset(G->counter, 0, sizeof(unsigned) * Gn) != cudaSuccess) {
+    TRY(dalloc(G, &G->partial2, (size_t)Gn * max_tiles));
+    TRY(dalloc(G, &G->counter2, (size_t)Gn));
+    if (cudaMemset(G->counter, 0, sizeof(unsigned) * Gn) != cudaSuccess ||
+        cudaMemset(G->counter2, 0, sizeof(unsigned) * Gn) != cudaSuccess) {
         egt_free_game(G);
         return fail(EGT_E_CUDA, "memset");
     }
@@ -468,6 +478,12 @@ extern "C" void egt_free_game(egt_game* G) {
     for (void* p : G->allocs) cudaFree(p);
     if (G->ev_in) cudaEventDestroy(G->ev_in);
     if (G->ev_out) cudaEventDestroy(G->ev_out);
+    if (G->ev_fork) cudaEventDestroy(G->ev_fork);
+    if (G->ev_join) cudaEventDestroy(G->ev_join);
+    if (G->st2) {
+        cudaStreamSynchronize(G->st2);
+        cudaStreamDestroy(G->st2);
+    }
     if (G->st) cudaStreamDestroy(G->st);
     delete G;
 }
@@ -891,31 +907,53 @@ static int record_egt_iteration(egt_game* G) {
         CK(tree(G, p, A));
     }
     if (var == EGT_AS) {
-        // excessive gap at the candidate: phi_{mu_x+}(y+) and -f_{mu_y+}(x+); refreshes the caches
+        // excessive gap at the candidate: phi_{mu_x+}(y+) and -f_{mu_y+}(x+) (refreshes the
+        // caches), then the stopping test (Alg. 3 line 5) at the candidate from the same
+        // gradients A y+ and A^T x+.  The two players' chains are independent: in graph mode
+        // player 1's runs on a second stream (own reduction scratch) beside player 0's -- not
+        // when sharded, where both chains' all-reduces must keep one order on every rank.
+        const bool fork = !G->timing && !G->comm;
+        cudaStream_t main_st = G->st;
+        if (fork) {
+            CK(cudaEventRecord(G->ev_fork, main_st));
+            CK(cudaStreamWaitEvent(G->st2, G->ev_fork, 0));
+        }
         for (int p = 0; p < 2; ++p) {
             const int o = 1 - p;
-            CK(grad(G, p, slot2(G, G->S[o], o, 1), vec(G->GR[p], G->V[p])));
-            TreeArgs A = base_args();
-            A.mode = TM_SBR;
-            A.g = vec(G->GR[p], G->V[p]);
-            A.gsign = GSIGN[p];
-            A.mu = S.mu_cand + (size_t)p * Gn;
-            A.out_b = slot2(G, G->C[p], p, 1);
-            A.value = S.val + (size_t)p * Gn;
-            A.partial = G->partial;
-            A.counter = G->counter;
-            CK(tree(G, p, A));
+            if (fork) G->st = p == 0 ? main_st : G->st2;
+            double* partial = (fork && p == 1) ? G->partial2 : G->partial;
+            unsigned* counter = (fork && p == 1) ? G->counter2 : G->counter;
+            int r = 0;
+            cudaError_t e = grad(G, p, slot2(G, G->S[o], o, 1), vec(G->GR[p], G->V[p]));
+            if (e == cudaSuccess) {
+                TreeArgs A = base_args();
+                A.mode = TM_SBR;
+                A.g = vec(G->GR[p], G->V[p]);
+                A.gsign = GSIGN[p];
+                A.mu = S.mu_cand + (size_t)p * Gn;
+                A.out_b = slot2(G, G->C[p], p, 1);
+                A.value = S.val + (size_t)p * Gn;
+                A.partial = partial;
+                A.counter = counter;
+                e = tree(G, p, A);
+            }
+            if (e == cudaSuccess) {
+                TreeArgs A = base_args();
+                A.mode = TM_BR;
+                A.g = vec(G->GR[p], G->V[p]);
+                A.gsign = GSIGN[p];
+                A.value = G->gapval + (size_t)p * Gn;
+                A.partial = partial;
+                A.counter = counter;
+                e = tree(G, p, A);
+            }
+            G->st = main_st;
+            if (e != cudaSuccess) r = fail(EGT_E_CUDA, std::string("excessive-gap check: ") + cudaGetErrorString(e));
+            if (r) return r;
         }
-        // stopping test (Alg. 3 line 5) at the candidate from the same gradients: A y+ and A^T x+
-        for (int p = 0; p < 2; ++p) {
-            TreeArgs A = base_args();
-            A.mode = TM_BR;
-            A.g = vec(G->GR[p], G->V[p]);
-            A.gsign = GSIGN[p];
-            A.value = G->gapval + (size_t)p * Gn;
-            A.partial = G->partial;
-            A.counter = G->counter;
-            CK(tree(G, p, A));
+        if (fork) {
+            CK(cudaEventRecord(G->ev_join, G->st2));
+            CK(cudaStreamWaitEvent(main_st, G->ev_join, 0));
         }
     }
     CK(scalar_k(G, [&] { return launch_egt_accept(var, Gn, S, G->st); }));
