@@ -550,7 +550,10 @@ static size_t grad_smem_bytes(const DevGame& G) {
     return (size_t)G.esz * (size_t)(3 * G.H_pad + 1 + G.n_ce);
 }
 
-static constexpr int STG_NT = 416, STG_K = 3, STG_CH = 6;  // positions <= 1248, 52 cards x 8 lanes
+#ifndef STG_CH_DEF
+#define STG_CH_DEF 6
+#endif
+static constexpr int STG_NT = 416, STG_K = 3, STG_CH = STG_CH_DEF;  // positions <= 1248, card segments <= 6 x 8 lanes
 
 static size_t grad_staged_smem_bytes(const DevGame& G) {
     const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
