@@ -28,9 +28,9 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
 
 // exp(x) for x <= 0 to ~1 ulp: x = (64 k + j) ln2 / 64 + r, |r| <= ln2 / 128,
 // exp(x) = 2^k' * tab[j] * (1 + r + ... + r^5/120) (truncation < 4e-17 relative).
-// tab[j] = 2^(j/64) lives in shared memory.  Returns 0 below exp's normal range.
+// tab[j] = 2^(j/64) lives in shared memory.  Arguments below -707 give exp(-707).
 __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict__ tab) {
-    if (x < -707.0) return 0.0;  // keeps 2^k' * v a normal number
+    x = fmax(x, -707.0);  // keeps 2^k' * v normal; exp(-707) ~ 1e-307 stands in for 0
     const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
     const double big = fma(x, 92.332482616893656877, magic);
     const int k = __double2loint(big);
@@ -837,9 +837,16 @@ struct TreeDownCtx {
     T* __restrict__ av;
 };
 
-template <int N, int MODE, class T>
+// OUTS: the set of output rows (TO_* bits) fixed at compile time, or 0 = decided at run time
+enum TreeOuts { TO_B = 1, TO_Q = 2, TO_COMB = 4, TO_AVG = 8 };
+
+template <int N, int MODE, int OUTS, class T>
 __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool ok, T qp, T unif, int first,
                                                  T* col, int h, int Hp) {
+    const bool wb = OUTS ? (OUTS & TO_B) != 0 : D.ob != nullptr;
+    const bool wq = OUTS ? (OUTS & TO_Q) != 0 : D.oq != nullptr;
+    const bool wc = OUTS ? (OUTS & TO_COMB) != 0 : D.co != nullptr;
+    const bool wa = OUTS ? (OUTS & TO_AVG) != 0 : D.av != nullptr;
     const size_t ix0 = (size_t)first * Hp + h;
     T b[N], cv[N], avv[N];
 #pragma unroll
@@ -848,43 +855,43 @@ __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool o
         else if (MODE == TM_UNIFORM) b[a] = unif;
         else if (MODE == TM_COMBINE) b[a] = D.bin[ix0 + (size_t)a * Hp];
         else b[a] = col[a * TH_HANDS];
-        cv[a] = D.co ? D.ci[ix0 + (size_t)a * Hp] : T(0);
-        avv[a] = D.av ? D.av[ix0 + (size_t)a * Hp] : T(0);
+        cv[a] = wc ? D.ci[ix0 + (size_t)a * Hp] : T(0);
+        avv[a] = wa ? D.av[ix0 + (size_t)a * Hp] : T(0);
     }
 #pragma unroll
     for (int a = 0; a < N; ++a) {
         const T q = qp * b[a];
         col[a * TH_HANDS] = q;
         const size_t ix = ix0 + (size_t)a * Hp;
-        if (D.ob) D.ob[ix] = b[a];
-        if (D.oq) D.oq[ix] = q;
-        if (D.co) D.co[ix] = (T(1) - D.tau) * cv[a] + D.tau * q;
-        if (D.av) D.av[ix] = D.alpha * q + (T(1) - D.alpha) * avv[a];
+        if (wb) D.ob[ix] = b[a];
+        if (wq) D.oq[ix] = q;
+        if (wc) D.co[ix] = (T(1) - D.tau) * cv[a] + D.tau * q;
+        if (wa) D.av[ix] = D.alpha * q + (T(1) - D.alpha) * avv[a];
     }
 }
 
-template <int MODE, class T>
+template <int MODE, int OUTS, class T>
 __device__ __forceinline__ void tree_node_down_any(const TreeDownCtx<T>& D, bool ok, T qp, int first, int n,
                                                    T* col, int h, int Hp) {
     const T unif = T(1) / n;
     switch (n) {
-        case 1: tree_node_down_n<1, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 2: tree_node_down_n<2, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 3: tree_node_down_n<3, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
-        case 4: tree_node_down_n<4, MODE, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 1: tree_node_down_n<1, MODE, OUTS, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 2: tree_node_down_n<2, MODE, OUTS, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 3: tree_node_down_n<3, MODE, OUTS, T>(D, ok, qp, unif, first, col, h, Hp); return;
+        case 4: tree_node_down_n<4, MODE, OUTS, T>(D, ok, qp, unif, first, col, h, Hp); return;
         default: break;
     }
     for (int a0 = 0; a0 < n; a0 += 4) {  // wider nodes: four actions per round trip
         const int k = min(4, n - a0);
         T* c0 = col + a0 * TH_HANDS;
-        if (k == 4) tree_node_down_n<4, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else if (k == 3) tree_node_down_n<3, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else if (k == 2) tree_node_down_n<2, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
-        else tree_node_down_n<1, MODE, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        if (k == 4) tree_node_down_n<4, MODE, OUTS, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 3) tree_node_down_n<3, MODE, OUTS, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else if (k == 2) tree_node_down_n<2, MODE, OUTS, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
+        else tree_node_down_n<1, MODE, OUTS, T>(D, ok, qp, unif, first + a0, c0, h, Hp);
     }
 }
 
-template <class T, int MODE>
+template <class T, int MODE, int OUTS>
 __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     double* s_exptab = reinterpret_cast<double*>(sm_raw);        // [64] 2^(j/64) (fp64 exp only)
@@ -1025,7 +1032,7 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
     }
 
     // ---- top-down, shallowest level first
-    const bool want_td = A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR;
+    const bool want_td = OUTS ? true : (A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR);
     if (!want_td) return;
     T* __restrict__ ob = A.out_b.ok() ? A.out_b.at<T>(g) : nullptr;
     T* __restrict__ oq = A.out_q.ok() ? A.out_q.at<T>(g) : nullptr;
@@ -1072,7 +1079,7 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
                 const int c = lane + 32 * j, h = h0 + c;
                 const bool ok = h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h]);
                 const T qp = par == 0 ? (ok ? T(1) : T(0)) : tile[par * TH_HANDS + c];
-                tree_node_down_any<MODE, T>(Dn, ok, qp, first, n, tile + (size_t)first * TH_HANDS + c, h, Hp);
+                tree_node_down_any<MODE, OUTS, T>(Dn, ok, qp, first, n, tile + (size_t)first * TH_HANDS + c, h, Hp);
             }
         }
         __syncthreads();
@@ -1082,12 +1089,26 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st) {
     dim3 grid((G.H_pad + TH_HANDS - 1) / TH_HANDS, G.n_games);
     const size_t sm = tree_smem_bytes(P, G.esz);
+    const int outs = (A.out_b.ok() ? TO_B : 0) | (A.out_q.ok() ? TO_Q : 0) | (A.comb_out.ok() ? TO_COMB : 0) |
+                     (A.avg.ok() ? TO_AVG : 0);
+#define EGT_TREE_GO(M, O)                                                                       \
+    {                                                                                           \
+        if (G.esz == 4) tree_kernel<float, M, O><<<grid, TH_NT, sm, st>>>(G, P, player, A);     \
+        else tree_kernel<double, M, O><<<grid, TH_NT, sm, st>>>(G, P, player, A);               \
+        return cudaGetLastError();                                                              \
+    }
+    // the solver's hot (mode, outputs) combinations get fully specialised kernels
+    if (A.mode == TM_SBR && outs == TO_B) EGT_TREE_GO(TM_SBR, TO_B)
+    if (A.mode == TM_SBR && outs == (TO_Q | TO_COMB)) EGT_TREE_GO(TM_SBR, TO_Q | TO_COMB)
+    if (A.mode == TM_PROX && outs == TO_COMB) EGT_TREE_GO(TM_PROX, TO_COMB)
+    if (A.mode == TM_COMBINE && outs == TO_COMB) EGT_TREE_GO(TM_COMBINE, TO_COMB)
+    if (A.mode == TM_CFR && outs == (TO_Q | TO_AVG)) EGT_TREE_GO(TM_CFR, TO_Q | TO_AVG)
 #define EGT_TREE_LAUNCH(M)                                                                            \
     case M:                                                                                           \
-        if (G.esz == 4) tree_kernel<float, M><<<grid, TH_NT, sm, st>>>(G, P, player, A);              \
-        else tree_kernel<double, M><<<grid, TH_NT, sm, st>>>(G, P, player, A);                        \
+        if (G.esz == 4) tree_kernel<float, M, 0><<<grid, TH_NT, sm, st>>>(G, P, player, A);           \
+        else tree_kernel<double, M, 0><<<grid, TH_NT, sm, st>>>(G, P, player, A);                     \
         break;
-    switch (A.mode) {  // one specialised kernel per mode: no mode branches, fewer live registers
+    switch (A.mode) {  // otherwise one kernel per mode, outputs decided at run time
         EGT_TREE_LAUNCH(TM_SBR)
         EGT_TREE_LAUNCH(TM_PROX)
         EGT_TREE_LAUNCH(TM_BR)
@@ -1096,6 +1117,7 @@ cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const 
         EGT_TREE_LAUNCH(TM_COMBINE)
         default: return cudaErrorInvalidValue;
     }
+#undef EGT_TREE_GO
 #undef EGT_TREE_LAUNCH
     return cudaGetLastError();
 }
@@ -1111,9 +1133,12 @@ static cudaError_t prepare_t() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, T>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    const void* tk[] = {(const void*)tree_kernel<T, TM_SBR>,     (const void*)tree_kernel<T, TM_PROX>,
-                        (const void*)tree_kernel<T, TM_BR>,      (const void*)tree_kernel<T, TM_CFR>,
-                        (const void*)tree_kernel<T, TM_UNIFORM>, (const void*)tree_kernel<T, TM_COMBINE>};
+    const void* tk[] = {(const void*)tree_kernel<T, TM_SBR, 0>,     (const void*)tree_kernel<T, TM_PROX, 0>,
+                        (const void*)tree_kernel<T, TM_BR, 0>,      (const void*)tree_kernel<T, TM_CFR, 0>,
+                        (const void*)tree_kernel<T, TM_UNIFORM, 0>, (const void*)tree_kernel<T, TM_COMBINE, 0>,
+                        (const void*)tree_kernel<T, TM_SBR, TO_B>,  (const void*)tree_kernel<T, TM_SBR, TO_Q | TO_COMB>,
+                        (const void*)tree_kernel<T, TM_PROX, TO_COMB>, (const void*)tree_kernel<T, TM_COMBINE, TO_COMB>,
+                        (const void*)tree_kernel<T, TM_CFR, TO_Q | TO_AVG>};
     for (const void* f : tk)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     return e;
