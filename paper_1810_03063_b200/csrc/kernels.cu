@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         bulk_g2s(cent, G.tab_cent + (size_t)g * n_ce, bC, &bar[0]);
         for (int q = 0; q < 2 && T0 + q < T1; ++q) {
             const int so = t_so[q];
-            if (so) {
+            if (so && !(q > 0 && so == t_so[q - 1])) {
                 mbar_expect_tx(&bar[1 + q], bD);
                 bulk_g2s(vb + q * NP, vo + (size_t)so * Hp, bD, &bar[1 + q]);
             }
@@ -419,27 +419,34 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     unsigned par[2] = {0u, 0u};
     mbar_wait(&bar[0], 0);
     __syncthreads();  // t_end
+    // w's chunk, its total and this thread's prefix survive a terminal: the next terminal
+    // reuses them (and the card sums) when it reads the same opponent row (a fold / call pair
+    // of one decision node); the first of such a pair then writes the full card-array prefixes
+    T x[K];
+    T total = T(0), pbase = T(0);
     for (int ti = T0; ti < T1; ++ti) {
         const int q = (ti - T0) & 1, li = ti - T0;
         const int so = t_so[li];
         const bool sd = t_kind[li] == 2;
+        const bool reuse = li > 0 && so == t_so[li - 1];
+        const bool full = sd || (li + 1 < nT && t_so[li + 1] == so && t_kind[li + 1] == 2);
         // prefetch terminal ti+1's row into the other buffer (its previous reader, terminal
         // ti-1, finished phase A before that terminal's first barrier)
         if (tid == 0 && ti > T0 && ti + 1 < T1) {
             const int so1 = t_so[li + 1];
-            if (so1) {
+            if (so1 && so1 != so) {
                 fence_proxy_async();
                 mbar_expect_tx(&bar[1 + (q ^ 1)], Hp * sizeof(T));
                 bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)so1 * Hp, Hp * sizeof(T), &bar[1 + (q ^ 1)]);
             }
         }
-        if (so) {
+        if (so && !reuse) {
             mbar_wait(&bar[1 + q], par[q]);
             par[q] ^= 1u;
         }
+        if (!reuse) {  // warp-uniform (the whole CTA takes the same branch)
         const T* vrow = vb + q * NP;
         // ---- phase A: w = prior_opp * v_opp in chunks of K positions, warp scan of the chunk sums
-        T x[K];
         T run = T(0);
 #pragma unroll
         for (int j = 0; j < K; ++j) {
@@ -468,15 +475,15 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
                 if (part >= o) inc += u;
             }
             if (has_seg) {
+                // the same accumulation order in both cases, so a segment total never depends
+                // on whether the terminal needs the full prefixes (folds: end slot only)
+                const int end_slot = sgi * W + W - 1;
                 T run2 = inc - ssum;
-                if (sd) {
 #pragma unroll
-                    for (int j = 0; j < CH; ++j) {
-                        if (sbeg + j < send) Ex[sbeg + j] = run2;
-                        run2 += y[j];
-                    }
-                } else if (send == sgi * W + W && send > sbeg) {
-                    Ex[send - 1] = inc;  // fold: only the segment totals (end slot)
+                for (int j = 0; j < CH; ++j) {
+                    const int e = sbeg + j;
+                    if (e < send && (full || e == end_slot)) Ex[e] = run2;
+                    run2 += y[j];
                 }
             }
         }
@@ -484,9 +491,9 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         const T wsc = warp_incl_scan(lane < NW ? wtot[lane] : T(0), lane);
         const T wpre_incl = __shfl_sync(0xffffffffu, wsc, (wid + 31) & 31);
         const T wpre = wid ? wpre_incl : T(0);
-        const T total = __shfl_sync(0xffffffffu, wsc, NW - 1);
-        const T pbase = wpre + incl - run;
-        if (sd) {
+        total = __shfl_sync(0xffffffffu, wsc, NW - 1);
+        pbase = wpre + incl - run;
+        if (full) {
             T p = pbase;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
@@ -495,6 +502,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             }
         }
         __syncthreads();
+        }  // !reuse
         // ---- phase C (positions beyond H compute on padding and are never stored)
         const T scale = (T)t_w[li];
         T pre = pbase;
