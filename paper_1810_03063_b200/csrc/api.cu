@@ -54,6 +54,8 @@ struct egt_game {
     unsigned* counter = nullptr;
     double* partial2 = nullptr;     // reduction scratch of the second stream
     unsigned* counter2 = nullptr;
+    double *partial_br = nullptr, *partial2_br = nullptr;  // fused best-response reductions
+    unsigned *counter_br = nullptr, *counter2_br = nullptr;
     // solver state
     int solver = SOLVER_NONE;
     int variant = 0;
@@ -370,7 +372,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         P.n_rows_term = (int)L.rows_term.size();
         P.max_level_width = 0;
         for (int l = 0; l < P.n_levels; ++l) P.max_level_width = std::max(P.max_level_width, L.lvl_off[l + 1] - L.lvl_off[l]);
-        int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt, *co, *so, *sn, *rs;
+        int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt, *co, *so, *sn, *rs, *ss;
         double* be;
         TRY(upload(G, &a, L.first));
         TRY(upload(G, &b, L.nact));
@@ -388,6 +390,9 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         TRY(upload(G, &so, L.sched_off));
         TRY(upload(G, &sn, L.sched_nodes));
         TRY(upload(G, &rs, L.root_slot));
+        TRY(upload(G, &ss, L.seq_slot));
+        P.seq_slot = ss;
+        P.n_int = L.n_int;
         P.sched_off = so;
         P.sched_nodes = sn;
         P.root_slot = rs;
@@ -420,8 +425,14 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(dalloc(G, &G->counter, (size_t)Gn));
     TRY(dalloc(G, &G->partial2, (size_t)Gn * max_tiles));
     TRY(dalloc(G, &G->counter2, (size_t)Gn));
+    TRY(dalloc(G, &G->partial_br, (size_t)Gn * max_tiles));
+    TRY(dalloc(G, &G->counter_br, (size_t)Gn));
+    TRY(dalloc(G, &G->partial2_br, (size_t)Gn * max_tiles));
+    TRY(dalloc(G, &G->counter2_br, (size_t)Gn));
     if (cudaMemset(G->counter, 0, sizeof(unsigned) * Gn) != cudaSuccess ||
-        cudaMemset(G->counter2, 0, sizeof(unsigned) * Gn) != cudaSuccess) {
+        cudaMemset(G->counter2, 0, sizeof(unsigned) * Gn) != cudaSuccess ||
+        cudaMemset(G->counter_br, 0, sizeof(unsigned) * Gn) != cudaSuccess ||
+        cudaMemset(G->counter2_br, 0, sizeof(unsigned) * Gn) != cudaSuccess) {
         egt_free_game(G);
         return fail(EGT_E_CUDA, "memset");
     }
@@ -923,9 +934,13 @@ static int record_egt_iteration(egt_game* G) {
             if (fork) G->st = p == 0 ? main_st : G->st2;
             double* partial = (fork && p == 1) ? G->partial2 : G->partial;
             unsigned* counter = (fork && p == 1) ? G->counter2 : G->counter;
+            double* br_partial = (fork && p == 1) ? G->partial2_br : G->partial_br;
+            unsigned* br_counter = (fork && p == 1) ? G->counter2_br : G->counter_br;
             int r = 0;
             cudaError_t e = grad(G, p, slot2(G, G->S[o], o, 1), vec(G->GR[p], G->V[p]));
             if (e == cudaSuccess) {
+                // one pass: the smoothed response (cache + EGV term) and the best response of
+                // the same gradient (the stopping test at the candidate)
                 TreeArgs A = base_args();
                 A.mode = TM_SBR;
                 A.g = vec(G->GR[p], G->V[p]);
@@ -935,16 +950,9 @@ static int record_egt_iteration(egt_game* G) {
                 A.value = S.val + (size_t)p * Gn;
                 A.partial = partial;
                 A.counter = counter;
-                e = tree(G, p, A);
-            }
-            if (e == cudaSuccess) {
-                TreeArgs A = base_args();
-                A.mode = TM_BR;
-                A.g = vec(G->GR[p], G->V[p]);
-                A.gsign = GSIGN[p];
-                A.value = G->gapval + (size_t)p * Gn;
-                A.partial = partial;
-                A.counter = counter;
+                A.br_value = G->gapval + (size_t)p * Gn;
+                A.br_partial = br_partial;
+                A.br_counter = br_counter;
                 e = tree(G, p, A);
             }
             G->st = main_st;

@@ -361,6 +361,10 @@ static void build_layout(HostGame& G) {
             }
         }
         L.sched_off[(size_t)L.depth * TREE_WARPS] = (int)L.sched_nodes.size();
+        L.seq_slot.assign(L.n_pub, -1);
+        L.n_int = 0;
+        for (int s = 0; s < L.n_pub; ++s)
+            if (L.kid_off[s + 1] > L.kid_off[s]) L.seq_slot[s] = L.n_int++;
     }
 }
 

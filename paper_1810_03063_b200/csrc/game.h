@@ -59,8 +59,8 @@ struct PlayerLayout {
     // nodes sharing a parent sequence (other than the empty one) run on one warp, so their
     // values can be added into the parent entry without races; root nodes (parent = empty
     // sequence) keep their values in root_slot[m] >= 0
-    std::vector<int> sched_off, sched_nodes, root_slot;
-    int n_root = 0;
+    std::vector<int> sched_off, sched_nodes, root_slot, seq_slot;
+    int n_root = 0, n_int = 0;
     int depth = 0;
 };
 

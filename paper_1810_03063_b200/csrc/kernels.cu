@@ -68,6 +68,27 @@ __device__ __forceinline__ double rcp_pos(double x) {
 }
 __device__ __forceinline__ float rcp_pos(float x) { return __frcp_rn(x); }
 
+// Per-game value: the CTA's sum v (valid in thread 0) goes to partial[g][tile]; the last
+// CTA of the game sums the tiles in order (deterministic) into value[g].  Contains a barrier.
+__device__ __forceinline__ void game_value_reduce(double v, double* partial, unsigned* counter, double* value, int g) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        partial[(size_t)g * gridDim.x + blockIdx.x] = v;
+        __threadfence();
+        const unsigned ticket = atomicAdd(&counter[g], 1u);
+        last = ticket == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double s = 0.0;
+        const volatile double* pp = partial + (size_t)g * gridDim.x;
+        for (unsigned i = 0; i < gridDim.x; ++i) s += pp[i];
+        value[g] = s;
+        counter[g] = 0;
+    }
+}
+
 template <class T>
 __device__ __forceinline__ T big_value() { return sizeof(T) == 8 ? (T)DBL_MAX : (T)FLT_MAX; }
 
@@ -639,7 +660,8 @@ static constexpr int TH_HPL = 1, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, 
 #endif
 
 size_t tree_smem_bytes(const DevPlayer& P, int esz) {
-    return sizeof(double) * 64 + (size_t)esz * ((size_t)TH_HANDS * (P.n_pub + P.n_root) + 3 * P.n_nodes) +
+    return sizeof(double) * 64 + (size_t)esz * ((size_t)TH_HANDS * (P.n_pub + 2 * P.n_root + P.n_int) + 3 * P.n_nodes) +
+           sizeof(int) * (size_t)P.n_pub +
            sizeof(int) * (size_t)(6 * P.n_nodes + P.n_levels * TH_WARPS + 1);
 }
 
@@ -846,12 +868,12 @@ struct TreeDownCtx {
 };
 
 // OUTS: the set of output rows (TO_* bits) fixed at compile time, or 0 = decided at run time
-enum TreeOuts { TO_B = 1, TO_Q = 2, TO_COMB = 4, TO_AVG = 8 };
+enum TreeOuts { TO_B = 1, TO_Q = 2, TO_COMB = 4, TO_AVG = 8, TO_FUSEBR = 16 };
 
 template <int N, int MODE, int OUTS, class T>
 __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool ok, T qp, T unif, int first,
                                                  T* col, int h, int Hp) {
-    const bool wb = OUTS ? (OUTS & TO_B) != 0 : D.ob != nullptr;
+    const bool wb = OUTS ? (OUTS & TO_B) != 0 : D.ob != nullptr;  // (TO_FUSEBR is a bottom-up flag)
     const bool wq = OUTS ? (OUTS & TO_Q) != 0 : D.oq != nullptr;
     const bool wc = OUTS ? (OUTS & TO_COMB) != 0 : D.co != nullptr;
     const bool wa = OUTS ? (OUTS & TO_AVG) != 0 : D.av != nullptr;
@@ -914,13 +936,16 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
     T* s_logn = rootv + (size_t)P.n_root * TH_HANDS;              // [n_nodes]
     T* s_wgt = s_logn + n_nodes;                                  // [n_nodes] (mu) beta_j (all-valid games)
     T* s_iw = s_wgt + n_nodes;                                    // [n_nodes] its reciprocal
-    int* s_first = reinterpret_cast<int*>(s_iw + n_nodes);
+    T* brv = s_iw + n_nodes;                                      // [n_int][TH_HANDS] fused BR: child values
+    T* brroot = brv + (size_t)P.n_int * TH_HANDS;                 // [n_root][TH_HANDS] fused BR: root values
+    int* s_first = reinterpret_cast<int*>(brroot + (size_t)P.n_root * TH_HANDS);
     int* s_nact = s_first + n_nodes;
     int* s_par = s_nact + n_nodes;
     int* s_bs = s_par + n_nodes;
     int* s_rslot = s_bs + n_nodes;
     int* s_sn = s_rslot + n_nodes;                                // [n_nodes]
     int* s_so = s_sn + n_nodes;                                   // [n_lv * TH_WARPS + 1]
+    int* s_slot = s_so + n_lv * TH_WARPS + 1;                     // [n_pub]
     for (int i = tid; i < n_nodes; i += TH_NT) {
         s_first[i] = P.node_first[i];
         s_nact[i] = P.node_nact[i];
@@ -931,6 +956,10 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
         s_logn[i] = log((T)P.node_nact[i]);
     }
     for (int i = tid; i <= n_lv * TH_WARPS; i += TH_NT) s_so[i] = P.sched_off[i];
+    if (OUTS & TO_FUSEBR) {
+        for (int i = tid; i < n_pub; i += TH_NT) s_slot[i] = P.seq_slot[i];
+        for (int i = tid; i < P.n_int * TH_HANDS; i += TH_NT) brv[i] = T(0);
+    }
     for (int i = tid; i < 64; i += TH_NT) s_exptab[i] = exp2((double)i / 64.0);
     const uint8_t* __restrict__ valid_g = G.tab_valid + (size_t)g * G.n_bs * Hp;
     const bool all_valid = G.all_valid != 0;
@@ -965,6 +994,38 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+
+    // ---- fused best response (stopping test on the same gradient): min_q <q, sc g> bottom-up
+    // on the untouched tile, children's values kept in brv (before the SBR pass edits the tile)
+    if (OUTS & TO_FUSEBR) {
+        for (int L = n_lv - 1; L >= 0; --L) {
+            const int i0 = s_so[L * TH_WARPS + wid], i1 = s_so[L * TH_WARPS + wid + 1];
+            for (int idx = i0; idx < i1; ++idx) {
+                const int m = s_sn[idx];
+                const int first = s_first[m], n = s_nact[m], par = s_par[m], rs = s_rslot[m];
+                const int c = lane, h = h0 + c;
+                T mn = T(0);
+                if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h])) {
+                    mn = big_value<T>();
+                    for (int a = 0; a < n; ++a) {
+                        const int sq = first + a, sl = s_slot[sq];
+                        const T x = sc * tile[sq * TH_HANDS + c] + (sl >= 0 ? brv[sl * TH_HANDS + c] : T(0));
+                        mn = fmin(mn, x);
+                    }
+                }
+                if (rs >= 0) brroot[rs * TH_HANDS + c] = mn;
+                else brv[s_slot[par] * TH_HANDS + c] += mn;
+            }
+            __syncthreads();
+        }
+        double v = 0.0;
+        if (wid == 0 && h0 + lane < G.H) {
+            v = scd * (double)tile[lane];
+            for (int r = 0; r < P.n_root; ++r) v += (double)brroot[r * TH_HANDS + lane];
+        }
+        v = warp_sum(v);
+        game_value_reduce(v, A.br_partial, A.br_counter, A.br_value, g);
+    }
 
     // ---- bottom-up, deepest level first
     TreeNodeCtx<T> C;
@@ -1021,22 +1082,7 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
             }
         }
         v = warp_sum(v);
-        __shared__ bool last;
-        if (tid == 0) {
-            A.partial[(size_t)g * gridDim.x + blockIdx.x] = v;
-            __threadfence();
-            const unsigned ticket = atomicAdd(&A.counter[g], 1u);
-            last = ticket == gridDim.x - 1;
-        }
-        __syncthreads();
-        if (last && tid == 0) {
-            __threadfence();
-            double s = 0.0;
-            const volatile double* pp = A.partial + (size_t)g * gridDim.x;
-            for (unsigned i = 0; i < gridDim.x; ++i) s += pp[i];
-            A.value[g] = s;
-            A.counter[g] = 0;
-        }
+        game_value_reduce(v, A.partial, A.counter, A.value, g);
     }
 
     // ---- top-down, shallowest level first
@@ -1105,6 +1151,10 @@ cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const 
         else tree_kernel<double, M, O><<<grid, TH_NT, sm, st>>>(G, P, player, A);               \
         return cudaGetLastError();                                                              \
     }
+    if (A.br_value) {  // the fused stopping test exists for the excessive-gap check's SBR only
+        if (A.mode != TM_SBR || outs != TO_B) return cudaErrorInvalidValue;
+        EGT_TREE_GO(TM_SBR, TO_B | TO_FUSEBR)
+    }
     // the solver's hot (mode, outputs) combinations get fully specialised kernels
     if (A.mode == TM_SBR && outs == TO_B) EGT_TREE_GO(TM_SBR, TO_B)
     if (A.mode == TM_SBR && outs == (TO_Q | TO_COMB)) EGT_TREE_GO(TM_SBR, TO_Q | TO_COMB)
@@ -1146,7 +1196,8 @@ static cudaError_t prepare_t() {
                         (const void*)tree_kernel<T, TM_UNIFORM, 0>, (const void*)tree_kernel<T, TM_COMBINE, 0>,
                         (const void*)tree_kernel<T, TM_SBR, TO_B>,  (const void*)tree_kernel<T, TM_SBR, TO_Q | TO_COMB>,
                         (const void*)tree_kernel<T, TM_PROX, TO_COMB>, (const void*)tree_kernel<T, TM_COMBINE, TO_COMB>,
-                        (const void*)tree_kernel<T, TM_CFR, TO_Q | TO_AVG>};
+                        (const void*)tree_kernel<T, TM_CFR, TO_Q | TO_AVG>,
+                        (const void*)tree_kernel<T, TM_SBR, TO_B | TO_FUSEBR>};
     for (const void* f : tk)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     return e;

@@ -65,6 +65,8 @@ struct DevPlayer {
     const int* sched_nodes;  // [n_nodes]
     const int* root_slot;    // [n_nodes] slot of a root node's value, -1 otherwise
     int n_root;
+    const int* seq_slot;     // [n_pub] slot of a sequence with child nodes, -1 otherwise
+    int n_int;
     const double* beta;      // [n_nodes][H_pad]
     const int* term_off;     // [n_pub+1] terminals grouped by this player's last sequence
     const int* term_idx;
@@ -94,6 +96,10 @@ struct TreeArgs {
     double* value = nullptr;   // per-game value (SBR/BR)
     double* partial = nullptr; // [G][n_tiles] scratch
     unsigned* counter = nullptr; // [G] zero-initialised
+    // SBR only: also the best-response value of the same gradient (min <q, gsign g>), fused
+    double* br_value = nullptr;
+    double* br_partial = nullptr;
+    unsigned* br_counter = nullptr;
     const int* mask = nullptr; // run game g only if mask[g] == want
     int want = 0;
 };
