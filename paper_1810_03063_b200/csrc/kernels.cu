@@ -845,13 +845,20 @@ template <int MODE, class T>
 __device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                    int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
                                                    T* __restrict__ rg, T sc, T wgt, T iw) {
+    // register-resident widths: up to 9 actions for SBR / BR (one array), fewer for the modes
+    // that also hold the centre or the regrets
+    constexpr int NMAX = (MODE == TM_SBR || MODE == TM_BR) ? 9 : (MODE == TM_PROX ? 6 : 4);
     switch (n) {  // warp-uniform: every lane works on the same node
 #define EGT_NODE_CASE(K) \
-    case K: return tree_node_up_n<K, MODE, T>(C, P, col, first, m, h, Hp, logn, cz, rg, sc, wgt, iw);
-        EGT_NODE_CASE(1) EGT_NODE_CASE(2) EGT_NODE_CASE(3) EGT_NODE_CASE(4)
+    case K:              \
+        if (K <= NMAX) return tree_node_up_n<(K <= NMAX ? K : 1), MODE, T>(C, P, col, first, m, h, Hp, logn, cz, rg, sc, wgt, iw); \
+        break;
+        EGT_NODE_CASE(1) EGT_NODE_CASE(2) EGT_NODE_CASE(3) EGT_NODE_CASE(4) EGT_NODE_CASE(5) EGT_NODE_CASE(6)
+        EGT_NODE_CASE(7) EGT_NODE_CASE(8) EGT_NODE_CASE(9)
 #undef EGT_NODE_CASE
-        default: return tree_node_up<MODE, T>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
+        default: break;
     }
+    return tree_node_up<MODE, T>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
 }
 
 // Top-down work of simplex (node, hand): q_i = q_{p_j} * qbar_i and the requested output rows.
