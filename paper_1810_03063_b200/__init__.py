@@ -8,3 +8,4 @@ if it is missing.
 """
 from .binding import (CFR_PLUS, CFR_RM, CFR_RMP, EGT_AS, EGT_BALANCED, EGT_THEORY, KUHN, LEDUC,  # noqa: F401
                       RIVER, EGTError, Game, load_game, load_library)
+from .solve import solve  # noqa: F401

@@ -1,0 +1,74 @@
+"""The public API end to end (paper_1810_03063_b200.solve) and the C ABI's error paths."""
+import numpy as np
+import pytest
+
+from oracle import br, games, seqform
+from paper_1810_03063_b200 import workloads
+from tests.paritylib import Pair
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("solver", ["egt_as", "egt_balanced", "cfr_plus", "cfr_rmp"])
+def test_solve_kuhn_to_equilibrium(solver):
+    """Kuhn poker's value to player 1 is -1/18 (tests/golden/kuhn.json)."""
+    import paper_1810_03063_b200 as P
+    G = P.Game(P.KUHN, n_games=2)
+    sf = seqform.build(games.kuhn())
+    res = P.solve(G, solver, eps=2e-3, max_iters=20000, check_every=50)
+    assert np.all(res["gap"] <= 2e-3)
+    x = res["strategy"][0][0].reshape(-1)
+    y = res["strategy"][1][0].reshape(-1)
+    pair = Pair("kuhn", n_games=1)
+    # host strategy is [n_pub][n_combos]; map to the oracle's sequence space by labels
+    Gh = pair.game
+    xs = np.zeros((Gh.n_pub[0], Gh.H_pad))
+    ys = np.zeros((Gh.n_pub[1], Gh.H_pad))
+    xs[:, :3] = x.reshape(Gh.n_pub[0], 3)
+    ys[:, :3] = y.reshape(Gh.n_pub[1], 3)
+    xv = pair.from_product(0, 0, xs.reshape(-1))
+    yv = pair.from_product(0, 1, ys.reshape(-1))
+    xv[0] = yv[0] = 1.0
+    value = xv @ (sf.A @ yv)          # player 2's expected payoff; the game value is +1/18
+    assert abs(value - 1.0 / 18.0) <= 2e-3
+    # the reported gap is the oracle's eps_sad of the returned strategies
+    assert abs(br.saddle_gap(sf, xv, yv) - res["gap"][0]) <= 1e-9 * max(1.0, res["gap"][0])
+
+
+def test_solve_river_stops_at_target():
+    import paper_1810_03063_b200 as P
+    boards = workloads.random_boards(4, 77)
+    p1, p2 = workloads.random_priors(boards, 77)
+    G = P.Game(P.RIVER, n_games=4, river=workloads.river_spec("simple"), boards=boards, prior1=p1, prior2=p2)
+    res = P.solve(G, "egt_as", eps_mbb=200.0, max_iters=3000, check_every=20)
+    assert np.all(res["gap"] <= 20.0) and res["iters"] <= 3000
+    x, y = res["strategy"]
+    assert x.shape == (4, G.n_pub[0], G.n_combos) and y.shape == (4, G.n_pub[1], G.n_combos)
+    assert np.all(x >= 0) and np.all(x <= 1 + 1e-12)
+
+
+def test_error_paths():
+    import paper_1810_03063_b200 as P
+    G = P.Game(P.KUHN, n_games=1)
+    with pytest.raises(P.EGTError):
+        G.egt_step(1)                     # before egt_init: EGT_E_STATE
+    with pytest.raises(P.EGTError):
+        G.cfr_step(1)
+    with pytest.raises(P.EGTError):
+        G.saddle_gap(0)                   # no solver yet
+    d = torch.zeros(G.vec_shape(0), dtype=torch.float64, device="cuda")
+    with pytest.raises(P.EGTError):
+        G.egt_gradient(2, d, d)           # bad player
+    G.egt_init(P.EGT_AS, 1.0, 1.0)
+    with pytest.raises(P.EGTError):
+        G.shard(0, 1)                     # after init: EGT_E_STATE
+    with pytest.raises(P.EGTError):      # invalid board (repeated card)
+        P.Game(P.RIVER, n_games=1, river=workloads.river_spec("tiny"), boards=np.array([[1, 1, 2, 3, 4]]))
+    with pytest.raises(P.EGTError):      # negative prior
+        b = workloads.random_boards(1, 3)
+        p1, p2 = workloads.random_priors(b, 3)
+        p1[0, np.flatnonzero(p1[0])[0]] = -1.0
+        P.Game(P.RIVER, n_games=1, river=workloads.river_spec("tiny"), boards=b, prior1=p1, prior2=p2)
+    with pytest.raises(P.EGTError):      # unknown precision
+        P.Game(P.KUHN, n_games=1, precision=7)
