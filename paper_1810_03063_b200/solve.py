@@ -36,7 +36,11 @@ def solve(game, solver="egt_as", eps=None, eps_mbb=None, max_iters=10000, check_
     else:
         game.cfr_init(code)
         step, which = game.cfr_step, 1
-    it = 0
+    # at least one iteration first: the CFR average is defined from iteration 1 on
+    # (Gen-CFR line 34 with alpha^1 = 1)
+    it = min(check_every, max_iters) if max_iters > 0 else 0
+    if it:
+        step(it)
     gap = game.saddle_gap(which)
     while it < max_iters and np.max(gap) > eps:
         n = min(check_every, max_iters - it)
