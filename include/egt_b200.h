@@ -223,6 +223,25 @@ int egt_scalars(egt_game* game, double* host_out);
 int egt_nccl_unique_id(uint8_t* out);
 int egt_shard(egt_game* game, int32_t rank, int32_t world, const uint8_t* id);
 
+/* Fused compute + all-gather over NVLink (replaces the all-reduce of egt_shard): every rank's
+ * gradient kernels store the rows they compute straight into every rank's gradient buffer
+ * (peer memory), then a one-element NCCL all-reduce orders the ranks.  Rows are disjoint, so
+ * no reduction is needed and each gradient crosses NVLink once (an all-reduce moves it twice).
+ * egt_ipc_handles: HOST out[2 * EGT_IPC_HANDLE_BYTES], this rank's gradient buffers (player 0,
+ * player 1) as CUDA IPC handles.  egt_shard_peers: HOST handles[world][2][EGT_IPC_HANDLE_BYTES]
+ * gathered from every rank (own entry ignored); after egt_shard with an NCCL id, before
+ * egt_init / cfr_init; world <= 8.  Applies to the solvers' gradients (egt_gradient keeps the
+ * all-reduce, its output buffer being the caller's). */
+#define EGT_IPC_HANDLE_BYTES 64
+int egt_ipc_handles(egt_game* game, uint8_t* out);
+int egt_shard_peers(egt_game* game, const uint8_t* handles);
+
+/* The fused kernel's stores for shard `rank` of `world` into n_dst DEVICE buffers dsts[] (each
+ * laid out like a gradient of `player`, zeroed by the caller), synchronous, no communication:
+ * several "ranks" emulated on one device must leave every buffer equal to egt_gradient's result. */
+int egt_gradient_rows_to(egt_game* game, int32_t player, int32_t rank, int32_t world, const double* dev_in,
+                         const uint64_t* dsts, int32_t n_dst);
+
 /* Rows of the gradient that shard `rank` of `world` computes, without communication:
  * DEVICE dout receives those rows, every other row 0 (the sum over all ranks is
  * egt_gradient's result).  Synchronous.  For tests and inspection. */

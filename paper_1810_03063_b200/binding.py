@@ -60,7 +60,9 @@ EXPORTS = [
     "egt_init", "egt_step", "cfr_init", "cfr_step", "saddle_gap", "get_avg_strategy",
     "get_strategy_device", "egt_scalars", "egt_last_error", "saddle_gap_device",
     "egt_timing", "egt_timing_get", "egt_nccl_unique_id", "egt_shard", "egt_gradient_rows",
+    "egt_ipc_handles", "egt_shard_peers", "egt_gradient_rows_to",
 ]
+IPC_HANDLE_BYTES = 64
 KERNEL_KINDS = ("grad_Ay", "grad_ATx", "tree", "scalar", "comm")
 NCCL_ID_BYTES = 128
 
@@ -107,6 +109,9 @@ def load_library():
         "egt_nccl_unique_id": ([ctypes.c_char_p], I32),
         "egt_shard": ([P, I32, I32, ctypes.c_char_p], I32),
         "egt_gradient_rows": ([P, I32, I32, I32, VP, VP], I32),
+        "egt_ipc_handles": ([P, ctypes.c_char_p], I32),
+        "egt_shard_peers": ([P, ctypes.c_char_p], I32),
+        "egt_gradient_rows_to": ([P, I32, I32, I32, VP, ctypes.POINTER(ctypes.c_uint64), I32], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -276,6 +281,30 @@ class Game:
             uid = broadcast_uid(nccl_unique_id() if rank == 0 else None)
         buf = None if uid is None else ctypes.create_string_buffer(bytes(uid), NCCL_ID_BYTES)
         _check(self._L.egt_shard(self._h, rank, world, buf))
+
+    def gradient_rows_to(self, player, rank, world, din, dsts):
+        """Shard `rank`'s rows stored into every buffer of dsts (the fused all-gather's stores)."""
+        arr = (ctypes.c_uint64 * len(dsts))(*[_ptr(d) for d in dsts])
+        _check(self._L.egt_gradient_rows_to(self._h, player, rank, world, _ptr(din), arr, len(dsts)))
+
+    def ipc_handles(self):
+        buf = ctypes.create_string_buffer(2 * IPC_HANDLE_BYTES)
+        _check(self._L.egt_ipc_handles(self._h, buf))
+        return buf.raw
+
+    def shard_peers(self, all_handles):
+        """all_handles: bytes of every rank's ipc_handles() in rank order (fused all-gather)."""
+        blob = b"".join(all_handles)
+        _check(self._L.egt_shard_peers(self._h, ctypes.create_string_buffer(blob, len(blob))))
+
+    def shard_fused(self, rank, world):
+        """egt_shard + egt_shard_peers over an initialised torch.distributed group: rank 0's
+        NCCL id and every rank's IPC handles travel over the host-side group."""
+        import torch.distributed as dist
+        self.shard(rank, world)
+        handles = [None] * world
+        dist.all_gather_object(handles, self.ipc_handles())
+        self.shard_peers(handles)
 
     def timing(self, enable):
         _check(self._L.egt_timing(self._h, int(bool(enable))))

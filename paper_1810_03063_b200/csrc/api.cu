@@ -41,6 +41,12 @@ struct egt_game {
     // NCCL all-reduce (sum) per gradient gives every rank the full gradient
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    // fused all-gather (egt_shard_peers): the gradient kernels store their rows into every
+    // rank's gradient buffer over NVLink; a one-element NCCL all-reduce then orders the ranks
+    bool p2p = false;
+    DevPeers peers[2];
+    std::vector<void*> ipc_opened;
+    double* barrier_word = nullptr;
     int esz = 8;                    // bytes per vector element (8: fp64, 4: fp32 mode)
     std::vector<void*> allocs;
     cudaStream_t st = nullptr;      // internal stream (graphs are captured here)
@@ -485,6 +491,7 @@ extern "C" void egt_free_game(egt_game* G) {
         cudaEventDestroy(p.b);
     }
     for (cudaEvent_t e : G->ev_pool) cudaEventDestroy(e);
+    for (void* q : G->ipc_opened) cudaIpcCloseMemHandle(q);
     if (G->comm) nccl_destroy(G->comm);
     for (void* p : G->allocs) cudaFree(p);
     if (G->ev_in) cudaEventDestroy(G->ev_in);
@@ -585,6 +592,71 @@ extern "C" int egt_gradient_rows(egt_game* G, int32_t player, int32_t rank, int3
     for (void* q : tmp) cudaFree(q);
     if (r) return r;
     return end(G);
+}
+
+extern "C" int egt_gradient_rows_to(egt_game* G, int32_t player, int32_t rank, int32_t world, const double* din,
+                                    const uint64_t* dsts, int32_t n_dst) {
+    if (!G || !din || !dsts || player < 0 || player > 1 || world < 1 || rank < 0 || rank >= world || n_dst < 1 ||
+        n_dst > EGT_MAX_PEERS)
+        return fail(EGT_E_ARG, "bad argument");
+    DevPeers pr;
+    pr.n = n_dst;
+    for (int d = 0; d < n_dst; ++d) pr.base[d] = reinterpret_cast<void*>(dsts[d]);
+    std::vector<void*> tmp;
+    DevPlayer P;
+    int r = make_slice(G, player, rank, world, P, tmp);
+    if (!r && begin(G)) r = EGT_E_CUDA;
+    if (!r) {
+        cudaError_t e = launch_gradient(G->dg, P, player, vec(const_cast<double*>(din), G->V[1 - player]),
+                                        vec(reinterpret_cast<double*>(dsts[0]), G->V[player]), nullptr, 0, 0, G->st,
+                                        &pr);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(G->st);
+        if (e != cudaSuccess) r = fail(EGT_E_CUDA, std::string("egt_gradient_rows_to: ") + cudaGetErrorString(e));
+    }
+    for (void* q : tmp) cudaFree(q);
+    if (r) return r;
+    return end(G);
+}
+
+extern "C" int egt_ipc_handles(egt_game* G, uint8_t* out) {
+    if (!G || !out) return fail(EGT_E_ARG, "bad argument");
+    for (int p = 0; p < 2; ++p) {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, G->GR[p]));
+        static_assert(sizeof(h) == EGT_IPC_HANDLE_BYTES, "IPC handle size");
+        memcpy(out + p * sizeof(h), &h, sizeof(h));
+    }
+    return 0;
+}
+
+extern "C" int egt_shard_peers(egt_game* G, const uint8_t* handles) {
+    if (!G || !handles) return fail(EGT_E_ARG, "bad argument");
+    if (!G->comm) return fail(EGT_E_STATE, "egt_shard_peers needs egt_shard with an NCCL id first");
+    if (G->world > EGT_MAX_PEERS) return fail(EGT_E_ARG, "too many ranks for the fused all-gather");
+    if (G->solver != SOLVER_NONE) return fail(EGT_E_STATE, "egt_shard_peers must precede egt_init / cfr_init");
+    if (!G->barrier_word && dalloc(G, &G->barrier_word, 1)) return EGT_E_CUDA;
+    CK(cudaMemset(G->barrier_word, 0, sizeof(double)));
+    for (int p = 0; p < 2; ++p) {
+        G->peers[p].n = G->world;
+        for (int r = 0; r < G->world; ++r) {
+            if (r == G->rank) {
+                G->peers[p].base[r] = G->GR[p];
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            memcpy(&h, handles + ((size_t)r * 2 + p) * sizeof(h), sizeof(h));
+            void* q = nullptr;
+            CK(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+            G->ipc_opened.push_back(q);
+            G->peers[p].base[r] = q;
+        }
+    }
+    G->p2p = true;
+    if (G->graph) {
+        cudaGraphExecDestroy(G->graph);
+        G->graph = nullptr;
+    }
+    return 0;
 }
 
 extern "C" int egt_nccl_unique_id(uint8_t* out) {
@@ -792,13 +864,28 @@ static cudaError_t allreduce_grad(egt_game* G, int p, VecRef out) {
     });
 }
 
+// ranks' barrier after a fused all-gather: a one-element all-reduce on the stream
+static cudaError_t peer_barrier(egt_game* G) {
+    std::string err;
+    NcclApi* a = nccl_api(err);
+    if (!a) return cudaErrorInvalidValue;
+    return timed(G, EGT_KERNEL_COMM, 0, [&] {
+        return a->allReduce(G->barrier_word, G->barrier_word, 1, ncclDouble, ncclSum, G->comm, G->st) == ncclSuccess
+                   ? cudaSuccess
+                   : cudaErrorUnknown;
+    });
+}
+
 static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0) {
+    const bool fused = G->p2p && out.base == G->GR[p] && !out.slot_sel;
     cudaError_t e = timed(
         G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
-        [&] { return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st); },
+        [&] {
+            return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st, fused ? &G->peers[p] : nullptr);
+        },
         G->timing ? grad_bytes_per_game(G, p) : 0.0);
     if (e != cudaSuccess) return e;
-    return allreduce_grad(G, p, out);
+    return fused ? peer_barrier(G) : allreduce_grad(G, p, out);
 }
 template <class F>
 static cudaError_t scalar_k(egt_game* G, F&& launch) {

@@ -122,7 +122,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Hands that do not share their tie group read their own P / Pc from registers.
 template <int NT, int KMAX, int EMAX, typename T>
 __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
-                                                     const int* __restrict__ mask, int want, int all_rows) {
+                                                     const int* __restrict__ mask, int want, int all_rows,
+                                                     DevPeers peers) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     T* sm = reinterpret_cast<T*>(sm_raw);
     constexpr int NW = NT / 32;
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
         }
     }
     const T* __restrict__ pself = static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
-    T* __restrict__ out = gout.at<T>(g) + (size_t)s * Hp;
+    const long long row_off = (long long)g * gout.game_stride + (long long)s * Hp;
     __syncthreads();
     if (fast) {
         const int K = (H + NT - 1) / NT;
@@ -302,9 +303,18 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
             if (j < K && i < H) w[i] = racc[j];
         }
         __syncthreads();
-        for (int i = tid; i < Hp; i += NT) out[i] = i < H ? pself[i] * w[i] : T(0);
+        for (int i = tid; i < Hp; i += NT) acc[i] = i < H ? pself[i] * w[i] : T(0);
     } else {
-        for (int i = tid; i < Hp; i += NT) out[i] = pself[i] * acc[i];
+        for (int i = tid; i < Hp; i += NT) acc[i] *= pself[i];
+    }
+    if (peers.n == 0) {
+        T* __restrict__ out = gout.at<T>(g) + (size_t)s * Hp;
+        for (int i = tid; i < Hp; i += NT) out[i] = acc[i];
+    } else {
+        for (int d = 0; d < peers.n; ++d) {  // this shard's row into every shard's buffer
+            T* __restrict__ out = reinterpret_cast<T*>(peers.base[d]) + row_off;
+            for (int i = tid; i < Hp; i += NT) out[i] = acc[i];
+        }
     }
 }
 
@@ -352,7 +362,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 template <int NT, int K, int CH, int HS, typename T>
 __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
                                                             VecRef gout, const int* __restrict__ mask, int want,
-                                                            int gl_log2) {
+                                                            int gl_log2, DevPeers peers) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     T* sm = reinterpret_cast<T*>(sm_raw);
     constexpr int NW = NT / 32, NP = NT * K;  // positions padded to NP
@@ -565,9 +575,20 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
                 if (i < H) ob[i] = pself[i] * racc[j];
                 racc[j] = T(0);
             }
-            fence_proxy_async();
-            __syncthreads();
-            if (tid == 0) bulk_s2g(outg + (size_t)srow * Hp, ob, Hp * sizeof(T));
+            if (peers.n == 0) {
+                fence_proxy_async();
+                __syncthreads();
+                if (tid == 0) bulk_s2g(outg + (size_t)srow * Hp, ob, Hp * sizeof(T));
+            } else {
+                // fused all-gather: the finished row goes from shared memory straight into every
+                // shard's gradient buffer (peer memory over NVLink), overlapping the next terminals
+                __syncthreads();
+                const long long off = (long long)g * gout.game_stride + (long long)srow * Hp;
+                for (int d = 0; d < peers.n; ++d) {
+                    T* __restrict__ dst = reinterpret_cast<T*>(peers.base[d]) + off;
+                    for (int i = tid; i < Hp; i += NT) dst[i] = ob[i];
+                }
+            }
         }
     }
     if (tid == 0) bulk_wait0();
@@ -603,27 +624,30 @@ static bool staged_ok(const DevGame& G) {
 
 template <class T>
 static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
-                                     const int* mask, int want, cudaStream_t st) {
+                                     const int* mask, int want, cudaStream_t st, const DevPeers& peers) {
     if (staged_ok(G) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
         const int gl = staged_gl_log2(G);
         if (G.hand_size == 2)
             grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, T>
-                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
+                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl, peers);
         else
             grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, T>
-                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl);
+                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl, peers);
         return cudaGetLastError();
     }
     dim3 grid(P.n_rows_term, G.n_games);
     grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>
-        <<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, 0);
+        <<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, 0, peers);
     return cudaGetLastError();
 }
 
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
-                            const int* mask, int want, int all_rows, cudaStream_t st) {
+                            const int* mask, int want, int all_rows, cudaStream_t st, const DevPeers* peers) {
+    const DevPeers none;
+    const DevPeers& pr = peers ? *peers : none;
+    if (pr.n && gout.slot_sel) return cudaErrorInvalidValue;
     if (all_rows) {
         // rows that end no terminal (or that another shard computes) are 0
         if (gout.slot_sel) return cudaErrorInvalidValue;
@@ -638,8 +662,8 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
         if (e != cudaSuccess) return e;
     }
     if (P.n_rows_term == 0) return cudaSuccess;
-    return G.esz == 4 ? launch_gradient_t<float>(G, P, player, vin, gout, mask, want, st)
-                      : launch_gradient_t<double>(G, P, player, vin, gout, mask, want, st);
+    return G.esz == 4 ? launch_gradient_t<float>(G, P, player, vin, gout, mask, want, st, pr)
+                      : launch_gradient_t<double>(G, P, player, vin, gout, mask, want, st, pr);
 }
 
 // ------------------------------------------------------------------ treeplex pass

@@ -76,6 +76,15 @@ struct DevPlayer {
     int max_chunk_terms;     // most terminals in one chunk (the staged kernel takes <= GRAD_CHUNK_MAX_TERMS)
 };
 
+// Fused compute + all-gather of a sharded gradient: every output row a shard computes is
+// stored straight into each listed buffer (its own and its peers' gradient buffers, mapped
+// over NVLink); rows are disjoint across shards, so no reduction is needed.
+constexpr int EGT_MAX_PEERS = 8;
+struct DevPeers {
+    int n = 0;                          // 0: write gout only
+    void* base[EGT_MAX_PEERS] = {};     // game 0, row 0 of each destination (the layout of gout)
+};
+
 enum TreeMode { TM_SBR = 0, TM_PROX = 1, TM_BR = 2, TM_CFR = 3, TM_UNIFORM = 4, TM_COMBINE = 5 };
 
 struct TreeArgs {
@@ -125,7 +134,8 @@ struct DevScalars {
 // all_rows = 1 writes every row of gout (rows without terminals get 0); 0 writes only the
 // rows that end a terminal (the solver's gradient buffers are zeroed once at allocation).
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
-                            const int* mask, int want, int all_rows, cudaStream_t st);
+                            const int* mask, int want, int all_rows, cudaStream_t st,
+                            const DevPeers* peers = nullptr);
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st);
 cudaError_t kernels_prepare();
 size_t tree_smem_bytes(const DevPlayer& P, int esz);

@@ -115,3 +115,47 @@ def test_kernel_timing_accounting():
     assert kt["scalar"][1] == 2 and kt["comm"][1] == 0
     G.egt_step(2)  # back on the CUDA graph
     assert np.isfinite(G.saddle_gap(0)).all()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_fused_allgather_stores_emulated(world):
+    """The fused kernel stores each shard's rows into every shard's buffer: after all emulated
+    ranks ran (one device, no waiting between them), every buffer equals the full gradient."""
+    pair = Pair("river", n_games=3, spec=workloads.river_spec("libratus"), seed=12, sample=[])
+    G = pair.game
+    for p in (0, 1):
+        din = _random_vec(G, 1 - p, 50 + p)
+        full = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
+        G.egt_gradient(p, din, full)
+        bufs = [torch.zeros_like(full) for _ in range(world)]
+        for r in range(world):
+            G.gradient_rows_to(p, r, world, din, bufs)
+        for b in bufs:
+            assert torch.equal(b, full)
+
+
+def test_fused_allgather_solver_one_rank():
+    """egt_shard + egt_shard_peers (IPC handles of this rank) runs the solver with the fused
+    gradient stores and the one-element NCCL barrier inside the graph: identical results."""
+    import paper_1810_03063_b200 as P
+    spec = workloads.river_spec("simple")
+    boards = workloads.random_boards(3, 33)
+    p1, p2 = workloads.random_priors(boards, 33)
+    res = []
+    for fused in (False, True):
+        G = P.Game(P.RIVER, n_games=3, river=spec, boards=boards, prior1=p1, prior2=p2)
+        if fused:
+            G.shard(0, 1, uid=P.binding.nccl_unique_id())
+            G.shard_peers([G.ipc_handles()])
+        G.egt_init(P.EGT_AS, 40.0, 40.0)
+        G.egt_step(5)
+        x = torch.zeros(G.vec_shape(0), dtype=torch.float64, device="cuda")
+        G.get_strategy_device(0, 0, x)
+        res.append((x.cpu().numpy(), G.saddle_gap(0)))
+        if fused:
+            G.timing(True)
+            G.egt_step(1)
+            kt = G.timing_get()
+            G.timing(False)
+            assert kt["comm"][1] >= 4 and kt["comm"][3] == 0      # barriers, no all-reduced bytes
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
