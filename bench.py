@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--converge-max-steps", type=int, default=4000)
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="f32: the optional fp32 mode (fp32 vectors and arithmetic, DESIGN.md row 9)")
+    ap.add_argument("--fused", action="store_true",
+                    help="with --shard: fused compute + all-gather over peer memory instead of the all-reduce")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: every rank holds the same batch and computes a slice of each "
                          "gradient's rows, NCCL all-reduce per gradient (DESIGN.md row 8)")
@@ -339,7 +341,10 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     game.set_stream(stream)
     if args.shard:
-        game.shard(rank, world)
+        if args.fused and world > 1:
+            game.shard_fused(rank, world)
+        else:
+            game.shard(rank, world)
     game.egt_init(P.EGT_AS)  # practical mu (R14)
     gap = torch.zeros(args.batch, dtype=torch.float64, device="cuda")
 

@@ -311,9 +311,12 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
         T* __restrict__ out = gout.at<T>(g) + (size_t)s * Hp;
         for (int i = tid; i < Hp; i += NT) out[i] = acc[i];
     } else {
-        for (int d = 0; d < peers.n; ++d) {  // this shard's row into every shard's buffer
-            T* __restrict__ out = reinterpret_cast<T*>(peers.base[d]) + row_off;
-            for (int i = tid; i < Hp; i += NT) out[i] = acc[i];
+#pragma unroll
+        for (int d = 0; d < EGT_MAX_PEERS; ++d) {  // this shard's row into every shard's buffer
+            if (d < peers.n) {
+                T* __restrict__ out = reinterpret_cast<T*>(peers.base[d]) + row_off;
+                for (int i = tid; i < Hp; i += NT) out[i] = acc[i];
+            }
         }
     }
 }
@@ -584,9 +587,12 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
                 // shard's gradient buffer (peer memory over NVLink), overlapping the next terminals
                 __syncthreads();
                 const long long off = (long long)g * gout.game_stride + (long long)srow * Hp;
-                for (int d = 0; d < peers.n; ++d) {
-                    T* __restrict__ dst = reinterpret_cast<T*>(peers.base[d]) + off;
-                    for (int i = tid; i < Hp; i += NT) dst[i] = ob[i];
+#pragma unroll
+                for (int d = 0; d < EGT_MAX_PEERS; ++d) {  // constant indices: no local copy of peers
+                    if (d < peers.n) {
+                        T* __restrict__ dst = reinterpret_cast<T*>(peers.base[d]) + off;
+                        for (int i = tid; i < Hp; i += NT) dst[i] = ob[i];
+                    }
                 }
             }
         }
