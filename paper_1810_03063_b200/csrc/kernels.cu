@@ -684,7 +684,10 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 // root simplexes keep their values apart.  Top-down (shallowest first) each entry becomes
 // q_i = q_{p_j} * qbar_i in place and the requested outputs (behavioural, sequence form,
 // EGT convex combinations, CFR average) are written row by row.
-static constexpr int TH_HPL = 1, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
+#ifndef TREE_HPL
+#define TREE_HPL 1
+#endif
+static constexpr int TH_HPL = TREE_HPL, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
 #ifndef TREE_MIN_CTAS
 #define TREE_MIN_CTAS 4
 #endif
@@ -1040,25 +1043,34 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
             for (int idx = i0; idx < i1; ++idx) {
                 const int m = s_sn[idx];
                 const int first = s_first[m], n = s_nact[m], par = s_par[m], rs = s_rslot[m];
-                const int c = lane, h = h0 + c;
-                T mn = T(0);
-                if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h])) {
-                    mn = big_value<T>();
-                    for (int a = 0; a < n; ++a) {
-                        const int sq = first + a, sl = s_slot[sq];
-                        const T x = sc * tile[sq * TH_HANDS + c] + (sl >= 0 ? brv[sl * TH_HANDS + c] : T(0));
-                        mn = fmin(mn, x);
+#pragma unroll
+                for (int j = 0; j < TH_HPL; ++j) {
+                    const int c = lane + 32 * j, h = h0 + c;
+                    T mn = T(0);
+                    if (h < G.H && (all_valid || valid_g[(size_t)s_bs[m] * Hp + h])) {
+                        mn = big_value<T>();
+                        for (int a = 0; a < n; ++a) {
+                            const int sq = first + a, sl = s_slot[sq];
+                            const T x = sc * tile[sq * TH_HANDS + c] + (sl >= 0 ? brv[sl * TH_HANDS + c] : T(0));
+                            mn = fmin(mn, x);
+                        }
                     }
+                    if (rs >= 0) brroot[rs * TH_HANDS + c] = mn;
+                    else brv[s_slot[par] * TH_HANDS + c] += mn;
                 }
-                if (rs >= 0) brroot[rs * TH_HANDS + c] = mn;
-                else brv[s_slot[par] * TH_HANDS + c] += mn;
             }
             __syncthreads();
         }
         double v = 0.0;
-        if (wid == 0 && h0 + lane < G.H) {
-            v = scd * (double)tile[lane];
-            for (int r = 0; r < P.n_root; ++r) v += (double)brroot[r * TH_HANDS + lane];
+        if (wid == 0) {
+#pragma unroll
+            for (int j = 0; j < TH_HPL; ++j) {
+                const int c = lane + 32 * j;
+                if (h0 + c < G.H) {
+                    v += scd * (double)tile[c];
+                    for (int r = 0; r < P.n_root; ++r) v += (double)brroot[r * TH_HANDS + c];
+                }
+            }
         }
         v = warp_sum(v);
         game_value_reduce(v, A.br_partial, A.br_counter, A.br_value, g);
