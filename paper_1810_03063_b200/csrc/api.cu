@@ -376,8 +376,6 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         P.n_nodes = (int)L.first.size();
         P.n_levels = (int)L.lvl_off.size() - 1;
         P.n_rows_term = (int)L.rows_term.size();
-        P.max_level_width = 0;
-        for (int l = 0; l < P.n_levels; ++l) P.max_level_width = std::max(P.max_level_width, L.lvl_off[l + 1] - L.lvl_off[l]);
         int *a, *b, *c, *d, *e, *f, *lo, *ln, *ko, *kd, *rt, *co, *so, *sn, *rs, *ss;
         double* be;
         TRY(upload(G, &a, L.first));

@@ -88,7 +88,7 @@ struct BoardTable {
     std::vector<int16_t> order;  // [H_pad] position -> hand
     std::vector<int16_t> lo, hi; // [H_pad] per position: tie-group bounds [lo, hi)
     std::vector<uint32_t> lohi;  // [H_pad] lo | hi << 16
-    std::vector<uint16_t> cent;  // [CE_SLOTS(H_pad, n_cards)] card array
+    std::vector<uint16_t> cent;  // [n_ce] card array
     std::vector<uint32_t> pcard; // [H_pad][2]
     std::vector<uint8_t> valid;  // [H_pad] per hand
 };

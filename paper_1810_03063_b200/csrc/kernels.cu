@@ -122,8 +122,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Hands that do not share their tie group read their own P / Pc from registers.
 template <int NT, int KMAX, int EMAX, typename T>
 __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
-                                                     const int* __restrict__ mask, int want, int all_rows,
-                                                     DevPeers peers) {
+                                                     const int* __restrict__ mask, int want, DevPeers peers) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     T* sm = reinterpret_cast<T*>(sm_raw);
     constexpr int NW = NT / 32;
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
     __shared__ int segf[NW];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
-    const int s = all_rows ? (int)blockIdx.x : P.rows_term[blockIdx.x];
+    const int s = P.rows_term[blockIdx.x];
     const int Hp = G.H_pad, hs = G.hand_size, H = G.H, n_ce = G.n_ce;
     const bool fast = G.ident && G.all_valid;  // positions are hands and every hand is valid
     T* w = sm;               // [Hp]   by position
@@ -645,7 +644,7 @@ static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int p
     }
     dim3 grid(P.n_rows_term, G.n_games);
     grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>
-        <<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, 0, peers);
+        <<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, peers);
     return cudaGetLastError();
 }
 

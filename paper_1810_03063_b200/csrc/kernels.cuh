@@ -51,7 +51,7 @@ struct DevGame {
 };
 
 struct DevPlayer {
-    int n_pub, n_nodes, n_levels, max_level_width;
+    int n_pub, n_nodes, n_levels;
     int n_rows_term;         // public sequences that end at least one terminal
     const int* node_first;   // [n_nodes], top-down order
     const int* node_nact;
