@@ -452,6 +452,21 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     unsigned par[2] = {0u, 0u};
     mbar_wait(&bar[0], 0);
     __syncthreads();  // t_end
+    // the game's tables are the same for every terminal: this thread's card-array slots and
+    // its positions' card / tie-group indices live in registers for the whole chunk
+    unsigned cpos[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+        const int e = sbeg + j;
+        cpos[j] = e < send ? (cent[e] & CE_END) : CE_END;
+    }
+    uint2 pcr[K];
+    uint32_t lhr[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        pcr[j] = pcard[base + j];
+        lhr[j] = lohi[base + j];
+    }
     // w's chunk, its total and this thread's prefix survive a terminal: the next terminal
     // reuses them (and the card sums) when it reads the same opponent row (a fold / call pair
     // of one decision node); the first of such a pair then writes the full card-array prefixes
@@ -496,9 +511,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             T ssum = T(0);
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
-                const int e = sbeg + j;
-                const unsigned pos = e < send ? (cent[e] & CE_END) : CE_END;
-                y[j] = pos != CE_END ? w[pos] : T(0);
+                y[j] = cpos[j] != CE_END ? w[cpos[j]] : T(0);
                 ssum += y[j];
             }
             // exclusive scan of the part sums inside the segment's lane group
@@ -542,11 +555,11 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             const int i = base + j;
-            const uint2 pc = pcard[i];
+            const uint2 pc = pcr[j];
             T v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
             if (HS == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
             if (sd) {
-                const uint32_t lh = lohi[i];
+                const uint32_t lh = lhr[j];
                 const int lo = lh & 0xFFFFu, hi = lh >> 16;
                 if (lo == i && hi == i + 1) {
                     const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
