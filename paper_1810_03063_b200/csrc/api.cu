@@ -66,8 +66,6 @@ struct egt_game {
     int solver = SOLVER_NONE;
     int variant = 0;
     DevScalars sc{};
-    double* mu_base = nullptr;      // [2][G] for the mu search
-    int* search_mask = nullptr;     // [G]
     double* gapval = nullptr;       // [2][G]
     double* gapout = nullptr;       // [G]
     double* gapcur = nullptr;       // [G] eps_sad of the current EGT/as iterate (maintained)
@@ -454,8 +452,6 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(dalloc(G, &S.attempts, (size_t)Gn));
     TRY(dalloc(G, &S.backtracks, (size_t)Gn));
     TRY(dalloc(G, &S.fail, (size_t)Gn));
-    TRY(dalloc(G, &G->mu_base, 2 * (size_t)Gn));
-    TRY(dalloc(G, &G->search_mask, (size_t)Gn));
     TRY(dalloc(G, &G->gapval, 2 * (size_t)Gn));
     TRY(dalloc(G, &G->gapcur, (size_t)Gn));
     S.brval = G->gapval;
@@ -1115,28 +1111,34 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
     CK(cudaMemcpyAsync(G->sc.mu, mu.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
     G->grads = 0;
     if (!given && variant != EGT_THEORY) {
-        // DESIGN.md R14: smallest mu_theory * 2^-k (k = 30..0) whose initial point satisfies the EGC
-        CK(cudaMemcpyAsync(G->mu_base, mu.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
-        std::vector<int> found(Gn, 0);
-        std::vector<double> chosen(mu);
+        // DESIGN.md R14: the smallest mu = mu_theory * 2^-k, k in [0, 30], whose initial point
+        // satisfies the EGC, by bisection over k per game (the EGC holds at k = 0, the theory mu)
+        std::vector<int> lo(Gn, 0), hi(Gn, 30), mid(Gn, 0);
+        std::vector<double> chosen(mu), trial(mu);
         std::vector<double> vals(2 * (size_t)Gn);
-        for (int k = 30; k >= 0; --k) {
-            std::vector<int> need(Gn);
+        for (int round = 0; round < 6; ++round) {
             int any = 0;
-            for (int g = 0; g < Gn; ++g) any += (need[g] = !found[g]);
+            for (int g = 0; g < Gn; ++g) {
+                mid[g] = lo[g] < hi[g] ? (lo[g] + hi[g] + 1) / 2 : lo[g];
+                any += lo[g] < hi[g];
+                trial[g] = mu[g] * std::ldexp(1.0, -mid[g]);
+                trial[Gn + g] = mu[Gn + g] * std::ldexp(1.0, -mid[g]);
+            }
             if (!any) break;
-            CK(cudaMemcpyAsync(G->search_mask, need.data(), sizeof(int) * Gn, cudaMemcpyHostToDevice, G->st));
-            CK(launch_set_mu_scale(Gn, G->sc, G->mu_base, std::ldexp(1.0, -k), G->search_mask, G->st));
+            CK(cudaMemcpyAsync(G->sc.mu, trial.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
             if (egt_initial_point(G)) return EGT_E_CUDA;
             G->grads += 3;
             CK(cudaMemcpyAsync(vals.data(), G->sc.val, sizeof(double) * 2 * Gn, cudaMemcpyDeviceToHost, G->st));
             CK(cudaStreamSynchronize(G->st));
-            for (int g = 0; g < Gn; ++g)
-                if (need[g] && vals[g] + vals[Gn + g] >= 0.0) {
-                    found[g] = 1;
-                    chosen[g] = mu[g] * std::ldexp(1.0, -k);
-                    chosen[Gn + g] = mu[Gn + g] * std::ldexp(1.0, -k);
-                }
+            for (int g = 0; g < Gn; ++g) {
+                if (lo[g] >= hi[g]) continue;
+                if (vals[g] + vals[Gn + g] >= 0.0) lo[g] = mid[g];
+                else hi[g] = mid[g] - 1;
+            }
+        }
+        for (int g = 0; g < Gn; ++g) {
+            chosen[g] = mu[g] * std::ldexp(1.0, -lo[g]);
+            chosen[Gn + g] = mu[Gn + g] * std::ldexp(1.0, -lo[g]);
         }
         CK(cudaMemcpyAsync(G->sc.mu, chosen.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
     }

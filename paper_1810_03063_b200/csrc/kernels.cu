@@ -1317,12 +1317,6 @@ __global__ void tick_kernel(int n, int* t) {
     if (g < n) t[g] += 1;
 }
 
-__global__ void set_mu_scale_kernel(int n, DevScalars S, const double* base, double scale, const int* mask) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n || (mask && !mask[g])) return;
-    S.mu[g] = base[g] * scale;
-    S.mu[n + g] = base[n + g] * scale;
-}
 
 // eps_sad per game from the two best-response values:
 // val[g] = min_x <x, A y>, val[n+g] = min_y <y, -A^T x> = -max_y <x, A y>.
@@ -1346,11 +1340,6 @@ cudaError_t launch_egt_accept(int variant, int n, DevScalars S, cudaStream_t st)
 }
 cudaError_t launch_tick(int n, int* t, cudaStream_t st) {
     tick_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, t);
-    return cudaGetLastError();
-}
-cudaError_t launch_set_mu_scale(int n, DevScalars S, const double* base, double scale, const int* mask,
-                                cudaStream_t st) {
-    set_mu_scale_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, S, base, scale, mask);
     return cudaGetLastError();
 }
 

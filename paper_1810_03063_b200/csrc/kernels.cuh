@@ -144,6 +144,5 @@ cudaError_t launch_egt_prepare(int variant, int n_games, DevScalars S, cudaStrea
 cudaError_t launch_egt_accept(int variant, int n_games, DevScalars S, cudaStream_t st);
 cudaError_t launch_tick(int n_games, int* t, cudaStream_t st);
 cudaError_t launch_gap_combine(int n, const double* val, double* out, cudaStream_t st);
-cudaError_t launch_set_mu_scale(int n_games, DevScalars S, const double* mu_base, double scale, const int* mask, cudaStream_t st);
 
 }  // namespace egt
