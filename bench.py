@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--eps-mbb", type=float, nargs="+", default=[100.0, 10.0, 1.0],
                     help="saddle-gap targets in milli-big-blinds (time to each, median game)")
     ap.add_argument("--converge-max-steps", type=int, default=4000)
+    ap.add_argument("--no-f32", action="store_true", help="skip the extra fp32-mode measurement")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="f32: the optional fp32 mode (fp32 vectors and arithmetic, DESIGN.md row 9)")
     ap.add_argument("--fused", action="store_true",
@@ -455,6 +456,29 @@ def run_b200(args):
                                    "+ K x (egt_step + saddle_gap into pinned host memory); the K iterations' "
                                    "gradient evaluations over the whole time", "seconds": el}
         g2.close()
+
+    if rank == 0 and world == 1 and args.precision == "f64" and not args.no_f32 and not args.shard:
+        # the optional fp32 mode (DESIGN.md row 9) on the same workload, device-timed the same way
+        g32 = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2, precision="f32")
+        g32.set_stream(stream)
+        g32.egt_init(P.EGT_AS)
+        gap32 = torch.zeros(args.batch, dtype=torch.float64, device="cuda")
+        for _ in range(args.warmup):
+            g32.egt_step(1)
+            g32.saddle_gap_device(0, gap32)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            g32.egt_step(1)
+            g32.saddle_gap_device(0, gap32)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms32 = e0.elapsed_time(e1)
+        line["fp32_mode"] = {"value": throughput(args.batch, 1, args.steps, ms32), "unit": UNIT,
+                             "ms_per_step": ms32 / args.steps, "dtype": "f32",
+                             "what": "same workload and timing with precision EGT_F32 (parity 1e-5 vs the oracle)"}
+        g32.close()
 
     if args.converge_games > 0:
         n = args.converge_games
