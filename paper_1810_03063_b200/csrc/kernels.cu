@@ -1150,6 +1150,16 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
     const bool want_td = OUTS ? true : (A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR);
     if (!want_td) return;
     T* __restrict__ ob = A.out_b.ok() ? A.out_b.at<T>(g) : nullptr;
+    if ((OUTS & ~TO_FUSEBR) == TO_B && has_grad) {
+        // behavioural output only: after the bottom-up every action column of the tile holds its
+        // b (0 where the hand is blocked or past H), so no level-by-level descent is needed --
+        // one coalesced row-by-row copy, row 0 = 1 for live hands.
+        for (int i = tid; i < n_pub * TH_HANDS; i += TH_NT) {
+            const int r = i / TH_HANDS, c = i % TH_HANDS, h = h0 + c;
+            if (h < Hp) ob[(size_t)r * Hp + h] = r == 0 ? (h < G.H ? T(1) : T(0)) : tile[i];
+        }
+        return;
+    }
     T* __restrict__ oq = A.out_q.ok() ? A.out_q.at<T>(g) : nullptr;
     const T* __restrict__ ci = A.comb_in.ok() ? A.comb_in.at<T>(g) : nullptr;
     T* __restrict__ co = A.comb_out.ok() ? A.comb_out.at<T>(g) : nullptr;
