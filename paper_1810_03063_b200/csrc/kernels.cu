@@ -26,6 +26,17 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
     return v;
 }
 
+// inclusive scan that is exact for lanes < LIM (a power of two <= 32)
+template <int LIM, typename T>
+__device__ __forceinline__ T warp_incl_scan_lim(T v, int lane) {
+#pragma unroll
+    for (int o = 1; o < LIM; o <<= 1) {
+        const T u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
 // exp(x) for x <= 0 to ~1 ulp: x = (64 k + j) ln2 / 64 + r, |r| <= ln2 / 128,
 // exp(x) = 2^k' * tab[j] * (1 + r + ... + r^5/120) (truncation < 4e-17 relative).
 // tab[j] = 2^(j/64) lives in shared memory.  Arguments below -707 give exp(-707).
@@ -361,7 +372,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 // Card sums: every card's segment (seg_w slots) is scanned by one group of GL lanes (CH
 // slots each, GL * CH >= seg_w), so segments never straddle groups or warps.
-template <int NT, int K, int CH, int HS, typename T>
+template <int NT, int K, int CH, int HS, int GLL, typename T>
 __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
                                                             VecRef gout, const int* __restrict__ mask, int want,
                                                             int gl_log2, DevPeers peers) {
@@ -380,8 +391,8 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     T* popp = sm;                 // [NP] (0 beyond H)
     T* pself = popp + NP;         // [Hp]
     T* vb = pself + Hp;           // [2][NP] opponent rows (0 beyond Hp)
-    T* w = vb + 2 * NP;           // [NP]
-    T* ob = w + NP;               // [Hp] output row staging
+    T* w = vb + 2 * NP;           // [NP + 4] (w[NP] = 0 stands in for empty card slots)
+    T* ob = w + NP + 4;           // [Hp] output row staging
     T* Pf = ob + Hp;              // [NP + 2]
     T* Ex = Pf + NP + 4;          // [n_ce] (Pf padded to keep 16-byte alignment)
     uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [NP]
@@ -414,6 +425,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         pcard[i] = make_uint2(0u, 0u);
         lohi[i] = 0u;
     }
+    if (tid < 4) w[NP + tid] = T(0);
     for (int i = H + tid; i < Hp; i += NT) ob[i] = T(0);
     __syncthreads();
     for (int r = r0 + tid; r < r1; r += NT) {
@@ -441,31 +453,48 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     const T sd_sign = player == 0 ? T(1) : T(-1);
     const int base = tid * K;
     // card-array role: segment sgi, part of it [sbeg, sbeg + CH)
-    const int GL = 1 << gl_log2;
-    const int sgi = tid >> gl_log2, part = tid & (GL - 1);
+    const int gll = GLL >= 0 ? GLL : gl_log2;
+    const int GL = 1 << gll;
+    const int sgi = tid >> gll, part = tid & (GL - 1);
     const bool has_seg = sgi < G.n_cards;
     const int sbeg = sgi * W + part * CH;
     const int send = has_seg ? min(sgi * W + W, sbeg + CH) : sbeg;
     T racc[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) racc[j] = T(0);
-    unsigned par[2] = {0u, 0u};
+    unsigned par = 0u;  // mbarrier phase bit of each opponent-row buffer
     mbar_wait(&bar[0], 0);
     __syncthreads();  // t_end
     // the game's tables are the same for every terminal: this thread's card-array slots and
     // its positions' card / tie-group indices live in registers for the whole chunk
-    unsigned cpos[CH];
+    // (cpos: byte offsets into w, empty slots read the zero at w[NP]; the card-array slots
+    // this thread writes: all of them (wr_full) or only its segment's end slot (wr_end))
+    static_assert(NP * sizeof(T) < 65536, "card slot offsets are packed in 16 bits");
+    unsigned cpos[(CH + 1) / 2];  // two 16-bit offsets per register
+    unsigned wr_full = 0u, wr_end = 0u;
+    const int end_slot = sgi * W + W - 1;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
         const int e = sbeg + j;
-        cpos[j] = e < send ? (cent[e] & CE_END) : CE_END;
+        const unsigned c = e < send ? (cent[e] & CE_END) : CE_END;
+        const unsigned off = (c == CE_END ? (unsigned)NP : c) * (unsigned)sizeof(T);
+        if (j & 1) cpos[j / 2] |= off << 16;
+        else cpos[j / 2] = off;
+        if (has_seg && e < send) {
+            wr_full |= 1u << j;
+            if (e == end_slot) wr_end |= 1u << j;
+        }
     }
+    T* const exs = Ex + sbeg;
+    const unsigned char* const wbytes = reinterpret_cast<const unsigned char*>(w);
     uint2 pcr[K];
     uint32_t lhr[K];
+    unsigned adj = 0u;  // positions whose tie group is the position itself (lo == i, hi == i + 1)
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         pcr[j] = pcard[base + j];
         lhr[j] = lohi[base + j];
+        if ((int)(lhr[j] & 0xFFFFu) == base + j && (int)(lhr[j] >> 16) == base + j + 1) adj |= 1u << j;
     }
     // w's chunk, its total and this thread's prefix survive a terminal: the next terminal
     // reuses them (and the card sums) when it reads the same opponent row (a fold / call pair
@@ -489,8 +518,8 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             }
         }
         if (so && !reuse) {
-            mbar_wait(&bar[1 + q], par[q]);
-            par[q] ^= 1u;
+            mbar_wait(&bar[1 + q], (par >> q) & 1u);
+            par ^= 1u << q;
         }
         if (!reuse) {  // warp-uniform (the whole CTA takes the same branch)
         const T* vrow = vb + q * NP;
@@ -511,30 +540,35 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             T ssum = T(0);
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
-                y[j] = cpos[j] != CE_END ? w[cpos[j]] : T(0);
+                y[j] = *reinterpret_cast<const T*>(wbytes + ((j & 1) ? (cpos[j / 2] >> 16) : (cpos[j / 2] & 0xFFFFu)));
                 ssum += y[j];
             }
             // exclusive scan of the part sums inside the segment's lane group
             T inc = ssum;
-            for (int o = 1; o < GL; o <<= 1) {
-                const T u = __shfl_up_sync(0xffffffffu, inc, o, GL);
-                if (part >= o) inc += u;
-            }
-            if (has_seg) {
-                // the same accumulation order in both cases, so a segment total never depends
-                // on whether the terminal needs the full prefixes (folds: end slot only)
-                const int end_slot = sgi * W + W - 1;
-                T run2 = inc - ssum;
+            if (GLL >= 0) {
 #pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int e = sbeg + j;
-                    if (e < send && (full || e == end_slot)) Ex[e] = run2;
-                    run2 += y[j];
+                for (int o = 1; o < (1 << (GLL >= 0 ? GLL : 0)); o <<= 1) {
+                    const T u = __shfl_up_sync(0xffffffffu, inc, o, GL);
+                    if (part >= o) inc += u;
                 }
+            } else {
+                for (int o = 1; o < GL; o <<= 1) {
+                    const T u = __shfl_up_sync(0xffffffffu, inc, o, GL);
+                    if (part >= o) inc += u;
+                }
+            }
+            // the same accumulation order in both cases, so a segment total never depends on
+            // whether the terminal needs the full prefixes (folds: end slot only)
+            const unsigned wm = full ? wr_full : wr_end;
+            T run2 = inc - ssum;
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                if (wm & (1u << j)) exs[j] = run2;
+                run2 += y[j];
             }
         }
         // block prefix of the warp totals: one load per lane, a warp scan, two shuffles
-        const T wsc = warp_incl_scan(lane < NW ? wtot[lane] : T(0), lane);
+        const T wsc = warp_incl_scan_lim<(NW <= 16 ? 16 : 32)>(lane < NW ? wtot[lane] : T(0), lane);
         const T wpre_incl = __shfl_sync(0xffffffffu, wsc, (wid + 31) & 31);
         const T wpre = wid ? wpre_incl : T(0);
         total = __shfl_sync(0xffffffffu, wsc, NW - 1);
@@ -554,14 +588,13 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         T pre = pbase;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            const int i = base + j;
             const uint2 pc = pcr[j];
             T v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
             if (HS == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
             if (sd) {
                 const uint32_t lh = lhr[j];
                 const int lo = lh & 0xFFFFu, hi = lh >> 16;
-                if (lo == i && hi == i + 1) {
+                if (adj & (1u << j)) {
                     const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
                     v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
                     if (HS == 2) {
@@ -625,7 +658,7 @@ static constexpr int STG_NT = 416, STG_K = 3, STG_CH = STG_CH_DEF;  // positions
 
 static size_t grad_staged_smem_bytes(const DevGame& G) {
     const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
-    return (size_t)G.esz * (2 * Hp + 5 * NP + 4 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
+    return (size_t)G.esz * (2 * Hp + 5 * NP + 8 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
            sizeof(uint16_t) * G.n_ce + 16;
 }
 
@@ -647,12 +680,14 @@ static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int p
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
         const int gl = staged_gl_log2(G);
-        if (G.hand_size == 2)
-            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, T>
-                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl, peers);
+        const size_t sm = grad_staged_smem_bytes(G);
+        // the river's card segments (47 slots = 8 lanes x 6) get a fully unrolled lane-group scan
+        if (G.hand_size == 2 && gl == 3)
+            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, 3, T><<<grid, STG_NT, sm, st>>>(G, P, player, vin, gout, mask, want, gl, peers);
+        else if (G.hand_size == 2)
+            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, -1, T><<<grid, STG_NT, sm, st>>>(G, P, player, vin, gout, mask, want, gl, peers);
         else
-            grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, T>
-                <<<grid, STG_NT, grad_staged_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, gl, peers);
+            grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, -1, T><<<grid, STG_NT, sm, st>>>(G, P, player, vin, gout, mask, want, gl, peers);
         return cudaGetLastError();
     }
     dim3 grid(P.n_rows_term, G.n_games);
@@ -1257,10 +1292,13 @@ static cudaError_t prepare_t() {
     cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, T>,
+        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, 3, T>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, T>,
+        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, -1, T>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, -1, T>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     const void* tk[] = {(const void*)tree_kernel<T, TM_SBR, 0>,     (const void*)tree_kernel<T, TM_PROX, 0>,
                         (const void*)tree_kernel<T, TM_BR, 0>,      (const void*)tree_kernel<T, TM_CFR, 0>,
