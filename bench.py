@@ -437,9 +437,12 @@ def run_b200(args):
         t0 = time.perf_counter()
         g2 = P.Game(P.RIVER, n_games=args.batch, river=spec, boards=boards, prior1=p1, prior2=p2,
                     precision=args.precision)
+        t_load = time.perf_counter()
         if args.shard:
             g2.shard(rank, world)
         g2.egt_init(P.EGT_AS)
+        torch.cuda.synchronize()
+        t_init = time.perf_counter()
         for _ in range(args.steps):
             g2.egt_step(1)
             g2.saddle_gap(0, out=pinned)
@@ -454,7 +457,9 @@ def run_b200(args):
                            "what": "wall clock of a whole job through the public API: egt_load_game from host "
                                    "arrays (tables built on the host, copied in) + egt_init (practical-mu search) "
                                    "+ K x (egt_step + saddle_gap into pinned host memory); the K iterations' "
-                                   "gradient evaluations over the whole time", "seconds": el}
+                                   "gradient evaluations over the whole time", "seconds": el,
+                           "breakdown_s": {"load": t_load - t0, "init": t_init - t_load,
+                                           "steps": el - (t_init - t0) if world == 1 else None}}
         g2.close()
 
     if rank == 0 and world == 1 and args.precision == "f64" and not args.no_f32 and not args.shard:

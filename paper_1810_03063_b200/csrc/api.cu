@@ -1101,8 +1101,8 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
     std::vector<double> mth(Gn);
     if (!given) {
         // mu_x = mu_y = ||A|| / sqrt(phi_X phi_Y), phi = 1/M
-        for (int g = 0; g < Gn; ++g)
-            mth[g] = compute_max_abs_A(H, g) * std::sqrt(H.M[0][g] * H.M[1][g]);
+        const std::vector<double> amax = compute_max_abs_A_all(H);
+        for (int g = 0; g < Gn; ++g) mth[g] = amax[g] * std::sqrt(H.M[0][g] * H.M[1][g]);
     }
     for (int g = 0; g < Gn; ++g) {
         mu[g] = given ? mu_x : mth[g];

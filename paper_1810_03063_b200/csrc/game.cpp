@@ -547,6 +547,14 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
         const std::vector<int>& bd = game_boards[g];
         std::vector<std::pair<int64_t, int>> hv;  // (strength, combo)
         std::vector<std::pair<int, int>> cards;
+        // A hand's strength depends only on its two ranks and on whether each hole card has the
+        // board's flush suit (the one suit with >= 3 board cards; with none, no flush exists):
+        // one evaluation per such key, shared by every hand that has it.
+        int fs = -1, scnt[4] = {0, 0, 0, 0};
+        for (int c : bd) scnt[c % G.n_suits]++;
+        for (int su = 0; su < G.n_suits; ++su)
+            if (scnt[su] >= 3) fs = su;
+        std::vector<int64_t> memo(13 * 13 * 4, -1);
         for (int c1 = 0; c1 < G.n_cards; ++c1)
             for (int c2 = c1 + 1; c2 < G.n_cards; ++c2) {
                 if (std::find(bd.begin(), bd.end(), c1) != bd.end() ||
@@ -554,8 +562,12 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
                 int ranks[7], suits[7], n = 0;
                 ranks[n] = 13 - G.n_ranks + c1 / G.n_suits; suits[n++] = c1 % G.n_suits;
                 ranks[n] = 13 - G.n_ranks + c2 / G.n_suits; suits[n++] = c2 % G.n_suits;
-                for (int c : bd) { ranks[n] = 13 - G.n_ranks + c / G.n_suits; suits[n++] = c % G.n_suits; }
-                hv.push_back({hand_strength(ranks, suits, n), combo_index(c1, c2, G.n_cards)});
+                const int key = ((ranks[0] * 13 + ranks[1]) * 2 + (suits[0] == fs)) * 2 + (suits[1] == fs);
+                if (memo[key] < 0) {
+                    for (int c : bd) { ranks[n] = 13 - G.n_ranks + c / G.n_suits; suits[n++] = c % G.n_suits; }
+                    memo[key] = hand_strength(ranks, suits, n);
+                }
+                hv.push_back({memo[key], combo_index(c1, c2, G.n_cards)});
             }
         if ((int)hv.size() != H) return "internal: hand count";
         std::sort(hv.begin(), hv.end());
@@ -654,6 +666,15 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& G) {
 // most 2 * 46 others, so the scan is short); terminals whose player-1 (-2) sequence is
 // empty aggregate their block's columns (rows) into row (column) 0, computed with the
 // same card-removal sums as the gradient (O(H) per terminal).
+std::vector<double> compute_max_abs_A_all(const HostGame& G) {
+    std::vector<double> out(G.n_games, 0.0);
+    parallel_games(G.n_games, [&](int g) -> std::string {
+        out[g] = compute_max_abs_A(G, g);
+        return "";
+    });
+    return out;
+}
+
 double compute_max_abs_A(const HostGame& G, int g) {
     const int H = G.H, Hp = G.H_pad, nbs = G.tree.n_board_states, hs = G.hand_size;
     const double* pr[2] = {&G.prior[0][(size_t)g * Hp], &G.prior[1][(size_t)g * Hp]};

@@ -126,6 +126,8 @@ std::string build_host_game(const egt_game_spec& spec, HostGame& out);
 
 // ||A|| = max |A_ij| of game g (R7), O(H^2) per board state.
 double compute_max_abs_A(const HostGame& G, int g);
+// compute_max_abs_A of every game, games spread over the host's cores
+std::vector<double> compute_max_abs_A_all(const HostGame& G);
 
 // 5..7-card poker hand strength (larger is better, equal = tie).
 int64_t hand_strength(const int* ranks, const int* suits, int n);
