@@ -221,16 +221,20 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kind, workload_name):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+def ncu_entry(kind, workload_name):
+    """The committed ncu capture's record for the dominant kernel (profiles/ncu_traffic.json)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        e = d.get(workload_name, {}).get(kind)
-        return None if e is None else float(e["dram_bytes_per_game_launch"])
+            return json.load(f).get(workload_name, {}).get(kind)
     except Exception:
         return None
+
+
+def ncu_traffic(kind, workload_name):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+    e = ncu_entry(kind, workload_name)
+    return None if e is None else float(e["dram_bytes_per_game_launch"])
 
 
 # ----------------------------------------------------------------------------- CPU oracle leg
@@ -401,6 +405,9 @@ def run_b200(args):
             "frac": achieved / peak, "traffic": None if tr is None else tr * active / nl,
             "peak_source": peak_src, "algorithmic_bytes_per_launch": byts / nl,
             "avg_launch_ms": ms_k / nl, "share_of_step": ms_k / tot_ms}
+    lim = (ncu_entry("grad" if dom.startswith("grad") else "tree", args.workload) or {}).get("limiter")
+    if lim:
+        roof["limiter"] = lim  # what ncu shows the kernel actually waits on (not DRAM)
     other = [n for n in groups if n != dom][0]
     ko = groups[other]
     ms_o = sum(kt[k][0] for k in ko)
