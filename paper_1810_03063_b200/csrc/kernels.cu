@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
 // the chunk's terminals.  The game's tables and priors are staged in shared memory once
 // per CTA with bulk async copies (TMA engine, cp.async.bulk + mbarrier); each terminal's
 // opponent row is double-buffered -- the copy of terminal t+1's row overlaps terminal t.
-// Every global read is a bulk copy; each output row leaves in one bulk store.
+// Every global read is a bulk copy; a finished output row goes from registers straight to
+// global memory (each warp writes 96 consecutive positions), with no barrier at a row end.
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -360,14 +361,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Card sums: every card's segment (seg_w slots) is scanned by one group of GL lanes (CH
@@ -392,8 +385,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     T* pself = popp + NP;         // [Hp]
     T* vb = pself + Hp;           // [2][NP] opponent rows (0 beyond Hp)
     T* w = vb + 2 * NP;           // [NP + 4] (w[NP] = 0 stands in for empty card slots)
-    T* ob = w + NP + 4;           // [Hp] output row staging
-    T* Pf = ob + Hp;              // [NP + 2]
+    T* Pf = w + NP + 4;           // [NP + 4]
     T* Ex = Pf + NP + 4;          // [n_ce] (Pf padded to keep 16-byte alignment)
     uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [NP]
     uint32_t* lohi = reinterpret_cast<uint32_t*>(pcard + NP);        // [NP]
@@ -401,7 +393,6 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     const int r0 = P.chunk_off[blockIdx.x], r1 = P.chunk_off[blockIdx.x + 1];
     const int T0 = P.term_off[P.rows_term[r0]], T1 = P.term_off[P.rows_term[r1 - 1] + 1];
     const T* __restrict__ vo = vin.at<T>(g);
-    T* __restrict__ outg = gout.at<T>(g);
     const int* __restrict__ tidx = P.term_idx;
     const int nT = T1 - T0;
     for (int i = tid; i < nT; i += NT) {
@@ -426,7 +417,6 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         lohi[i] = 0u;
     }
     if (tid < 4) w[NP + tid] = T(0);
-    for (int i = H + tid; i < Hp; i += NT) ob[i] = T(0);
     __syncthreads();
     for (int r = r0 + tid; r < r1; r += NT) {
         const int srow = P.rows_term[r];
@@ -468,10 +458,11 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
     // the game's tables are the same for every terminal: this thread's card-array slots and
     // its positions' card / tie-group indices live in registers for the whole chunk
     // (cpos: byte offsets into w, empty slots read the zero at w[NP]; the card-array slots
-    // this thread writes: all of them (wr_full) or only its segment's end slot (wr_end))
+    // this thread writes: all of them (bits 0-7 of masks) or only its segment's end slot (bits 8-15);
+    // bits 16+ mark positions alone in their tie group)
     static_assert(NP * sizeof(T) < 65536, "card slot offsets are packed in 16 bits");
     unsigned cpos[(CH + 1) / 2];  // two 16-bit offsets per register
-    unsigned wr_full = 0u, wr_end = 0u;
+    unsigned masks = 0u;
     const int end_slot = sgi * W + W - 1;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
@@ -481,20 +472,19 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         if (j & 1) cpos[j / 2] |= off << 16;
         else cpos[j / 2] = off;
         if (has_seg && e < send) {
-            wr_full |= 1u << j;
-            if (e == end_slot) wr_end |= 1u << j;
+            masks |= 1u << j;
+            if (e == end_slot) masks |= 1u << (8 + j);
         }
     }
     T* const exs = Ex + sbeg;
     const unsigned char* const wbytes = reinterpret_cast<const unsigned char*>(w);
     uint2 pcr[K];
     uint32_t lhr[K];
-    unsigned adj = 0u;  // positions whose tie group is the position itself (lo == i, hi == i + 1)
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         pcr[j] = pcard[base + j];
         lhr[j] = lohi[base + j];
-        if ((int)(lhr[j] & 0xFFFFu) == base + j && (int)(lhr[j] >> 16) == base + j + 1) adj |= 1u << j;
+        if ((int)(lhr[j] & 0xFFFFu) == base + j && (int)(lhr[j] >> 16) == base + j + 1) masks |= 1u << (16 + j);
     }
     // w's chunk, its total and this thread's prefix survive a terminal: the next terminal
     // reuses them (and the card sums) when it reads the same opponent row (a fold / call pair
@@ -559,7 +549,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             }
             // the same accumulation order in both cases, so a segment total never depends on
             // whether the terminal needs the full prefixes (folds: end slot only)
-            const unsigned wm = full ? wr_full : wr_end;
+            const unsigned wm = full ? masks : masks >> 8;
             T run2 = inc - ssum;
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
@@ -594,7 +584,7 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             if (sd) {
                 const uint32_t lh = lhr[j];
                 const int lo = lh & 0xFFFFu, hi = lh >> 16;
-                if (adj & (1u << j)) {
+                if (masks & (1u << (16 + j))) {
                     const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
                     v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
                     if (HS == 2) {
@@ -612,37 +602,38 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             racc[j] += scale * v;
             pre += x[j];
         }
-        // ---- row end: stage prior_self * acc, one bulk store per row
+        // ---- row end: prior_self * acc straight from registers to the output row(s): each warp's
+        // 96 consecutive positions form one contiguous 768-byte span (coalesced in L2), and no
+        // staging buffer means no barrier at a row end
         const int srow = t_end[li];
         if (srow >= 0) {
-            if (tid == 0) bulk_wait_read0();  // the previous row's store has left ob
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                const int i = base + j;
-                if (i < H) ob[i] = pself[i] * racc[j];
-                racc[j] = T(0);
-            }
             if (peers.n == 0) {
-                fence_proxy_async();
-                __syncthreads();
-                if (tid == 0) bulk_s2g(outg + (size_t)srow * Hp, ob, Hp * sizeof(T));
+                T* __restrict__ dst = gout.at<T>(g) + (size_t)srow * Hp;
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int i = base + j;
+                    if (i < Hp) dst[i] = i < H ? pself[i] * racc[j] : T(0);
+                }
             } else {
-                // fused all-gather: the finished row goes from shared memory straight into every
-                // shard's gradient buffer (peer memory over NVLink), overlapping the next terminals
-                __syncthreads();
+                // fused all-gather: the finished row goes straight into every shard's gradient
+                // buffer (peer memory over NVLink), overlapping the next terminals
                 const long long off = (long long)g * gout.game_stride + (long long)srow * Hp;
 #pragma unroll
                 for (int d = 0; d < EGT_MAX_PEERS; ++d) {  // constant indices: no local copy of peers
                     if (d < peers.n) {
                         T* __restrict__ dst = reinterpret_cast<T*>(peers.base[d]) + off;
-                        for (int i = tid; i < Hp; i += NT) dst[i] = ob[i];
+#pragma unroll
+                        for (int j = 0; j < K; ++j) {
+                            const int i = base + j;
+                            if (i < Hp) dst[i] = i < H ? pself[i] * racc[j] : T(0);
+                        }
                     }
                 }
             }
+#pragma unroll
+            for (int j = 0; j < K; ++j) racc[j] = T(0);
         }
     }
-    if (tid == 0) bulk_wait0();
 }
 
 static constexpr int GRAD_NT = 512, GRAD_KMAX = 3, GRAD_EMAX = 6;  // H <= 1536, card array <= 3072
@@ -658,7 +649,7 @@ static constexpr int STG_NT = 416, STG_K = 3, STG_CH = STG_CH_DEF;  // positions
 
 static size_t grad_staged_smem_bytes(const DevGame& G) {
     const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
-    return (size_t)G.esz * (2 * Hp + 5 * NP + 8 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
+    return (size_t)G.esz * (Hp + 5 * NP + 8 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
            sizeof(uint16_t) * G.n_ce + 16;
 }
 
