@@ -4,12 +4,31 @@
 #include <nccl.h>  // types only; the library is opened at run time (egt_shard)
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
+
+// EGT_TRACE=1 in the environment: host-side phase timings of loading and initialisation on
+// stderr (wall clock; device work is synchronised where a phase ends in a host wait)
+namespace {
+struct Trace {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    const char* what;
+    explicit Trace(const char* w) : on(std::getenv("EGT_TRACE") != nullptr), t(std::chrono::steady_clock::now()), what(w) {}
+    void mark(const char* phase) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[egt] %s: %s %.2f ms\n", what, phase, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+}  // namespace
 
 #include "../../include/egt_b200.h"
 #include "game.h"
@@ -49,6 +68,8 @@ struct egt_game {
     double* barrier_word = nullptr;
     int esz = 8;                    // bytes per vector element (8: fp64, 4: fp32 mode)
     std::vector<void*> allocs;
+    std::vector<void*> pool_allocs;  // stream-ordered allocations from the library pool (lib_pool)
+    bool gr_ipc[2] = {false, false};  // GR[p] is a plain cudaMalloc buffer (exportable over IPC)
     cudaStream_t st = nullptr;      // internal stream (graphs are captured here)
     cudaStream_t user = nullptr;    // caller's stream (nullptr = legacy default)
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -96,24 +117,72 @@ struct egt_game {
 
 const char* egt_last_error(void) { return g_err.c_str(); }
 
+// The library's device memory pool (one per device, created on first use): the large
+// per-game vectors are stream-ordered allocations from it, and memory a freed game returns
+// stays reserved for the next game (release threshold: unlimited), so loading a batch after
+// another one does not pay the page mapping of several GB again.
+static cudaMemPool_t lib_pool(cudaError_t* err) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    *err = cudaGetDevice(&dev);
+    if (*err != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        *err = cudaMemPoolCreate(&pool, &props);
+        if (*err != cudaSuccess) return nullptr;
+        uint64_t keep = UINT64_MAX;
+        *err = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        if (*err != cudaSuccess) return nullptr;
+        pools[dev] = pool;
+    }
+    return pools[dev];
+}
+
+// n elements of T: from the library pool on the game's stream (plain cudaMalloc before the
+// stream exists)
 template <class T>
 static int dalloc(egt_game* G, T** p, size_t n) {
     void* q = nullptr;
     if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc(&q, n * sizeof(T));
-    if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    G->allocs.push_back(q);
+    if (!G->st) {
+        cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+        if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        G->allocs.push_back(q);
+    } else {
+        cudaError_t e = cudaSuccess;
+        cudaMemPool_t pool = lib_pool(&e);
+        if (pool) e = cudaMallocFromPoolAsync(&q, n * sizeof(T), pool, G->st);
+        if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMallocFromPoolAsync: ") + cudaGetErrorString(e));
+        G->pool_allocs.push_back(q);
+    }
     *p = (T*)q;
     return 0;
 }
 
-// a per-game vector buffer of n elements in the game's precision (base address only)
-static int dalloc_vec(egt_game* G, double** p, size_t n) {
+// a per-game vector buffer of n elements in the game's precision (base address only):
+// from the library pool on the game's stream, or a plain cudaMalloc when the buffer is
+// shared with other processes through CUDA IPC (pool memory has no IPC handle)
+static int dalloc_vec(egt_game* G, double** p, size_t n, bool ipc = false) {
     void* q = nullptr;
     if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc(&q, n * (size_t)G->esz);
-    if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    G->allocs.push_back(q);
+    const size_t bytes = n * (size_t)G->esz;
+    if (ipc || !G->st) {
+        cudaError_t e = cudaMalloc(&q, bytes);
+        if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        G->allocs.push_back(q);
+    } else {
+        cudaError_t e = cudaSuccess;
+        cudaMemPool_t pool = lib_pool(&e);
+        if (pool) e = cudaMallocFromPoolAsync(&q, bytes, pool, G->st);
+        if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("cudaMallocFromPoolAsync: ") + cudaGetErrorString(e));
+        G->pool_allocs.push_back(q);
+    }
     *p = (double*)q;
     return 0;
 }
@@ -122,7 +191,8 @@ template <class T>
 static int upload(egt_game* G, T** p, const std::vector<T>& v) {
     int r = dalloc(G, p, v.size());
     if (r) return r;
-    if (!v.empty()) CK(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    // stream-ordered after the pool allocation; a pageable source is staged before the call returns
+    if (!v.empty()) CK(cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, G->st));
     G->h2d_bytes += (long long)(v.size() * sizeof(T));
     return 0;
 }
@@ -261,9 +331,11 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EGT_E_CUDA, "no CUDA device");
     if (spec->precision != EGT_F64 && spec->precision != EGT_F32) return fail(EGT_E_ARG, "bad precision");
+    Trace tr("load");
     egt_game* G = new egt_game();
     G->esz = spec->precision == EGT_F32 ? 4 : 8;
     std::string err = build_host_game(*spec, G->host);
+    tr.mark("host build (trees, strengths, tables)");
     if (!err.empty()) {
         delete G;
         return fail(EGT_E_ARG, err);
@@ -292,6 +364,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
             return fail(EGT_E_CUDA, std::string("stream/event: ") + cudaGetErrorString(e));
         }
     }
+    tr.mark("streams, events, kernel attributes");
     // tables
     std::vector<int> nvalid;
     std::vector<int16_t> order;
@@ -431,10 +504,10 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(dalloc(G, &G->counter_br, (size_t)Gn));
     TRY(dalloc(G, &G->partial2_br, (size_t)Gn * max_tiles));
     TRY(dalloc(G, &G->counter2_br, (size_t)Gn));
-    if (cudaMemset(G->counter, 0, sizeof(unsigned) * Gn) != cudaSuccess ||
-        cudaMemset(G->counter2, 0, sizeof(unsigned) * Gn) != cudaSuccess ||
-        cudaMemset(G->counter_br, 0, sizeof(unsigned) * Gn) != cudaSuccess ||
-        cudaMemset(G->counter2_br, 0, sizeof(unsigned) * Gn) != cudaSuccess) {
+    if (cudaMemsetAsync(G->counter, 0, sizeof(unsigned) * Gn, G->st) != cudaSuccess ||
+        cudaMemsetAsync(G->counter2, 0, sizeof(unsigned) * Gn, G->st) != cudaSuccess ||
+        cudaMemsetAsync(G->counter_br, 0, sizeof(unsigned) * Gn, G->st) != cudaSuccess ||
+        cudaMemsetAsync(G->counter2_br, 0, sizeof(unsigned) * Gn, G->st) != cudaSuccess) {
         egt_free_game(G);
         return fail(EGT_E_CUDA, "memset");
     }
@@ -462,7 +535,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         TRY(dalloc_vec(G, &G->GR[p], n));
         TRY(dalloc_vec(G, &G->HAT[p], n));
         // rows that end no terminal are never written by the solver's gradient launches
-        if (cudaMemset(G->GR[p], 0, n * G->esz) != cudaSuccess) {
+        if (cudaMemsetAsync(G->GR[p], 0, n * G->esz, G->st) != cudaSuccess) {
             egt_free_game(G);
             return fail(EGT_E_CUDA, "memset");
         }
@@ -472,6 +545,7 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
         return fail(EGT_E_CUDA, "sync after load");
     }
 #undef TRY
+    tr.mark("device tables (allocate + copy)");
     *out = G;
     return 0;
 }
@@ -488,6 +562,10 @@ extern "C" void egt_free_game(egt_game* G) {
     for (void* q : G->ipc_opened) cudaIpcCloseMemHandle(q);
     if (G->comm) nccl_destroy(G->comm);
     for (void* p : G->allocs) cudaFree(p);
+    if (G->st) {
+        for (void* p : G->pool_allocs) cudaFreeAsync(p, G->st);
+        cudaStreamSynchronize(G->st);
+    }
     if (G->ev_in) cudaEventDestroy(G->ev_in);
     if (G->ev_out) cudaEventDestroy(G->ev_out);
     if (G->ev_fork) cudaEventDestroy(G->ev_fork);
@@ -615,6 +693,26 @@ extern "C" int egt_gradient_rows_to(egt_game* G, int32_t player, int32_t rank, i
 extern "C" int egt_ipc_handles(egt_game* G, uint8_t* out) {
     if (!G || !out) return fail(EGT_E_ARG, "bad argument");
     for (int p = 0; p < 2; ++p) {
+        if (!G->gr_ipc[p]) {
+            // pool memory has no IPC handle: move this gradient buffer to a plain allocation
+            // (its contents are scratch except the rows no terminal ends, which stay 0)
+            const size_t n = (size_t)G->host.n_games * G->V[p];
+            double* q = nullptr;
+            if (dalloc_vec(G, &q, n, true)) return EGT_E_CUDA;
+            CK(cudaMemset(q, 0, n * G->esz));
+            CK(cudaStreamSynchronize(G->st));
+            auto it = std::find(G->pool_allocs.begin(), G->pool_allocs.end(), (void*)G->GR[p]);
+            if (it != G->pool_allocs.end()) {
+                CK(cudaFreeAsync(*it, G->st));
+                G->pool_allocs.erase(it);
+            }
+            G->GR[p] = q;
+            G->gr_ipc[p] = true;
+            if (G->graph) {  // a captured iteration would still name the old buffer
+                cudaGraphExecDestroy(G->graph);
+                G->graph = nullptr;
+            }
+        }
         cudaIpcMemHandle_t h;
         CK(cudaIpcGetMemHandle(&h, G->GR[p]));
         static_assert(sizeof(h) == EGT_IPC_HANDLE_BYTES, "IPC handle size");
@@ -629,7 +727,8 @@ extern "C" int egt_shard_peers(egt_game* G, const uint8_t* handles) {
     if (G->world > EGT_MAX_PEERS) return fail(EGT_E_ARG, "too many ranks for the fused all-gather");
     if (G->solver != SOLVER_NONE) return fail(EGT_E_STATE, "egt_shard_peers must precede egt_init / cfr_init");
     if (!G->barrier_word && dalloc(G, &G->barrier_word, 1)) return EGT_E_CUDA;
-    CK(cudaMemset(G->barrier_word, 0, sizeof(double)));
+    CK(cudaMemsetAsync(G->barrier_word, 0, sizeof(double), G->st));
+    CK(cudaStreamSynchronize(G->st));
     for (int p = 0; p < 2; ++p) {
         G->peers[p].n = G->world;
         for (int r = 0; r < G->world; ++r) {
@@ -888,19 +987,31 @@ static cudaError_t scalar_k(egt_game* G, F&& launch) {
 
 // EGT initial point (Alg. 1/3 lines 1-2, R4) at the current per-game mu;
 // leaves val[0] = phi_{mu_x}(y0), val[1] = -f_{mu_y}(x0) and the caches C[.][cur].
-static int egt_initial_point(egt_game* G) {
-    const int Gn = G->host.n_games;
-    DevScalars& S = G->sc;
-    // x_omega: the uniform behavioural strategy in sequence form
+// A^T x_omega, x_omega the uniform behavioural strategy in sequence form (into HAT[0]);
+// independent of mu, so the mu search evaluates it once (into `out`)
+static int egt_omega_gradient(egt_game* G, double* out) {
     TreeArgs U = base_args();
     U.mode = TM_UNIFORM;
     U.out_q = vec(G->HAT[0], G->V[0]);
     CK(tree(G, 0, U));
+    CK(grad(G, 1, vec(G->HAT[0], G->V[0]), vec(out, G->V[1])));
+    return 0;
+}
+
+// Alg. 1 / 3 initialisation at the current mu: y0 = y_mu(x_omega), x0 = x_mu(y0) (cache C[0]),
+// y_mu(x0) (cache C[1]) and the values the excessive-gap check needs.  g_omega: A^T x_omega
+// already evaluated (the mu search), or nullptr to evaluate it here.
+static int egt_initial_point(egt_game* G, double* g_omega) {
+    const int Gn = G->host.n_games;
+    DevScalars& S = G->sc;
+    if (!g_omega) {
+        if (egt_omega_gradient(G, G->GR[1])) return EGT_E_CUDA;
+        g_omega = G->GR[1];
+    }
     // y0 = y_{mu_y}(x_omega)
-    CK(grad(G, 1, vec(G->HAT[0], G->V[0]), vec(G->GR[1], G->V[1])));
     TreeArgs A = base_args();
     A.mode = TM_SBR;
-    A.g = vec(G->GR[1], G->V[1]);
+    A.g = vec(g_omega, G->V[1]);
     A.gsign = GSIGN[1];
     A.mu = S.mu + Gn;
     A.out_q = slot2(G, G->S[1], 1, 0);
@@ -1087,7 +1198,9 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
     if (!G || variant < EGT_THEORY || variant > EGT_AS) return fail(EGT_E_ARG, "bad argument");
     const HostGame& H = G->host;
     const int Gn = H.n_games;
+    Trace tr("egt_init");
     if (ensure_egt_buffers(G)) return EGT_E_CUDA;
+    tr.mark("solver buffers");
     if (begin(G)) return EGT_E_CUDA;
     if (zero_scalars(G)) return EGT_E_CUDA;
     G->solver = SOLVER_EGT;
@@ -1098,11 +1211,13 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
     }
     std::vector<double> mu(2 * (size_t)Gn);
     const bool given = mu_x > 0 && mu_y > 0;
+    double* omega = nullptr;  // A^T x_omega once the mu search has evaluated it
     std::vector<double> mth(Gn);
     if (!given) {
         // mu_x = mu_y = ||A|| / sqrt(phi_X phi_Y), phi = 1/M
         const std::vector<double> amax = compute_max_abs_A_all(H);
         for (int g = 0; g < Gn; ++g) mth[g] = amax[g] * std::sqrt(H.M[0][g] * H.M[1][g]);
+        tr.mark("max |A| (host)");
     }
     for (int g = 0; g < Gn; ++g) {
         mu[g] = given ? mu_x : mth[g];
@@ -1116,6 +1231,9 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
         std::vector<int> lo(Gn, 0), hi(Gn, 30), mid(Gn, 0);
         std::vector<double> chosen(mu), trial(mu);
         std::vector<double> vals(2 * (size_t)Gn);
+        if (egt_omega_gradient(G, G->RESP[1])) return EGT_E_CUDA;  // RESP is scratch until the first step
+        G->grads += 1;
+        omega = G->RESP[1];
         for (int round = 0; round < 6; ++round) {
             int any = 0;
             for (int g = 0; g < Gn; ++g) {
@@ -1126,8 +1244,8 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
             }
             if (!any) break;
             CK(cudaMemcpyAsync(G->sc.mu, trial.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
-            if (egt_initial_point(G)) return EGT_E_CUDA;
-            G->grads += 3;
+            if (egt_initial_point(G, omega)) return EGT_E_CUDA;
+            G->grads += 2;
             CK(cudaMemcpyAsync(vals.data(), G->sc.val, sizeof(double) * 2 * Gn, cudaMemcpyDeviceToHost, G->st));
             CK(cudaStreamSynchronize(G->st));
             for (int g = 0; g < Gn; ++g) {
@@ -1141,9 +1259,10 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
             chosen[Gn + g] = mu[Gn + g] * std::ldexp(1.0, -lo[g]);
         }
         CK(cudaMemcpyAsync(G->sc.mu, chosen.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
+        tr.mark("practical mu search (device, host waits per round)");
     }
-    if (egt_initial_point(G)) return EGT_E_CUDA;
-    G->grads += 3;
+    if (egt_initial_point(G, omega)) return EGT_E_CUDA;
+    G->grads += omega ? 2 : 3;
     G->grads_per_iter = variant == EGT_AS ? 4 : 3;
     if (variant == EGT_AS) {
         int r = enqueue_gap(G, 0, G->gapcur);  // eps_sad(x0, y0); steps keep it current
