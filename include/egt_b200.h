@@ -113,7 +113,10 @@ typedef struct {
  * Errors: EGT_E_ARG on an invalid spec (bad kind/deck/board/fractions), EGT_E_CUDA. */
 int egt_load_game(const egt_game_spec* spec, egt_game** out);
 
-/* Free everything owned by the handle (NULL is a no-op). */
+/* Free everything owned by the handle (NULL is a no-op).  Device buffers are allocated from
+ * the library's per-device memory pool and return to it: the memory stays reserved for the
+ * next game the process loads (the pool is never trimmed; processes that need it back for
+ * other allocators should exit or load no further games). */
 void egt_free_game(egt_game* game);
 
 /* Stream for every subsequent call on this game (cudaStream_t as void*; NULL = legacy default). */
