@@ -270,6 +270,10 @@ int egt_timing_get(egt_game* game, double* host_out);
 
 const char* egt_last_error(void);
 
+/* Release the memory the current device's library pool keeps reserved from freed games
+ * (cudaMemPoolTrimTo(pool, 0)); memory of live games is untouched.  EGT_E_CUDA on failure. */
+int egt_pool_trim(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,5 +7,5 @@ package does not load the library; the first solver call does, and fails loudly
 if it is missing.
 """
 from .binding import (CFR_PLUS, CFR_RM, CFR_RMP, EGT_AS, EGT_BALANCED, EGT_THEORY, KUHN, LEDUC,  # noqa: F401
-                      RIVER, EGTError, Game, load_game, load_library)
+                      RIVER, EGTError, Game, load_game, load_library, pool_trim)
 from .solve import solve  # noqa: F401

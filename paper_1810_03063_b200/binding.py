@@ -60,7 +60,7 @@ EXPORTS = [
     "egt_init", "egt_step", "cfr_init", "cfr_step", "saddle_gap", "get_avg_strategy",
     "get_strategy_device", "egt_scalars", "egt_last_error", "saddle_gap_device",
     "egt_timing", "egt_timing_get", "egt_nccl_unique_id", "egt_shard", "egt_gradient_rows",
-    "egt_ipc_handles", "egt_shard_peers", "egt_gradient_rows_to",
+    "egt_ipc_handles", "egt_shard_peers", "egt_gradient_rows_to", "egt_pool_trim",
 ]
 IPC_HANDLE_BYTES = 64
 KERNEL_KINDS = ("grad_Ay", "grad_ATx", "tree", "scalar", "comm")
@@ -103,6 +103,7 @@ def load_library():
         "get_strategy_device": ([P, I32, I32, VP], I32),
         "egt_scalars": ([P, ctypes.POINTER(D)], I32),
         "egt_last_error": ([], ctypes.c_char_p),
+        "egt_pool_trim": ([], I32),
         "saddle_gap_device": ([P, I32, VP], I32),
         "egt_timing": ([P, I32], I32),
         "egt_timing_get": ([P, ctypes.POINTER(D)], I32),
@@ -336,6 +337,12 @@ def _host_ptr(a):
         assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
         return a.ctypes.data
     return a.data_ptr()  # pinned torch CPU tensor
+
+
+def pool_trim():
+    """Give the memory the library's device pool keeps from freed games back to the driver
+    (egt_pool_trim); live games keep theirs."""
+    _check(load_library().egt_pool_trim())
 
 
 def nccl_unique_id():

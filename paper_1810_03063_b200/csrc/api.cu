@@ -165,6 +165,14 @@ static int dalloc(egt_game* G, T** p, size_t n) {
     return 0;
 }
 
+extern "C" int egt_pool_trim(void) {
+    cudaError_t e = cudaSuccess;
+    cudaMemPool_t pool = lib_pool(&e);
+    if (pool) e = cudaMemPoolTrimTo(pool, 0);
+    if (e != cudaSuccess) return fail(EGT_E_CUDA, std::string("pool trim: ") + cudaGetErrorString(e));
+    return 0;
+}
+
 // a per-game vector buffer of n elements in the game's precision (base address only):
 // from the library pool on the game's stream, or a plain cudaMalloc when the buffer is
 // shared with other processes through CUDA IPC (pool memory has no IPC handle)

@@ -72,3 +72,25 @@ def test_error_paths():
         P.Game(P.RIVER, n_games=1, river=workloads.river_spec("tiny"), boards=b, prior1=p1, prior2=p2)
     with pytest.raises(P.EGTError):      # unknown precision
         P.Game(P.KUHN, n_games=1, precision=7)
+
+
+def test_pool_reuse_and_trim():
+    """Game buffers come from the library's device pool: a freed game's memory serves the next
+    load, egt_pool_trim hands it back, and a game loaded after the trim computes the same."""
+    import torch
+    import paper_1810_03063_b200 as P
+    boards = workloads.random_boards(4, 77)
+    p1, p2 = workloads.random_priors(boards, 77)
+    spec = workloads.river_spec("simple")
+    gaps = []
+    for trim in (False, True, False):
+        G = P.Game(P.RIVER, n_games=4, river=spec, boards=boards, prior1=p1, prior2=p2)
+        G.egt_init(P.EGT_AS)
+        G.egt_step(5)
+        gaps.append(G.saddle_gap(0))
+        G.close()
+        if trim:
+            free0 = torch.cuda.mem_get_info()[0]
+            P.pool_trim()
+            assert torch.cuda.mem_get_info()[0] >= free0
+    assert np.array_equal(gaps[0], gaps[1]) and np.array_equal(gaps[1], gaps[2])
