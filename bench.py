@@ -170,30 +170,62 @@ def workload_config(args, game=None, world=1):
 
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
-    """nvidia-smi samples DURING the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle reasons sampled DURING the timed region (B200_PROFILING.md clocks
+    line): NVML every 10 ms (nvidia-smi every 200 ms if NVML is unavailable)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason{HwSlowdown,HwThermalSlowdown,SwThermalSlowdown,SwPowerCap}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reason names)
+        self.source = None
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def sample():
+                r = get_reasons(h)
+                return (float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), float(mx),
+                        {n for n, b in zip(self.NAMES, self.BITS) if r & b})
+            sample()
+            return sample
+        except Exception:
+            return None
+
+    def _smi(self):
+        def sample():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            r = [c.strip() for c in out.split(",")]
+            return (float(r[1]), float(r[2]), {n for n, v in zip(self.NAMES, r[5:9]) if v.lower() == "active"})
+        return sample
+
     def start(self):
+        sample = self._nvml()
+        self.source, period = ("nvml", 0.01) if sample else ("nvidia-smi", 0.2)
+        sample = sample or self._smi()
+
         def run():
-            while not self._stop.is_set():
+            while True:
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([c.strip() for c in out.split(",")])
+                    self.rows.append(sample())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                if self._stop.wait(period):
+                    break
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -202,13 +234,10 @@ class Clocks:
         if self._t:
             self._t.join(timeout=10)
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*(r[2] for r in self.rows))), "samples": len(self.rows),
+                "source": self.source}
 
 
 # ----------------------------------------------------------------------------- roofline
