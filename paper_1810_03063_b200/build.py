@@ -42,9 +42,9 @@ def build(force=False, verbose=False):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-pthread", "-I", os.path.join(ROOT, "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd[1:1] = os.environ.get("EGT_EXTRA_NVCC", "").split()  # experiments only
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
-            cmd[1:1] = os.environ.get("EGT_EXTRA_NVCC", "").split()  # experiments only
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

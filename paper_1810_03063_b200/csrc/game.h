@@ -18,7 +18,10 @@ constexpr int EGT_MAX_HANDS = 1280;
 // warps of the treeplex kernel; each level's nodes are scheduled onto them on the host
 constexpr int TREE_WARPS = 8;
 // terminals per CTA of the staged river gradient kernel (rows are never split)
-constexpr int GRAD_CHUNK_TERMS = 32;
+#ifndef EGT_GRAD_CHUNK_TERMS
+#define EGT_GRAD_CHUNK_TERMS 16
+#endif
+constexpr int GRAD_CHUNK_TERMS = EGT_GRAD_CHUNK_TERMS;
 constexpr int GRAD_CHUNK_MAX_TERMS = 64;  // a chunk never exceeds this (rows are small)
 
 enum NodeKind { ND_DECISION = 0, ND_CHANCE = 1, ND_TERMINAL = 2 };
