@@ -1063,8 +1063,24 @@ static int record_egt_iteration(egt_game* G) {
         CK(cudaMemcpyAsync(G->focus_host.data(), S.focus, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
         CK(cudaStreamSynchronize(G->st));
     }
+    // The two focus chains touch disjoint games (every launch is masked by the game's focus
+    // player), so in graph mode player 2's chain runs on the second stream beside player 1's:
+    // the half-empty masked launches of one chain fill the SMs the other leaves idle.  Not in
+    // timing mode (per-kernel events) and not when sharded (one all-reduce order on all ranks).
+    const bool fork_focus = !G->timing && !G->comm;
+    cudaStream_t main_st = G->st;
+    struct Restore {  // G->st is the main stream again on every exit path
+        egt_game* g;
+        cudaStream_t s;
+        ~Restore() { g->st = s; }
+    } restore{G, main_st};
+    if (fork_focus) {
+        CK(cudaEventRecord(G->ev_fork, main_st));
+        CK(cudaStreamWaitEvent(G->st2, G->ev_fork, 0));
+    }
     for (int p = 0; p < 2; ++p) {
         const int o = 1 - p;
+        if (fork_focus) G->st = p == 0 ? main_st : G->st2;
         if (var != EGT_AS) {
             // x_{mu_x}(y) for the focused player (not cached without the EGC check)
             CK(grad(G, p, slot2(G, G->S[o], o, 0), vec(G->GR[p], G->V[p]), S.focus, p));
@@ -1116,6 +1132,11 @@ static int record_egt_iteration(egt_game* G) {
         A.mask = S.focus;
         A.want = p;
         CK(tree(G, p, A));
+        G->st = main_st;
+    }
+    if (fork_focus) {
+        CK(cudaEventRecord(G->ev_join, G->st2));
+        CK(cudaStreamWaitEvent(main_st, G->ev_join, 0));
     }
     if (var == EGT_AS) {
         // excessive gap at the candidate: phi_{mu_x+}(y+) and -f_{mu_y+}(x+) (refreshes the
@@ -1124,7 +1145,6 @@ static int record_egt_iteration(egt_game* G) {
         // player 1's runs on a second stream (own reduction scratch) beside player 0's -- not
         // when sharded, where both chains' all-reduces must keep one order on every rank.
         const bool fork = !G->timing && !G->comm;
-        cudaStream_t main_st = G->st;
         if (fork) {
             CK(cudaEventRecord(G->ev_fork, main_st));
             CK(cudaStreamWaitEvent(G->st2, G->ev_fork, 0));
