@@ -58,7 +58,7 @@ def parse():
                     help="also time EGT/as and CFR+ to eps_sad <= --eps-mbb on this many endgames (0: skip)")
     ap.add_argument("--eps-mbb", type=float, nargs="+", default=[100.0, 10.0, 1.0],
                     help="saddle-gap targets in milli-big-blinds (time to each, median game)")
-    ap.add_argument("--converge-max-steps", type=int, default=4000)
+    ap.add_argument("--converge-max-steps", type=int, default=20000)
     ap.add_argument("--no-f32", action="store_true", help="skip the extra fp32-mode measurement")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="f32: the optional fp32 mode (fp32 vectors and arithmetic, DESIGN.md row 9)")
@@ -136,7 +136,7 @@ def time_to_gap(P, spec, boards, p1, p2, solver, eps_mbb, max_steps, check_every
         ev.record(st)
         g = gap.cpu().numpy()
         checks.append((steps, ev, float(np.median(g)), float(np.max(g))))
-        if checks[-1][3] <= targets[-1] * mbb:
+        if checks[-1][2] <= targets[-1] * mbb:  # the median game reached the last target
             break
     torch.cuda.synchronize()
     sc = game.egt_scalars()
