@@ -211,3 +211,47 @@ def test_reduced_decks_ragged_tiles(n_ranks, n_suits):
         for g in range(G.n_games):
             assert np.abs(pair.from_product(g, p, q[g])[1:] - wants[g][0][1:]).max() <= TOL
             assert abs(vals[g] - wants[g][1]) <= TOL * max(1.0, abs(wants[g][1]))
+
+
+@pytest.mark.parametrize("variant", ["cfr_rm", "cfr_rmp"])
+def test_bench_workload_cfr_variants(bench_pair, variant):
+    """CFR(RM) and CFR(RM+) (uniform averaging) on the whole bench batch, one sampled game
+    against the oracle: averages and their saddle-point gap after 2 iterations."""
+    import paper_1810_03063_b200 as P
+    pair, G = bench_pair, bench_pair.game
+    g = SAMPLE[1]
+    G.cfr_init({"cfr_rm": P.CFR_RM, "cfr_rmp": P.CFR_RMP}[variant])
+    G.cfr_step(2)
+    avg = []
+    for p in (0, 1):
+        d = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
+        G.get_strategy_device(p, 1, d)
+        avg.append(pair.from_product(g, p, host(d).reshape(G.n_games, -1)[g]))
+    gaps = G.saddle_gap(1)
+    st = cfr.run(pair.sf[g], variant, 2)
+    assert np.abs(avg[0][1:] - st.xbar[1:]).max() <= TOL
+    assert np.abs(avg[1][1:] - st.ybar[1:]).max() <= TOL
+    want = br.saddle_gap(pair.sf[g], st.xbar, st.ybar)
+    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+
+
+def test_bench_workload_egt_balanced(bench_pair):
+    """EGT with mu balancing on the whole bench batch: game 295's iterate
+    after 2 graph-launched iterations against the oracle."""
+    import paper_1810_03063_b200 as P
+    pair, G = bench_pair, bench_pair.game
+    g = SAMPLE[-1]
+    sf = pair.sf[g]
+    mu = egt.theory_mu(sf) * 2.0 ** -4
+    G.egt_init(P.EGT_BALANCED, mu, mu)
+    G.egt_step(2)
+    xs = torch.zeros(G.vec_shape(0), dtype=torch.float64, device="cuda")
+    ys = torch.zeros(G.vec_shape(1), dtype=torch.float64, device="cuda")
+    G.get_strategy_device(0, 0, xs)
+    G.get_strategy_device(1, 0, ys)
+    st, prob = egt.run(sf, "balanced", 2, mu=mu)
+    assert np.abs(pair.from_product(g, 0, host(xs).reshape(G.n_games, -1)[g])[1:] - st.x[1:]).max() <= TOL
+    assert np.abs(pair.from_product(g, 1, host(ys).reshape(G.n_games, -1)[g])[1:] - st.y[1:]).max() <= TOL
+    gaps = G.saddle_gap(0)
+    want = br.saddle_gap(sf, st.x, st.y)
+    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
