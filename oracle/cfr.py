@@ -25,18 +25,20 @@ def alpha(scheme, t):
 SNAP = 1e-13
 
 
-def regret_update(kind, r, z, g):
+def regret_update(kind, r, z, g, scale=0.0):
     """One call of RM or RM+  on one simplex.
     g is the gain (utility) vector; returns (r^t, z^t).
 
     Reading R15: "if r^t = 0 use uniform strategy" is decided robustly -- a regret
-    entry no larger than SNAP * (|r^{t-1}_a| + |g_a| + |<z^{t-1}, g>|) (the rounding
-    noise of its own update) counts as 0 in [r^t]^+."""
+    entry no larger than SNAP * (|r^{t-1}_a| + |g_a| + |<z^{t-1}, g>| + scale) (the rounding
+    noise of its own update; `scale` = the largest |gradient entry| among the player's
+    sequences of the same private hand, the noise floor of gains that cancel to ~0 where
+    the opponent's reach is ~0) counts as 0 in [r^t]^+."""
     val = float(np.dot(z, g))
     r_new = r + g - val
     if kind == "rmp":
         r_new = np.maximum(r_new, 0.0)
-    tol = SNAP * (np.abs(r) + np.abs(g) + abs(val))
+    tol = SNAP * (np.abs(r) + np.abs(g) + abs(val) + scale)
     pos = np.where(r_new > tol, r_new, 0.0)
     tot = pos.sum()
     z_new = pos / tot if tot > 0 else np.full(len(r), 1.0 / len(r))
@@ -59,17 +61,31 @@ class CFRState:
         self.grads = 0
 
 
-def _pass(tp, g, z, r, kind):
+def hand_scales(labels, g):
+    """Per sequence: max |g| over the player's sequences of the same private hand (labels
+    "<hand>|<history>"; the empty sequence gets 0) -- the scale of reading R15."""
+    groups = {}
+    for i, lab in enumerate(labels):
+        if i > 0:
+            groups.setdefault(lab.split("|")[0], []).append(i)
+    sc = np.zeros(len(g))
+    for idx in groups.values():
+        sc[idx] = np.abs(np.asarray(g)[idx]).max()
+    return sc
+
+
+def _pass(tp, g, z, r, kind, labels=None):
     """Bottom-up pass of Gen-CFR lines 30-33 / 36-39: fold <g^j, z^{j,t-1}> into
     g_{p_j}, then z^{j,t} = R(g^j)."""
     g = np.array(g, dtype=float)
+    sc = hand_scales(labels, g) if labels is not None else np.zeros(len(g))
     z = z.copy()
     r = r.copy()
     for j in tp.bottom_up():
         s, n, p = tp.start[j], tp.size[j], tp.parent[j]
         gj = g[s:s + n]
         g[p] += np.dot(gj, z[s:s + n])
-        r[s:s + n], z[s:s + n] = regret_update(kind, r[s:s + n], z[s:s + n], gj)
+        r[s:s + n], z[s:s + n] = regret_update(kind, r[s:s + n], z[s:s + n], gj, sc[s])
     return z, r
 
 
@@ -77,13 +93,13 @@ def cfr_iteration(st):
     sf = st.sf
     g = -sf.Ay(st.y)                                   # line 29: g = -A y^{t-1}
     st.grads += 1
-    st.zx, st.rx = _pass(sf.X, g, st.zx, st.rx, st.kind)
+    st.zx, st.rx = _pass(sf.X, g, st.zx, st.rx, st.kind, sf.labels_x)
     st.x = sf.X.behavioral_to_sequence(st.zx)
     a = alpha(st.scheme, st.t)
     st.xbar = a * st.x + (1 - a) * st.xbar            # line 34
     g = sf.ATx(st.x)                                   # line 35: g = A^T x^t (alternating)
     st.grads += 1
-    st.zy, st.ry = _pass(sf.Y, g, st.zy, st.ry, st.kind)
+    st.zy, st.ry = _pass(sf.Y, g, st.zy, st.ry, st.kind, sf.labels_y)
     st.y = sf.Y.behavioral_to_sequence(st.zy)
     st.ybar = a * st.y + (1 - a) * st.ybar            # line 41, same alpha^t (reading R9)
     st.t += 1

@@ -741,6 +741,7 @@ struct TreeNodeCtx {
     int cfr_plus;
     T mu;
     const double* __restrict__ exptab;
+    T cfr_scale;  // CFR: max |g| over the hand's sequences (the noise floor of reading R15)
 };
 
 // Bottom-up work of simplex (node m, hand h) on its column; returns the simplex value.
@@ -808,7 +809,7 @@ __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlay
         if (C.cfr_plus) r = fmax(r, T(0));
         rg[ix] = r;
         // DESIGN.md R15: regrets at the rounding-noise level of their own update count as 0
-        const T tol = cfr_noise<T>() * (fabs(r0) + fabs(u) + fabs(v));
+        const T tol = cfr_noise<T>() * (fabs(r0) + fabs(u) + fabs(v) + C.cfr_scale);
         const T pr = r > tol ? r : T(0);
         col[a * TH_HANDS] = pr;
         S += pr;
@@ -896,7 +897,7 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
             T rr = r0 + u - v;
             if (C.cfr_plus) rr = fmax(rr, T(0));
             rg[ix0 + (size_t)a * Hp] = rr;
-            const T tol = cfr_noise<T>() * (fabs(r0) + fabs(u) + fabs(v));  // DESIGN.md R15
+            const T tol = cfr_noise<T>() * (fabs(r0) + fabs(u) + fabs(v) + C.cfr_scale);  // DESIGN.md R15
             x[a] = rr > tol ? rr : T(0);
             S += x[a];
         }
@@ -1117,6 +1118,16 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
     // ---- bottom-up, deepest level first
     TreeNodeCtx<T> C;
     C.cfr_plus = A.cfr_plus;
+    C.cfr_scale = T(0);
+    // CFR (reading R15): each hand's noise floor, the largest |g| over its sequences (the raw
+    // tile; |gsign| = 1), taken before the bottom-up folds child values in
+    T cfr_scale[TH_HPL];
+#pragma unroll
+    for (int j = 0; j < TH_HPL; ++j) {
+        cfr_scale[j] = T(0);
+        if (MODE == TM_CFR)
+            for (int r = 1; r < n_pub; ++r) cfr_scale[j] = fmax(cfr_scale[j], fabs(tile[r * TH_HANDS + lane + 32 * j]));
+    }
     C.mu = (mode == TM_SBR) ? (T)A.mu[g] : T(1);
     C.exptab = s_exptab;
     T* __restrict__ cz = A.center.ok() ? A.center.at<T>(g) : nullptr;
@@ -1142,6 +1153,7 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
                             wgt = (T)(wmu * P.beta[(size_t)m * Hp + h]);
                             iw = T(1) / wgt;
                         }
+                        if (MODE == TM_CFR) C.cfr_scale = cfr_scale[j];
                         value = tree_node_up_any<MODE, T>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
                     } else {
                         for (int a = 0; a < n; ++a) col[a * TH_HANDS] = T(0);
