@@ -255,3 +255,45 @@ def test_bench_workload_egt_balanced(bench_pair):
     gaps = G.saddle_gap(0)
     want = br.saddle_gap(sf, st.x, st.y)
     assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+
+
+@pytest.mark.parametrize("solver", ["egt_as", "cfr_plus"])
+def test_bench_workload_longer_runs(bench_pair, solver):
+    """Eight graph-launched iterations on the whole bench batch (EGT/as; CFR+), game 147
+    against the oracle: iterate / average, counters, eps_sad.  EGT/as starts from mu_theory/16
+    so that every prox centre stays interior for the oracle's literal prox form (DESIGN.md
+    R16; the practical mu search drives smoothed responses to fp64 underflow within a few
+    iterations, where only the kernel's multiplicative form is defined)."""
+    import paper_1810_03063_b200 as P
+    pair, G = bench_pair, bench_pair.game
+    g = SAMPLE[1]
+    sf = pair.sf[g]
+    n = 8
+    if solver == "egt_as":
+        mu_x = mu_y = egt.theory_mu(sf) / 16.0
+        G.egt_init(P.EGT_AS, mu_x, mu_y)
+        G.egt_step(n)
+        sc = G.egt_scalars()
+        prob = egt.Problem(sf)
+        x, y = egt.initialize(prob, mu_x, mu_y)
+        st = egt.EGTState(x, y, mu_x, mu_y)
+        for _ in range(int(sc[g, 3])):
+            egt.egt_iteration(prob, st, "as")
+        assert int(sc[g, 3]) + int(sc[g, 5]) == n and st.backtracks == int(sc[g, 5])
+        assert abs(sc[g, 0] - st.mu_x) <= 1e-12 * st.mu_x and abs(sc[g, 1] - st.mu_y) <= 1e-12 * st.mu_y
+        which, want_x, want_y = 0, st.x, st.y
+    else:
+        G.cfr_init(P.CFR_PLUS)
+        G.cfr_step(n)
+        st = cfr.run(sf, "cfr_plus", n)
+        which, want_x, want_y = 1, st.xbar, st.ybar
+    got = []
+    for p in (0, 1):
+        d = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
+        G.get_strategy_device(p, which, d)
+        got.append(pair.from_product(g, p, host(d).reshape(G.n_games, -1)[g]))
+    assert np.abs(got[0][1:] - want_x[1:]).max() <= TOL
+    assert np.abs(got[1][1:] - want_y[1:]).max() <= TOL
+    gaps = G.saddle_gap(which)
+    want = br.saddle_gap(sf, want_x, want_y)
+    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
