@@ -54,7 +54,98 @@ static int64_t eval5(const int* r, const int* s) {
     return key;
 }
 
+// The best 5 of n <= 7 cards directly (rank counts, suit counts, rank masks) -- the same key
+// as the maximum of eval5 over all 5-subsets (hand_strength_subsets), which it replaces on
+// the load path: category, then the group ranks ordered by (count desc, rank desc).
 int64_t hand_strength(const int* ranks, const int* suits, int n) {
+    if (n < 5 || n > 7) return hand_strength_subsets(ranks, suits, n);
+    int cnt[13] = {0}, scnt[8] = {0};
+    unsigned mask = 0, smask[8] = {0};
+    for (int i = 0; i < n; ++i) {
+        cnt[ranks[i]]++;
+        mask |= 1u << ranks[i];
+        const int su = suits[i] & 7;
+        scnt[su]++;
+        smask[su] |= 1u << ranks[i];
+    }
+    auto top_straight = [](unsigned m) {
+        for (int hi = 12; hi >= 4; --hi)
+            if (((m >> (hi - 4)) & 0x1Fu) == 0x1Fu) return hi;
+        if ((m & 0x100Fu) == 0x100Fu) return 3;  // wheel A-2-3-4-5
+        return -1;
+    };
+    auto key_of = [](int cat, const int* g, int ng) {
+        int64_t key = cat;
+        for (int i = 0; i < 5; ++i) key = key * 13 + (i < ng ? g[i] : 0);
+        return key;
+    };
+    auto straight_key = [](int cat, int top) {
+        int64_t key = (int64_t)cat * 13 + top;
+        for (int i = 1; i < 5; ++i) key *= 13;
+        return key;
+    };
+    int fs = -1;
+    for (int su = 0; su < 8; ++su)
+        if (scnt[su] >= 5) fs = su;
+    if (fs >= 0) {
+        const int t = top_straight(smask[fs]);
+        if (t >= 0) return straight_key(8, t);
+    }
+    // ranks by count, descending rank
+    int quads = -1, trips[2] = {-1, -1}, pairs[3] = {-1, -1, -1}, nt = 0, np = 0;
+    for (int rk = 12; rk >= 0; --rk) {
+        if (cnt[rk] == 4 && quads < 0) quads = rk;
+        else if (cnt[rk] == 3 && nt < 2) trips[nt++] = rk;
+        else if (cnt[rk] == 2 && np < 3) pairs[np++] = rk;
+    }
+    auto kickers = [&](int* out, int want, int ex1, int ex2) {  // highest ranks not ex1/ex2
+        int k = 0;
+        for (int rk = 12; rk >= 0 && k < want; --rk)
+            if (cnt[rk] > 0 && rk != ex1 && rk != ex2) out[k++] = rk;
+        return k;
+    };
+    int g[5];
+    if (quads >= 0) {
+        g[0] = quads;
+        const int k = kickers(g + 1, 1, quads, -1);
+        return key_of(7, g, 1 + k);
+    }
+    if (nt >= 1 && (nt >= 2 || np >= 1)) {  // full house: best trips + best other pair
+        g[0] = trips[0];
+        g[1] = nt >= 2 ? (np >= 1 ? std::max(trips[1], pairs[0]) : trips[1]) : pairs[0];
+        return key_of(6, g, 2);
+    }
+    if (fs >= 0) {
+        int k = 0;
+        for (int rk = 12; rk >= 0 && k < 5; --rk)
+            if (smask[fs] >> rk & 1u) g[k++] = rk;
+        return key_of(5, g, 5);
+    }
+    {
+        const int t = top_straight(mask);
+        if (t >= 0) return straight_key(4, t);
+    }
+    if (nt >= 1) {
+        g[0] = trips[0];
+        const int k = kickers(g + 1, 2, trips[0], -1);
+        return key_of(3, g, 1 + k);
+    }
+    if (np >= 2) {
+        g[0] = pairs[0];
+        g[1] = pairs[1];
+        const int k = kickers(g + 2, 1, pairs[0], pairs[1]);
+        return key_of(2, g, 2 + k);
+    }
+    if (np == 1) {
+        g[0] = pairs[0];
+        const int k = kickers(g + 1, 3, pairs[0], -1);
+        return key_of(1, g, 1 + k);
+    }
+    const int k = kickers(g, 5, -1, -1);
+    return key_of(0, g, k);
+}
+
+int64_t hand_strength_subsets(const int* ranks, const int* suits, int n) {
     int64_t best = -1;
     int idx[5];
     // all 5-subsets of n <= 7 cards

@@ -134,5 +134,7 @@ std::vector<double> compute_max_abs_A_all(const HostGame& G);
 
 // 5..7-card poker hand strength (larger is better, equal = tie).
 int64_t hand_strength(const int* ranks, const int* suits, int n);
+// the same key by brute force: max of the 5-card evaluation over all 5-subsets
+int64_t hand_strength_subsets(const int* ranks, const int* suits, int n);
 
 }  // namespace egt
