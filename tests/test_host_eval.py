@@ -1,0 +1,21 @@
+"""Host-side hand evaluation of the CUDA path's loader (csrc/game.cpp): the direct 7-card
+evaluator agrees with the brute-force 5-subset maximum (compiled with g++, CPU only)."""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="needs g++")
+def test_direct_evaluator_matches_subset_maximum(tmp_path):
+    exe = tmp_path / "hs_check"
+    csrc = os.path.join(ROOT, "paper_1810_03063_b200", "csrc")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-pthread", "-I", os.path.join(ROOT, "include"), "-I", csrc,
+                    os.path.join(ROOT, "tests", "cpp", "hand_strength_check.cpp"), os.path.join(csrc, "game.cpp"),
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout
+    assert "mismatches 0" in out.stdout
