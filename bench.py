@@ -521,6 +521,34 @@ def run_b200(args):
                              "what": "same workload and timing with precision EGT_F32 (parity 1e-5 vs the oracle)"}
         g32.close()
 
+    if rank == 0 and world == 1 and args.workload == "libratus" and not args.no_f32 and not args.shard:
+        # BASELINE.json configs[2]: the {1/2, 1, all-in} abstraction on the same boards and
+        # ranges, same step and timing (a smaller tree: 90 public sequences per player)
+        from paper_1810_03063_b200 import workloads as W
+        gs = P.Game(P.RIVER, n_games=args.batch, river=W.river_spec("simple"), boards=boards, prior1=p1,
+                    prior2=p2, precision=args.precision)
+        gs.set_stream(stream)
+        gs.egt_init(P.EGT_AS)
+        gaps_s = torch.zeros(args.batch, dtype=torch.float64, device="cuda")
+        for _ in range(args.warmup):
+            gs.egt_step(1)
+            gs.saddle_gap_device(0, gaps_s)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            gs.egt_step(1)
+            gs.saddle_gap_device(0, gaps_s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        mss = e0.elapsed_time(e1)
+        line["simple_abstraction"] = {"value": throughput(args.batch, 1, args.steps, mss), "unit": UNIT,
+                                      "ms_per_step": mss / args.steps, "pub_seqs": list(gs.n_pub),
+                                      "terminals": gs.n_terminals,
+                                      "what": "BASELINE.json configs[2]: {1/2, 1, all-in} bet abstraction, same "
+                                              "boards, ranges, batch and timing"}
+        gs.close()
+
     if args.converge_games > 0:
         n = args.converge_games
         conv = [time_to_gap(P, spec, boards[:n], p1[:n], p2[:n], sv, args.eps_mbb, args.converge_max_steps,
