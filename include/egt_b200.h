@@ -231,7 +231,9 @@ int egt_shard(egt_game* game, int32_t rank, int32_t world, const uint8_t* id);
  * (peer memory), then a one-element NCCL all-reduce orders the ranks.  Rows are disjoint, so
  * no reduction is needed and each gradient crosses NVLink once (an all-reduce moves it twice).
  * egt_ipc_handles: HOST out[2 * EGT_IPC_HANDLE_BYTES], this rank's gradient buffers (player 0,
- * player 1) as CUDA IPC handles.  egt_shard_peers: HOST handles[world][2][EGT_IPC_HANDLE_BYTES]
+ * player 1) as CUDA IPC handles (the first call moves those buffers from the library's memory
+ * pool, which has no IPC export, to plain device allocations; call it before egt_init /
+ * cfr_init).  egt_shard_peers: HOST handles[world][2][EGT_IPC_HANDLE_BYTES]
  * gathered from every rank (own entry ignored); after egt_shard with an NCCL id, before
  * egt_init / cfr_init; world <= 8.  Applies to the solvers' gradients (egt_gradient keeps the
  * all-reduce, its output buffer being the caller's). */
