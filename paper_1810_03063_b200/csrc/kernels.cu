@@ -1232,11 +1232,24 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
             }
         }
     }
+    // the global rows a node's descent reads (convex-combination input, behavioural input,
+    // running average): the next node's are requested into L1 while this one is processed
+    const T* pf_src[3] = {ci, bin, av};
+    auto prefetch_node = [&](int m2) {
+        const int f2 = s_first[m2], n2 = s_nact[m2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (pf_src[k])
+                for (int a = 0; a < n2; ++a)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(pf_src[k] + (size_t)(f2 + a) * Hp + h0 + lane));
+    };
     for (int L = 0; L < n_lv; ++L) {
         const int i0 = s_so[L * TH_WARPS + wid], i1 = s_so[L * TH_WARPS + wid + 1];
+        if (i0 < i1) prefetch_node(s_sn[i0]);
         for (int idx = i0; idx < i1; ++idx) {
             const int m = s_sn[idx];
             const int first = s_first[m], n = s_nact[m], par = s_par[m];
+            if (idx + 1 < i1) prefetch_node(s_sn[idx + 1]);
 #pragma unroll
             for (int j = 0; j < TH_HPL; ++j) {
                 const int c = lane + 32 * j, h = h0 + c;
