@@ -282,8 +282,9 @@ static void nccl_destroy(ncclComm_t c) {
 
 // Rows of player p's gradient that shard `rank` of `world` computes: a contiguous range of
 // the sequences that end a terminal, balanced by terminal count, split into chunks of
-// <= GRAD_CHUNK_TERMS terminals (relative to the range) for the staged kernel.
-static void shard_rows(const PlayerLayout& L, int rank, int world, int& r0, int& r1, std::vector<int>& chunks) {
+// ~grad_chunk_terms(n_games) terminals (relative to the range) for the staged kernel.
+static void shard_rows(const PlayerLayout& L, int rank, int world, int chunk_terms, int& r0, int& r1,
+                       std::vector<int>& chunks) {
     const int n = (int)L.rows_term.size();
     std::vector<long long> cum(n + 1, 0);
     for (int r = 0; r < n; ++r) cum[r + 1] = cum[r] + (L.term_off[L.rows_term[r] + 1] - L.term_off[L.rows_term[r]]);
@@ -296,7 +297,7 @@ static void shard_rows(const PlayerLayout& L, int rank, int world, int& r0, int&
     chunks.assign(1, 0);
     for (int r = r0, cnt = 0; r < r1; ++r) {
         cnt += (int)(cum[r + 1] - cum[r]);
-        if (cnt >= GRAD_CHUNK_TERMS || r + 1 == r1) {
+        if (cnt >= chunk_terms || r + 1 == r1) {
             chunks.push_back(r + 1 - r0);
             cnt = 0;
         }
@@ -316,7 +317,7 @@ static int max_chunk_terms(const PlayerLayout& L, int r0, const std::vector<int>
 static int make_slice(egt_game* G, int p, int rank, int world, DevPlayer& out, std::vector<void*>& allocs) {
     int r0, r1;
     std::vector<int> chunks;
-    shard_rows(G->host.pl[p], rank, world, r0, r1, chunks);
+    shard_rows(G->host.pl[p], rank, world, grad_chunk_terms(G->host.n_games), r0, r1, chunks);
     out = G->dp_full[p];
     out.rows_term = G->dp_full[p].rows_term + r0;
     out.n_rows_term = r1 - r0;

@@ -386,7 +386,7 @@ static void build_layout(HostGame& G) {
         for (int r = 0, n = 0; r < (int)L.rows_term.size(); ++r) {
             const int s = L.rows_term[r];
             n += L.term_off[s + 1] - L.term_off[s];
-            if (n >= GRAD_CHUNK_TERMS || r + 1 == (int)L.rows_term.size()) {
+            if (n >= grad_chunk_terms(G.n_games) || r + 1 == (int)L.rows_term.size()) {
                 L.chunk_off.push_back(r + 1);
                 n = 0;
             }
