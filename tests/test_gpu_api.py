@@ -94,3 +94,27 @@ def test_pool_reuse_and_trim():
             P.pool_trim()
             assert torch.cuda.mem_get_info()[0] >= free0
     assert np.array_equal(gaps[0], gaps[1]) and np.array_equal(gaps[1], gaps[2])
+
+
+def test_batch_independence():
+    """A game's EGT/as trajectory does not depend on the batch around it (different chunking,
+    launch shapes, masks): games 0 and n-1 of a 300-game batch equal the same games solved
+    alone, bit for bit."""
+    import paper_1810_03063_b200 as P
+    n = 300
+    spec = workloads.river_spec("libratus")
+    boards = workloads.random_boards(n, 99)
+    p1, p2 = workloads.random_priors(boards, 99)
+    G = P.Game(P.RIVER, n_games=n, river=spec, boards=boards, prior1=p1, prior2=p2)
+    G.egt_init(P.EGT_AS)
+    G.egt_step(3)
+    gap = G.saddle_gap(0)
+    sc = G.egt_scalars()
+    G.close()
+    for i in (0, n - 1):
+        G1 = P.Game(P.RIVER, n_games=1, river=spec, boards=boards[i:i + 1], prior1=p1[i:i + 1], prior2=p2[i:i + 1])
+        G1.egt_init(P.EGT_AS)
+        G1.egt_step(3)
+        assert G1.saddle_gap(0)[0] == gap[i]
+        assert np.array_equal(G1.egt_scalars()[0, :7], sc[i, :7])
+        G1.close()
