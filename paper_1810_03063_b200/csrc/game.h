@@ -22,10 +22,10 @@ constexpr int TREE_WARPS = 8;
 #define EGT_GRAD_CHUNK_TERMS 16
 #endif
 constexpr int GRAD_CHUNK_TERMS = EGT_GRAD_CHUNK_TERMS;
-// Terminals per gradient CTA for a batch of n_games: GRAD_CHUNK_TERMS from two games per SM up
-// (the bench batch), fewer for small batches so that a launch still spreads over the SMs
+// Terminals per gradient CTA for a batch of n_games: GRAD_CHUNK_TERMS from half a game per SM
+// up, fewer for small batches so that a launch still spreads over the SMs
 inline int grad_chunk_terms(int n_games) {
-    const int t = (GRAD_CHUNK_TERMS * n_games + 295) / 296;
+    const int t = (GRAD_CHUNK_TERMS * n_games + 73) / 74;
     return t < 4 ? 4 : (t > GRAD_CHUNK_TERMS ? GRAD_CHUNK_TERMS : t);
 }
 constexpr int GRAD_CHUNK_MAX_TERMS = 64;  // a chunk never exceeds this (rows are small)
