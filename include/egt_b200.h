@@ -180,6 +180,15 @@ int egt_init(egt_game* game, int32_t variant, double mu_x, double mu_y);
  * unchanged, so Alg. 4's inner loop unrolls into consecutive iterations. */
 int egt_step(egt_game* game, int32_t n_iters);
 
+/* Per-game stopping target for EGT_AS, Alg. 3's "while eps_sad(x, y) > eps"
+ * decided on the device: before each iteration a game whose maintained eps_sad is <= its
+ * target stops (every launch of the iteration skips it; its iterate, mu, tau and gap stay),
+ * so a batch spends no work on games already solved.  host_eps: HOST [n_games] targets in
+ * the game's payoff unit, <= 0 = none; NULL clears every target.  Every game is made live
+ * again (a lowered target resumes it).  Ignored by EGT_THEORY / EGT_BALANCED (they keep no
+ * gap) and by CFR.  Persists across egt_init. */
+int egt_set_target(egt_game* game, const double* host_eps);
+
 #define CFR_RM 0   /* CFR(RM):  RM,  alpha_t = 1/t */
 #define CFR_RMP 1  /* CFR(RM+): RM+, alpha_t = 1/t */
 #define CFR_PLUS 2 /* CFR+:     RM+, alpha_t = 2t/(t^2+t) */

@@ -60,7 +60,7 @@ EXPORTS = [
     "egt_init", "egt_step", "cfr_init", "cfr_step", "saddle_gap", "get_avg_strategy",
     "get_strategy_device", "egt_scalars", "egt_last_error", "saddle_gap_device",
     "egt_timing", "egt_timing_get", "egt_nccl_unique_id", "egt_shard", "egt_gradient_rows",
-    "egt_ipc_handles", "egt_shard_peers", "egt_gradient_rows_to", "egt_pool_trim",
+    "egt_ipc_handles", "egt_shard_peers", "egt_gradient_rows_to", "egt_pool_trim", "egt_set_target",
 ]
 IPC_HANDLE_BYTES = 64
 KERNEL_KINDS = ("grad_Ay", "grad_ATx", "tree", "scalar", "comm")
@@ -104,6 +104,7 @@ def load_library():
         "egt_scalars": ([P, ctypes.POINTER(D)], I32),
         "egt_last_error": ([], ctypes.c_char_p),
         "egt_pool_trim": ([], I32),
+        "egt_set_target": ([P, ctypes.POINTER(D)], I32),
         "saddle_gap_device": ([P, I32, VP], I32),
         "egt_timing": ([P, I32], I32),
         "egt_timing_get": ([P, ctypes.POINTER(D)], I32),
@@ -249,6 +250,15 @@ class Game:
     # ---- solvers
     def egt_init(self, variant, mu_x=0.0, mu_y=0.0):
         _check(self._L.egt_init(self._h, variant, float(mu_x), float(mu_y)))
+
+    def egt_set_target(self, eps):
+        """Per-game eps_sad target (scalar or [n_games], payoff units; None clears) at which
+        an EGT/as game stops iterating, decided on the device (egt_set_target)."""
+        if eps is None:
+            _check(self._L.egt_set_target(self._h, None))
+            return
+        t = np.ascontiguousarray(np.broadcast_to(np.asarray(eps, dtype=np.float64), (self.n_games,)))
+        _check(self._L.egt_set_target(self._h, t.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
 
     def egt_step(self, n=1):
         _check(self._L.egt_step(self._h, n))

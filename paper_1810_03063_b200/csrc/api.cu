@@ -534,6 +534,16 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(dalloc(G, &S.attempts, (size_t)Gn));
     TRY(dalloc(G, &S.backtracks, (size_t)Gn));
     TRY(dalloc(G, &S.fail, (size_t)Gn));
+    TRY(dalloc(G, &S.live, (size_t)Gn));
+    {
+        double* tg = nullptr;
+        TRY(dalloc(G, &tg, (size_t)Gn));
+        if (cudaMemsetAsync(tg, 0, sizeof(double) * Gn, G->st) != cudaSuccess) {
+            egt_free_game(G);
+            return fail(EGT_E_CUDA, "memset");
+        }
+        S.target = tg;
+    }
     TRY(dalloc(G, &G->gapval, 2 * (size_t)Gn));
     TRY(dalloc(G, &G->gapcur, (size_t)Gn));
     S.brval = G->gapval;
@@ -901,9 +911,14 @@ static cudaError_t timing_flush(egt_game* G) {
 static long long active_games(egt_game* G, const int* mask, int want) {
     const int Gn = G->host.n_games;
     if (!mask) return Gn;
-    if (mask != G->sc.focus || (int)G->focus_host.size() != Gn) return Gn;
+    if ((int)G->focus_host.size() != Gn) return Gn;
     long long n = 0;
-    for (int g = 0; g < Gn; ++g) n += G->focus_host[g] == want;
+    if (mask == G->sc.focus)
+        for (int g = 0; g < Gn; ++g) n += G->focus_host[g] == want;
+    else if (mask == G->sc.live)  // a stopped game has focus -1; live games have 0 or 1
+        for (int g = 0; g < Gn; ++g) n += (G->focus_host[g] >= 0) == (want == 1);
+    else
+        return Gn;
     return n;
 }
 
@@ -1158,7 +1173,7 @@ static int record_egt_iteration(egt_game* G) {
             double* br_partial = (fork && p == 1) ? G->partial2_br : G->partial_br;
             unsigned* br_counter = (fork && p == 1) ? G->counter2_br : G->counter_br;
             int r = 0;
-            cudaError_t e = grad(G, p, slot2(G, G->S[o], o, 1), vec(G->GR[p], G->V[p]));
+            cudaError_t e = grad(G, p, slot2(G, G->S[o], o, 1), vec(G->GR[p], G->V[p]), S.live, 1);
             if (e == cudaSuccess) {
                 // one pass: the smoothed response (cache + EGV term) and the best response of
                 // the same gradient (the stopping test at the candidate)
@@ -1174,6 +1189,8 @@ static int record_egt_iteration(egt_game* G) {
                 A.br_value = G->gapval + (size_t)p * Gn;
                 A.br_partial = br_partial;
                 A.br_counter = br_counter;
+                A.mask = S.live;  // games that reached their target (egt_set_target) stop
+                A.want = 1;
                 e = tree(G, p, A);
             }
             G->st = main_st;
@@ -1217,6 +1234,8 @@ static int zero_scalars(egt_game* G) {
     CK(cudaMemsetAsync(S.egv, 0, sizeof(double) * Gn, G->st));
     std::vector<double> half(Gn, 0.5);
     CK(cudaMemcpyAsync(S.tau, half.data(), sizeof(double) * Gn, cudaMemcpyHostToDevice, G->st));
+    std::vector<int> ones(Gn, 1);
+    CK(cudaMemcpyAsync(S.live, ones.data(), sizeof(int) * Gn, cudaMemcpyHostToDevice, G->st));
     CK(cudaStreamSynchronize(G->st));
     return 0;
 }
@@ -1297,6 +1316,20 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
         int r = enqueue_gap(G, 0, G->gapcur);  // eps_sad(x0, y0); steps keep it current
         if (r) return r;
     }
+    return end(G);
+}
+
+extern "C" int egt_set_target(egt_game* G, const double* host_eps) {
+    if (!G) return fail(EGT_E_ARG, "null game");
+    const int Gn = G->host.n_games;
+    std::vector<double> t(Gn, 0.0);
+    if (host_eps)
+        for (int g = 0; g < Gn; ++g) t[g] = host_eps[g] > 0.0 ? host_eps[g] : 0.0;
+    std::vector<int> ones(Gn, 1);
+    if (begin(G)) return EGT_E_CUDA;
+    CK(cudaMemcpyAsync(const_cast<double*>(G->sc.target), t.data(), sizeof(double) * Gn, cudaMemcpyHostToDevice, G->st));
+    CK(cudaMemcpyAsync(G->sc.live, ones.data(), sizeof(int) * Gn, cudaMemcpyHostToDevice, G->st));
+    CK(cudaStreamSynchronize(G->st));
     return end(G);
 }
 

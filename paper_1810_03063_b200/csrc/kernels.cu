@@ -1338,6 +1338,13 @@ cudaError_t kernels_prepare() {
 __global__ void egt_prepare_kernel(int variant, int n, DevScalars S) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
+    // Alg. 3's "while eps_sad > eps" per game: a game whose maintained gap
+    // reached its target stops -- focus -1 and live 0 mask every launch of the iteration
+    if (variant == 2 && S.target[g] > 0.0 && S.gap[g] <= S.target[g]) S.live[g] = 0;
+    if (!S.live[g]) {
+        S.focus[g] = -1;
+        return;
+    }
     const double mx = S.mu[g], my = S.mu[n + g];
     int focus;
     if (variant == 0) focus = (S.t[g] & 1);           // even t: x (Alg. 1 lines 6-9)
@@ -1353,7 +1360,7 @@ __global__ void egt_prepare_kernel(int variant, int n, DevScalars S) {
 
 __global__ void egt_accept_kernel(int variant, int n, DevScalars S) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
+    if (g >= n || !S.live[g]) return;
     S.attempts[g] += 1;
     bool accept = true;
     if (variant == 2) {

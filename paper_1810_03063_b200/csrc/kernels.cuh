@@ -128,6 +128,8 @@ struct DevScalars {
     int* fail;        // [G]
     const double* brval;  // [2][G] best-response values at the EGT/as candidate (gap)
     double* gap;      // [G] eps_sad of the current iterate (EGT/as maintains it)
+    int* live;        // [G] 1 while the game iterates; 0 once its gap reached its target
+    const double* target;  // [G] per-game eps_sad target (<= 0: none), egt_set_target
 };
 
 // Launchers (return cudaGetLastError()).

@@ -33,6 +33,8 @@ def solve(game, solver="egt_as", eps=None, eps_mbb=None, max_iters=10000, check_
         else:
             game.egt_init(code, mu, mu)
         step, which = game.egt_step, 0
+        if solver == "egt_as" and eps > 0:
+            game.egt_set_target(eps)  # solved games stop on the device (no work spent on them)
     else:
         game.cfr_init(code)
         step, which = game.cfr_step, 1
@@ -47,5 +49,7 @@ def solve(game, solver="egt_as", eps=None, eps_mbb=None, max_iters=10000, check_
         step(n)
         it += n
         gap = game.saddle_gap(which)
+    if kind == "egt" and solver == "egt_as" and eps > 0:
+        game.egt_set_target(None)
     strategy = (game.get_avg_strategy(0), game.get_avg_strategy(1))
     return {"gap": gap, "iters": it, "strategy": strategy}

@@ -118,3 +118,41 @@ def test_batch_independence():
         assert G1.saddle_gap(0)[0] == gap[i]
         assert np.array_equal(G1.egt_scalars()[0, :7], sc[i, :7])
         G1.close()
+
+
+def test_device_stopping_target():
+    """egt_set_target: a game whose eps_sad reached its target stops on the device (its
+    iterate, counters and gap freeze); the others follow exactly the trajectory of a run
+    without targets; clearing the targets resumes the stopped games."""
+    import paper_1810_03063_b200 as P
+    n, k = 12, 60
+    spec = workloads.river_spec("simple")
+    boards = workloads.random_boards(n, 31)
+    p1, p2 = workloads.random_priors(boards, 31)
+
+    def run(target):
+        G = P.Game(P.RIVER, n_games=n, river=spec, boards=boards, prior1=p1, prior2=p2)
+        G.egt_init(P.EGT_AS)
+        if target is not None:
+            G.egt_set_target(target)
+        G.egt_step(k)
+        return G, G.saddle_gap(0), G.egt_scalars()
+
+    G0, gap0, sc0 = run(None)
+    G0.close()
+    eps = float(np.median(gap0)) * 1.5  # some games get there within k iterations, some not
+    G1, gap1, sc1 = run(eps)
+    attempts0, attempts1 = sc0[:, 4], sc1[:, 4]
+    stopped = attempts1 < k
+    assert stopped.any() and not stopped.all()
+    assert np.all(gap1[stopped] <= eps)
+    assert np.array_equal(gap1[~stopped], gap0[~stopped])
+    assert np.array_equal(sc1[~stopped, :7], sc0[~stopped, :7])
+    # a stopped game froze at the first iteration its gap was <= eps: iterating further never
+    # happened, so one more block of steps changes nothing for it
+    G1.egt_step(5)
+    assert np.array_equal(G1.egt_scalars()[stopped, :7], sc1[stopped, :7])
+    G1.egt_set_target(None)
+    G1.egt_step(5)
+    assert np.all(G1.egt_scalars()[stopped, 4] == sc1[stopped, 4] + 5)
+    G1.close()
