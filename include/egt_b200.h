@@ -185,8 +185,10 @@ int egt_step(egt_game* game, int32_t n_iters);
  * target stops (every launch of the iteration skips it; its iterate, mu, tau and gap stay),
  * so a batch spends no work on games already solved.  host_eps: HOST [n_games] targets in
  * the game's payoff unit, <= 0 = none; NULL clears every target.  Every game is made live
- * again (a lowered target resumes it).  Ignored by EGT_THEORY / EGT_BALANCED (they keep no
- * gap) and by CFR.  Persists across egt_init. */
+ * again (a lowered target resumes it).  CFR: a game stops when a saddle_gap /
+ * saddle_gap_device evaluation of its average (which = 1) finds eps_sad <= its target.
+ * Ignored by EGT_THEORY / EGT_BALANCED (they keep no gap).  Persists across egt_init /
+ * cfr_init. */
 int egt_set_target(egt_game* game, const double* host_eps);
 
 #define CFR_RM 0   /* CFR(RM):  RM,  alpha_t = 1/t */

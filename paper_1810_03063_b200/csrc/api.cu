@@ -1356,8 +1356,9 @@ static int record_cfr_iteration(egt_game* G) {
     const int Gn = G->host.n_games;
     for (int p = 0; p < 2; ++p) {
         const int o = 1 - p;
-        // Gen-CFR line 29 / 35: g = -A y^{t-1} (x), g = A^T x^t (y, alternating)
-        CK(grad(G, p, vec(G->Q[o], G->V[o]), vec(G->GR[p], G->V[p])));
+        // Gen-CFR line 29 / 35: g = -A y^{t-1} (x), g = A^T x^t (y, alternating); games that
+        // reached their target (egt_set_target) are skipped
+        CK(grad(G, p, vec(G->Q[o], G->V[o]), vec(G->GR[p], G->V[p]), G->sc.live, 1));
         TreeArgs A = base_args();
         A.mode = TM_CFR;
         A.g = vec(G->GR[p], G->V[p]);
@@ -1369,9 +1370,11 @@ static int record_cfr_iteration(egt_game* G) {
         A.iter = G->sc.t;
         A.cfr_plus = G->variant != CFR_RM;
         A.avg_linear = G->variant == CFR_PLUS;
+        A.mask = G->sc.live;
+        A.want = 1;
         CK(tree(G, p, A));
     }
-    CK(scalar_k(G, [&] { return launch_tick(Gn, G->sc.t, G->st); }));
+    CK(scalar_k(G, [&] { return launch_tick(Gn, G->sc.t, G->sc.live, G->st); }));
     return 0;
 }
 
@@ -1393,6 +1396,7 @@ extern "C" int cfr_init(egt_game* G, int32_t variant) {
     }
     G->solver = SOLVER_CFR;
     G->variant = variant;
+    G->focus_host.clear();  // timing mode counts every game of a CFR launch as active
     G->grads = 0;
     G->grads_per_iter = 2;
     std::vector<int> one(Gn, 1);
@@ -1474,7 +1478,10 @@ static int gap_into(egt_game* G, int which, double* dev_out) {
         CK(cudaMemcpyAsync(dev_out, G->gapcur, sizeof(double) * G->host.n_games, cudaMemcpyDeviceToDevice, G->st));
         return 0;
     }
-    return enqueue_gap(G, which, dev_out);
+    int r = enqueue_gap(G, which, dev_out);
+    if (!r && G->solver == SOLVER_CFR && which == 1)
+        CK(launch_stop_at_target(G->host.n_games, dev_out, G->sc.target, G->sc.live, G->st));
+    return r;
 }
 
 extern "C" int saddle_gap(egt_game* G, int32_t which, double* host_out) {

@@ -1383,9 +1383,21 @@ __global__ void egt_accept_kernel(int variant, int n, DevScalars S) {
     }
 }
 
-__global__ void tick_kernel(int n, int* t) {
+__global__ void tick_kernel(int n, int* t, const int* live) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < n) t[g] += 1;
+    if (g < n && (!live || live[g])) t[g] += 1;
+}
+
+// A CFR game whose evaluated eps_sad (of its average) reached its target stops (egt_set_target)
+__global__ void stop_at_target_kernel(int n, const double* __restrict__ gap, const double* __restrict__ target,
+                                      int* live) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n && target[g] > 0.0 && gap[g] <= target[g]) live[g] = 0;
+}
+
+cudaError_t launch_stop_at_target(int n, const double* gap, const double* target, int* live, cudaStream_t st) {
+    stop_at_target_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, gap, target, live);
+    return cudaGetLastError();
 }
 
 
@@ -1409,8 +1421,8 @@ cudaError_t launch_egt_accept(int variant, int n, DevScalars S, cudaStream_t st)
     egt_accept_kernel<<<(n + 127) / 128, 128, 0, st>>>(variant, n, S);
     return cudaGetLastError();
 }
-cudaError_t launch_tick(int n, int* t, cudaStream_t st) {
-    tick_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, t);
+cudaError_t launch_tick(int n, int* t, const int* live, cudaStream_t st) {
+    tick_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, t, live);
     return cudaGetLastError();
 }
 

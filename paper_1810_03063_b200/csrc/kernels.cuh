@@ -144,7 +144,8 @@ size_t tree_smem_bytes(const DevPlayer& P, int esz);
 
 cudaError_t launch_egt_prepare(int variant, int n_games, DevScalars S, cudaStream_t st);
 cudaError_t launch_egt_accept(int variant, int n_games, DevScalars S, cudaStream_t st);
-cudaError_t launch_tick(int n_games, int* t, cudaStream_t st);
+cudaError_t launch_tick(int n_games, int* t, const int* live, cudaStream_t st);  // live: nullptr = all
+cudaError_t launch_stop_at_target(int n_games, const double* gap, const double* target, int* live, cudaStream_t st);
 cudaError_t launch_gap_combine(int n, const double* val, double* out, cudaStream_t st);
 
 }  // namespace egt

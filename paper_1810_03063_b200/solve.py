@@ -33,11 +33,12 @@ def solve(game, solver="egt_as", eps=None, eps_mbb=None, max_iters=10000, check_
         else:
             game.egt_init(code, mu, mu)
         step, which = game.egt_step, 0
-        if solver == "egt_as" and eps > 0:
-            game.egt_set_target(eps)  # solved games stop on the device (no work spent on them)
     else:
         game.cfr_init(code)
         step, which = game.cfr_step, 1
+    use_target = eps > 0 and (kind == "cfr" or solver == "egt_as")
+    if use_target:
+        game.egt_set_target(eps)  # solved games stop on the device (no work spent on them)
     # at least one iteration first: the CFR average is defined from iteration 1 on
     # (Gen-CFR line 34 with alpha^1 = 1)
     it = min(check_every, max_iters) if max_iters > 0 else 0
@@ -49,7 +50,7 @@ def solve(game, solver="egt_as", eps=None, eps_mbb=None, max_iters=10000, check_
         step(n)
         it += n
         gap = game.saddle_gap(which)
-    if kind == "egt" and solver == "egt_as" and eps > 0:
+    if use_target:
         game.egt_set_target(None)
     strategy = (game.get_avg_strategy(0), game.get_avg_strategy(1))
     return {"gap": gap, "iters": it, "strategy": strategy}

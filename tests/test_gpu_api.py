@@ -156,3 +156,39 @@ def test_device_stopping_target():
     G1.egt_step(5)
     assert np.all(G1.egt_scalars()[stopped, 4] == sc1[stopped, 4] + 5)
     G1.close()
+
+
+def test_cfr_stopping_target():
+    """CFR with egt_set_target: a game stops at the first saddle_gap evaluation of its average
+    that finds eps_sad <= its target; the others run exactly as without targets."""
+    import paper_1810_03063_b200 as P
+    n, checks, every = 10, 6, 10
+    spec = workloads.river_spec("simple")
+    boards = workloads.random_boards(n, 41)
+    p1, p2 = workloads.random_priors(boards, 41)
+
+    def run(target):
+        G = P.Game(P.RIVER, n_games=n, river=spec, boards=boards, prior1=p1, prior2=p2)
+        G.cfr_init(P.CFR_PLUS)
+        if target is not None:
+            G.egt_set_target(target)
+        hist = []
+        for _ in range(checks):
+            G.cfr_step(every)
+            hist.append(G.saddle_gap(1))
+        t = G.egt_scalars()[:, 3]
+        G.close()
+        return np.array(hist), t
+
+    h0, t0 = run(None)
+    eps = float(np.median(h0[-1]))  # about half the games get there within the run
+    h1, t1 = run(eps)
+    first = [next((c for c in range(checks) if h0[c, g] <= eps), None) for g in range(n)]
+    assert any(f is not None for f in first) and any(f is None for f in first)
+    for g, f in enumerate(first):
+        if f is None:
+            assert np.array_equal(h1[:, g], h0[:, g]) and t1[g] == t0[g]
+        else:
+            assert np.array_equal(h1[:f + 1, g], h0[:f + 1, g])   # identical until it stopped
+            assert np.all(h1[f:, g] == h0[f, g])                   # then frozen
+            assert t1[g] == 1 + every * (f + 1)
