@@ -70,3 +70,43 @@ def test_random_river_configurations(case):
         egt.egt_iteration(prob, st, "as")
     got = pair.from_product(1, 0, xs.cpu().numpy().reshape(G.n_games, -1)[1])
     assert np.abs(got[1:] - st.x[1:]).max() <= TOL
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_random_configurations_cfr_and_fp32(case):
+    """The same random configurations: CFR+ averages after 3 iterations (fp64, 1e-9) and the
+    fp32 mode's gradients (1e-5, DESIGN.md row 9)."""
+    import paper_1810_03063_b200 as P
+    from oracle import cfr
+    rng = np.random.default_rng(5000 + case)
+    n_ranks, n_suits = [(13, 4), (9, 4), (13, 3), (7, 4), (6, 2), (10, 3), (13, 2), (8, 3)][case]
+    spec = random_spec(rng)
+    seed = int(rng.integers(1 << 30))
+    pair = Pair("river", n_games=2, spec=spec, seed=seed, n_ranks=n_ranks, n_suits=n_suits, build_sparse=False)
+    G = pair.game
+    G.cfr_init(P.CFR_PLUS)
+    G.cfr_step(3)
+    st = cfr.run(pair.sf[0], "cfr_plus", 3)
+    for p, want in ((0, st.xbar), (1, st.ybar)):
+        d = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
+        G.get_strategy_device(p, 1, d)
+        got = pair.from_product(0, p, d.cpu().numpy().reshape(G.n_games, -1)[0])
+        assert np.abs(got[1:] - want[1:]).max() <= TOL, (case, p)
+    G32 = P.Game(P.RIVER, n_games=2, river=spec, boards=pair.boards, prior1=pair.priors[0], prior2=pair.priors[1],
+                 n_ranks=n_ranks, n_suits=n_suits, precision="f32")
+    for p in (0, 1):
+        o = 1 - p
+        v = pair.tp(0, o).behavioral_to_sequence(random_behavioral(pair.tp(0, o), rng))
+        blk = np.zeros((2, G.n_pub[o] * G.H_pad))
+        blk[0] = pair.to_product(0, o, v, row0=1.0)
+        blk[1, :G.H] = 1.0
+        dout = torch.zeros((2,) + G.vec_shape(p)[1:], dtype=torch.float32, device="cuda")
+        G32.egt_gradient(p, torch.tensor(blk.reshape((2,) + G.vec_shape(o)[1:]), dtype=torch.float32, device="cuda"),
+                         dout)
+        torch.cuda.synchronize()
+        out = dout.double().cpu().numpy().reshape(2, -1)[0]
+        want = pair.sf[0].Ay(v) if p == 0 else pair.sf[0].ATx(v)
+        got = pair.from_product(0, p, out)
+        got[0] = out[:G.H_pad].sum()
+        assert rel_err(got, want) <= 1e-5, (case, p)
+    G32.close()
