@@ -555,6 +555,24 @@ def run_b200(args):
                             precision=args.precision) for sv in ("egt_as", "cfr_plus")]
         if rank == 0:
             line["time_to_gap"] = conv
+        # the whole batch to 10 mbb through solve(): every game until its own eps_sad <= 10 mbb,
+        # solved games stopped on the device (egt_set_target); wall clock of the call
+        solved = {}
+        for sv in ("egt_as", "cfr_plus"):
+            gs = P.Game(P.RIVER, n_games=n, river=spec, boards=boards[:n], prior1=p1[:n], prior2=p2[:n],
+                        precision=args.precision)
+            gs.set_stream(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = P.solve(gs, sv, eps_mbb=10.0, max_iters=args.converge_max_steps)
+            torch.cuda.synchronize()
+            solved[sv] = {"seconds": time.perf_counter() - t0, "iterations": int(res["iters"]),
+                          "max_gap_mbb": float(np.max(res["gap"])) / (spec["big_blind"] / 1000.0)}
+            gs.close()
+        if rank == 0:
+            line["solve_batch_to_10mbb"] = dict(solved, games=n, what="P.solve(..., eps_mbb=10) on the same "
+                                                "games from a cold start (incl. init and mu search): every game "
+                                                "to 10 mbb, solved ones stopped on the device")
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         grads, secs, iters = oracle_sample(args, boards, p1, p2)
