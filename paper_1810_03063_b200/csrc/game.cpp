@@ -383,10 +383,15 @@ static void build_layout(HostGame& G) {
         for (int s = 0; s < L.n_pub; ++s)
             if (L.term_off[s + 1] > L.term_off[s]) L.rows_term.push_back(s);
         L.chunk_off.assign(1, 0);
+        // a tree with at most two chunks' worth of terminals keeps them in one CTA (staging the
+        // tables twice costs more than the second CTA gains); GRAD_CHUNK_MAX_TERMS still bounds it
+        int chunk = grad_chunk_terms(G.n_games);
+        const int n_terms = (int)L.term_idx.size();
+        if (n_terms <= 2 * chunk && n_terms <= GRAD_CHUNK_MAX_TERMS) chunk = n_terms;
         for (int r = 0, n = 0; r < (int)L.rows_term.size(); ++r) {
             const int s = L.rows_term[r];
             n += L.term_off[s + 1] - L.term_off[s];
-            if (n >= grad_chunk_terms(G.n_games) || r + 1 == (int)L.rows_term.size()) {
+            if (n >= chunk || r + 1 == (int)L.rows_term.size()) {
                 L.chunk_off.push_back(r + 1);
                 n = 0;
             }
