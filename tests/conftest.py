@@ -20,6 +20,9 @@ def pytest_collection_modifyitems(config, items):
     except Exception:
         has_gpu = False
     if has_gpu:
+        # the GPU tests call the in-tree library: build it if it is missing or stale (nvcc)
+        from paper_1810_03063_b200 import build
+        build.build()
         return
     skip = pytest.mark.skip(reason="no CUDA device")
     for item in items:
