@@ -39,9 +39,10 @@ class Problem:
         self.grads.n += 1
         return self.sf.Ay(other) if v == 0 else -self.sf.ATx(other)
 
-    def sbr(self, v, other, mu):
-        """(response, value) = argmin/min over own treeplex of <q, grad> + mu d(q)."""
-        return smoothed_best_response(self.tp[v], self.grad(v, other), mu)
+    def sbr(self, v, other, mu, behavioral=False):
+        """(response, value) = argmin/min over own treeplex of <q, grad> + mu d(q)
+        (behavioral=True: also its behavioural strategy and log, see dgf)."""
+        return smoothed_best_response(self.tp[v], self.grad(v, other), mu, behavioral)
 
 
 def smoothed_f(prob, x, mu_y):
@@ -67,6 +68,24 @@ def theory_mu(sf):
     return sf.max_abs_A() / math.sqrt(sf.X.phi * sf.Y.phi)
 
 
+def practical_mu(sf, kmax=30):
+    """Reading R14, "practically-tuned initial choice for the initial smoothing parameters"
+    (PAPER.md:545-547): mu_x = mu_y = theory_mu * 2^-k where k is the last of 0, 1, ..., kmax
+    before the excessive gap condition at the initial point (Alg. 1 / Alg. 3 lines 1-2,
+    PAPER.md:576-578) first fails -- a plain scan, every k evaluated until the first failure.
+    Returns (k, mu)."""
+    mu_th = theory_mu(sf)
+    prob = Problem(sf)
+    k_ok = 0
+    for k in range(kmax + 1):
+        mu = mu_th * 2.0 ** -k
+        x0, y0 = initialize(prob, mu, mu)
+        if excessive_gap(prob, x0, y0, mu, mu) < 0:
+            break
+        k_ok = k
+    return k_ok, mu_th * 2.0 ** -k_ok
+
+
 def initialize(prob, mu_x, mu_y):
     """Algorithm 1 lines 1-2, reading R4:
     x_omega = the DGF centre (uniform behavioural strategy, d = 0);
@@ -87,15 +106,16 @@ def _step(prob, v, mu, mu_other, p, o, tau):
              = prox at centre p_mu(o) of the gradient  s * grad f(p_hat),  s = tau / ((1 - tau) mu)
       p_plus = (1 - tau) p + tau p_til
       mu_plus = (1 - tau) mu
-    grad f(p_hat) = (view-v gradient at o_mu(p_hat))."""
+    grad f(p_hat) = (view-v gradient at o_mu(p_hat)).  The prox centre p_mu(o) enters
+    through its behavioural log-probabilities (reading R16)."""
     w = 1 - v
-    p_mu, _ = prob.sbr(v, o, mu)
+    p_mu, _, _, p_mu_lb = prob.sbr(v, o, mu, behavioral=True)
     p_hat = (1 - tau) * p + tau * p_mu
     o_mu_hat, _ = prob.sbr(w, p_hat, mu_other)
     o_plus = (1 - tau) * o + tau * o_mu_hat
     grad_f = prob.grad(v, o_mu_hat)
     s = tau / ((1 - tau) * mu)
-    p_til = prox_mapping(prob.tp[v], s * grad_f, p_mu)
+    p_til = prox_mapping(prob.tp[v], s * grad_f, lb_prev=p_mu_lb)
     p_plus = (1 - tau) * p + tau * p_til
     return (1 - tau) * mu, p_plus, o_plus
 
@@ -150,6 +170,8 @@ def run(sf, variant, iters, mu=None, record=None):
     prob = Problem(sf)
     if mu is None:
         mu = theory_mu(sf)
+    elif isinstance(mu, str) and mu == "practical":
+        mu = practical_mu(sf)[1]
     mu_x, mu_y = (mu, mu) if np.isscalar(mu) else mu
     x, y = initialize(prob, mu_x, mu_y)
     st = EGTState(x, y, mu_x, mu_y)

@@ -177,6 +177,39 @@ def test_river_tiny_tree_matches_hand_enumeration():
     assert nodes[0] == g["p1_nodes"] and nodes[1] == g["p2_nodes"]
 
 
+def test_libratus_raise_chains_match_hand_enumeration():
+    """Deep raise chains of the Libratus abstraction: every context incl. the "subsequent
+    raises" lists of both players at the nodes of two chains, with the bet
+    totals and payoffs derived by hand (tests/golden/river_libratus_raise_chains.json)."""
+    g = json.load(open(os.path.join(GOLD, "river_libratus_raise_chains.json")))
+    spec = workloads.river_spec("libratus")
+    rp = river.RiverParams(**{k: spec[k] for k in ("pot", "stack", "fracs", "allin", "raise_cap", "open_fold")})
+    tree = river.betting_tree(rp)
+    by_hist = {}
+
+    def rec(n):
+        by_hist[n.history] = n
+        for _, c in n.children:
+            rec(c)
+    rec(tree)
+    seen = set()
+    for chain in g["chains"]:
+        for nd in chain["nodes"]:
+            n = by_hist[nd["history"]]
+            assert n.kind == "decision" and n.player == nd["player"] - 1
+            assert [t for t, _ in n.children] == nd["children"], nd["history"]
+            seen.add(river.context(n.player, nd["history"].count("b")))
+            assert river.context(n.player, nd["history"].count("b")) == nd["context"]
+        for tm in chain["terminals"]:
+            n = by_hist[tm["history"]]
+            assert n.kind == "terminal"
+            if "fold_by" in tm:
+                assert n.fold_by == tm["fold_by"] - 1 and n.payoff_fold_to_p1 == tm["payoff_to_p1"]
+            else:
+                assert n.showdown_amount == tm["showdown_amount"]
+    assert seen == set(river.CONTEXTS)
+
+
 def test_libratus_abstraction_size():
     """Endgame-2-shaped tree: same order as the paper's 140k/144k dims and 176M
     leaves (the paper prunes zero-probability hands)."""

@@ -194,3 +194,42 @@ def test_cfr_plus_bound():
         if T in (1, 3, 10, 30, 100, 300, 1000):
             gap = br.saddle_gap(sf, st.xbar, st.ybar)
             assert gap <= 2 * cfr.cfr_plus_regret_bound(sf, T, L)
+
+
+# ----------------------------------------------------------------- practical mu (reading R14)
+@pytest.mark.parametrize("name", ["kuhn", "leduc", "pennies"])
+def test_practical_mu_scan(name):
+    """The scan returns the last k before the EGC at the initial point first fails: the EGC
+    holds at mu_theory * 2^-j for every j <= k (Nesterov's theorem covers j = 0,
+    PAPER.md:363-371) and fails at k + 1 (unless k is the cap)."""
+    sf = {"kuhn": kuhn, "pennies": pennies, "leduc": lambda: seqform.build(games.leduc())}[name]()
+    k, mu = egt.practical_mu(sf, kmax=30)
+    mu_th = egt.theory_mu(sf)
+    assert mu == mu_th * 2.0 ** -k
+    prob = egt.Problem(sf)
+    for j in range(k + 2):
+        if j > 30:
+            break
+        m = mu_th * 2.0 ** -j
+        x0, y0 = egt.initialize(prob, m, m)
+        assert sf.X.check_feasible(x0) and sf.Y.check_feasible(y0)
+        egv = egt.excessive_gap(prob, x0, y0, m, m)
+        assert (egv >= 0) == (j <= k), (j, egv)
+
+
+def test_egt_as_from_practical_mu_keeps_egc_and_converges():
+    """EGT/as (Alg. 3-4) from the practical mu on Kuhn: every accepted iterate satisfies the
+    EGC, eps_sad <= mu_x Omega_X + mu_y Omega_Y, and it approaches -1/18."""
+    sf = kuhn()
+    k, mu = egt.practical_mu(sf)
+    assert k >= 1
+    prob = egt.Problem(sf)
+    x, y = egt.initialize(prob, mu, mu)
+    st = egt.EGTState(x, y, mu, mu)
+    for _ in range(400):
+        egt.egt_iteration(prob, st, "as")
+        assert egt.excessive_gap(prob, st.x, st.y, st.mu_x, st.mu_y) >= 0
+        gap = br.saddle_gap(sf, st.x, st.y)
+        assert -1e-12 <= gap <= st.mu_x * sf.X.Omega + st.mu_y * sf.Y.Omega + 1e-12
+    assert br.saddle_gap(sf, st.x, st.y) < 2e-3
+    assert abs(-(st.x @ (sf.A @ st.y)) - (-1 / 18)) < 2e-3
