@@ -62,11 +62,13 @@ def parse():
     ap.add_argument("--no-f32", action="store_true", help="skip the extra fp32-mode measurement")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="f32: the optional fp32 mode (fp32 vectors and arithmetic, DESIGN.md row 9)")
-    ap.add_argument("--fused", action="store_true",
-                    help="with --shard: fused compute + all-gather over peer memory instead of the all-reduce")
+    ap.add_argument("--allreduce", action="store_true",
+                    help="with --shard: one in-place NCCL all-reduce per gradient instead of the fused "
+                         "compute + all-gather over peer memory")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: every rank holds the same batch and computes a slice of each "
-                         "gradient's rows, NCCL all-reduce per gradient (DESIGN.md row 8)")
+                         "gradient's rows; each row is stored into every rank's buffer over NVLink by the "
+                         "kernel that finishes it (fused all-gather, DESIGN.md row 8)")
     return ap.parse_args()
 
 
@@ -104,8 +106,13 @@ def throughput(games_per_rank, world, steps, ms, shard=False):
 def time_to_gap(P, spec, boards, p1, p2, solver, eps_mbb, max_steps, check_every=10, precision="f64"):
     """Device time (CUDA events) until the median game of the batch reaches eps_sad <= each
     target in eps_mbb (sum of regrets in milli-big-blinds, 1 mbb = big blind
-    / 1000 chips): graph-launched solver steps, eps_sad on the device after each step, read
-    back every `check_every` steps (an event is recorded at every check)."""
+    / 1000 chips): graph-launched solver steps; every `check_every` steps eps_sad is evaluated
+    on the device and read back.  Both solvers are checked the same way and the check is timed
+    apart from the solver: "seconds" is the solver's own device time (events around each block
+    of steps), "seconds_with_checks" adds the eps_sad evaluations (EGT/as keeps its gap
+    current at no gradient cost; CFR+'s average needs 2 gradients + 2 best responses).
+    grad_evals_per_game counts each solver's own gradients: 4 per EGT/as attempt, 2 per CFR+
+    iteration, not the checks."""
     import torch
     n = len(boards)
     game = P.Game(P.RIVER, n_games=n, river=spec, boards=boards, prior1=p1, prior2=p2, precision=precision)
@@ -114,41 +121,44 @@ def time_to_gap(P, spec, boards, p1, p2, solver, eps_mbb, max_steps, check_every
     gap = torch.zeros(n, dtype=torch.float64, device="cuda")
     if solver == "egt_as":
         game.egt_init(P.EGT_AS)
-        step = lambda: game.egt_step(1)  # noqa: E731
-        which = 0
+        step = game.egt_step
+        which, per_step = 0, 4
     else:
         game.cfr_init(P.CFR_PLUS)
-        step = lambda: game.cfr_step(1)  # noqa: E731
-        which = 1
+        step = game.cfr_step
+        which, per_step = 1, 2
     mbb = spec["big_blind"] / 1000.0
     targets = sorted(eps_mbb, reverse=True)
     torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev0.record(st)
-    checks = []  # (steps, event, median gap, max gap)
+    checks = []  # (steps, solver seconds so far, solver+check seconds so far, median gap, max gap)
+    solver_s = total_s = 0.0
     steps = 0
     while steps < max_steps:
-        for _ in range(check_every):
-            step()
-            game.saddle_gap_device(which, gap)
-            steps += 1
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record(st)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(st)
+        step(check_every)
+        steps += check_every
+        e1.record(st)
+        game.saddle_gap_device(which, gap)
+        e2.record(st)
         g = gap.cpu().numpy()
-        checks.append((steps, ev, float(np.median(g)), float(np.max(g))))
-        if checks[-1][2] <= targets[-1] * mbb:  # the median game reached the last target
+        solver_s += e0.elapsed_time(e1) / 1e3
+        total_s += e0.elapsed_time(e2) / 1e3
+        checks.append((steps, solver_s, total_s, float(np.median(g)), float(np.max(g))))
+        if checks[-1][3] <= targets[-1] * mbb:  # the median game reached the last target
             break
-    torch.cuda.synchronize()
-    sc = game.egt_scalars()
     game.close()
+    last = checks[-1]
     out = {"solver": solver, "games": n, "precision": precision, "steps_run": steps,
-           "seconds_run": ev0.elapsed_time(checks[-1][1]) / 1e3,
-           "final_gap_mbb": {"median": checks[-1][2] / mbb, "max": checks[-1][3] / mbb},
-           "grad_evals_per_game": float(sc[0, 7]), "to_eps": []}
+           "seconds_run": last[1], "seconds_run_with_checks": last[2], "check_every": check_every,
+           "final_gap_mbb": {"median": last[3] / mbb, "max": last[4] / mbb},
+           "grad_evals_per_game": per_step * steps, "to_eps": []}
     for e in targets:
-        hit = next((c for c in checks if c[2] <= e * mbb), None)
+        hit = next((c for c in checks if c[3] <= e * mbb), None)
         out["to_eps"].append({"eps_mbb": e, "median_game_steps": hit[0] if hit else None,
-                              "seconds": ev0.elapsed_time(hit[1]) / 1e3 if hit else None})
+                              "grad_evals_per_game": per_step * hit[0] if hit else None,
+                              "seconds": hit[1] if hit else None,
+                              "seconds_with_checks": hit[2] if hit else None})
     return out
 
 
@@ -157,8 +167,10 @@ def workload_config(args, game=None, world=1):
            "games_per_gpu": args.batch, "global_games": args.batch * world,
            "solver": "EGT/as (dilated entropy) + eps_sad per step", "pot": 2100, "stack": 18950,
            "bet_abstraction": "PAPER.md:673-685" if args.workload == "libratus" else "{0.5,1,all-in}",
-           "parallelism": ("shard%d (one batch; each gradient's terminal rows split over ranks, NCCL "
-                           "all-reduce per gradient)" % world) if getattr(args, "shard", False) else
+           "parallelism": ("shard%d (one batch; each gradient's terminal rows split over ranks, %s)"
+                           % (world, "NCCL all-reduce per gradient" if getattr(args, "allreduce", False)
+                              else "rows stored into every rank's buffer by the kernel (fused all-gather)"))
+                          if getattr(args, "shard", False) else
                           "dp%d (independent endgames per rank)" % world}
     if game is not None:
         cfg.update({"hands_per_player": game.H, "pub_seqs": list(game.n_pub),
@@ -297,6 +309,14 @@ def oracle_sample(args, boards, p1, p2, budget_s=20.0, max_iters=None):
     return grads, time.perf_counter() - t0, iters
 
 
+def host_cores():
+    """Cores this process may run on (the oracle's host threads can use at most these)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def host_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -338,12 +358,15 @@ def run_reference(args):
     el = time.perf_counter() - t0
     grads = prob.grads.n - g0
     v = grads / el
-    cores = host_threads()
-    sample = "1 endgame (game 0 of rank 0's batch), %d EGT/as iterations + eps_sad, fp64 numpy" % args.steps
+    cores = host_cores()
+    sample = ("1 endgame (game 0 of rank 0's %d-game batch) per step: %d EGT/as iterations + eps_sad, fp64 numpy "
+              "(BLAS threads %d)" % (args.batch, args.steps, host_threads()))
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": workload_config(args, None, 1),
+            "impl": "reference", "config": dict(workload_config(args, None, 1),
+                                                reference_sample="1 of the %d endgames per step (bounded CPU sample)"
+                                                                 % args.batch),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -375,7 +398,7 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     game.set_stream(stream)
     if args.shard:
-        if args.fused and world > 1:
+        if not args.allreduce and world > 1:
             game.shard_fused(rank, world)
         else:
             game.shard(rank, world)
@@ -475,7 +498,10 @@ def run_b200(args):
                     precision=args.precision)
         t_load = time.perf_counter()
         if args.shard:
-            g2.shard(rank, world)
+            if not args.allreduce and world > 1:
+                g2.shard_fused(rank, world)
+            else:
+                g2.shard(rank, world)
         g2.egt_init(P.EGT_AS)
         torch.cuda.synchronize()
         t_init = time.perf_counter()
@@ -576,7 +602,8 @@ def run_b200(args):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         grads, secs, iters = oracle_sample(args, boards, p1, p2)
-        line["cpu_baseline"] = {"value": grads / secs, "unit": UNIT, "cores": host_threads(), "kind": "oracle",
+        line["cpu_baseline"] = {"value": grads / secs, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+                                "blas_threads": host_threads(),
                                 "sample": "1 endgame (game 0), oracle EGT/as initial point + %d iterations "
                                           "each with eps_sad (%d gradient evals, %.1f s)" % (iters, grads, secs)}
     if rank == 0:

@@ -61,6 +61,7 @@ EXPORTS = [
     "get_strategy_device", "egt_scalars", "egt_last_error", "saddle_gap_device",
     "egt_timing", "egt_timing_get", "egt_nccl_unique_id", "egt_shard", "egt_gradient_rows",
     "egt_ipc_handles", "egt_shard_peers", "egt_gradient_rows_to", "egt_pool_trim", "egt_set_target",
+    "egt_shard_emulate",
 ]
 IPC_HANDLE_BYTES = 64
 KERNEL_KINDS = ("grad_Ay", "grad_ATx", "tree", "scalar", "comm")
@@ -91,7 +92,7 @@ def load_library():
         "egt_hand_cards": ([P, I32, ctypes.POINTER(I32)], I32),
         "egt_pub_history": ([P, I32, I32, ctypes.c_char_p, I32], I32),
         "egt_gradient": ([P, I32, VP, VP], I32),
-        "egt_smoothed_br": ([P, I32, VP, D, VP, VP, VP, VP], I32),
+        "egt_smoothed_br": ([P, I32, VP, D, VP, VP, VP, VP, VP], I32),
         "egt_prox": ([P, I32, VP, D, VP, VP, VP], I32),
         "egt_best_response": ([P, I32, VP, D, VP], I32),
         "egt_init": ([P, I32, D, D], I32),
@@ -114,6 +115,7 @@ def load_library():
         "egt_ipc_handles": ([P, ctypes.c_char_p], I32),
         "egt_shard_peers": ([P, ctypes.c_char_p], I32),
         "egt_gradient_rows_to": ([P, I32, I32, I32, VP, ctypes.POINTER(ctypes.c_uint64), I32], I32),
+        "egt_shard_emulate": ([P, I32, I32], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -237,12 +239,13 @@ class Game:
     def egt_gradient(self, player, din, dout):
         _check(self._L.egt_gradient(self._h, player, _ptr(din), _ptr(dout)))
 
-    def egt_smoothed_br(self, player, g, gsign, mu, q=None, b=None, value=None):
+    def egt_smoothed_br(self, player, g, gsign, mu, q=None, b=None, value=None, lb=None):
         _check(self._L.egt_smoothed_br(self._h, player, _ptr(g), float(gsign), _ptr(mu),
-                                       _ptr(q), _ptr(b), _ptr(value)))
+                                       _ptr(q), _ptr(b), _ptr(lb), _ptr(value)))
 
-    def egt_prox(self, player, g, gsign, step, center_b, q):
-        _check(self._L.egt_prox(self._h, player, _ptr(g), float(gsign), _ptr(step), _ptr(center_b), _ptr(q)))
+    def egt_prox(self, player, g, gsign, step, center_lb, q):
+        """center_lb: the centre's behavioural strategy as natural logs (R16)."""
+        _check(self._L.egt_prox(self._h, player, _ptr(g), float(gsign), _ptr(step), _ptr(center_lb), _ptr(q)))
 
     def egt_best_response(self, player, g, gsign, value):
         _check(self._L.egt_best_response(self._h, player, _ptr(g), float(gsign), _ptr(value)))
@@ -292,6 +295,10 @@ class Game:
             uid = broadcast_uid(nccl_unique_id() if rank == 0 else None)
         buf = None if uid is None else ctypes.create_string_buffer(bytes(uid), NCCL_ID_BYTES)
         _check(self._L.egt_shard(self._h, rank, world, buf))
+
+    def shard_emulate(self, world, fused=False):
+        """Emulate `world` ranks on this device (egt_shard_emulate; tests)."""
+        _check(self._L.egt_shard_emulate(self._h, world, int(bool(fused))))
 
     def gradient_rows_to(self, player, rank, world, din, dsts):
         """Shard `rank`'s rows stored into every buffer of dsts (the fused all-gather's stores)."""

@@ -66,6 +66,16 @@ struct egt_game {
     DevPeers peers[2];
     std::vector<void*> ipc_opened;
     double* barrier_word = nullptr;
+    // rows [shard_lo[p], shard_hi[p]] of player p's gradient hold this rank's slice; with the
+    // NCCL all-reduce every other row is zeroed before each sharded gradient (the previous
+    // all-reduce left the full gradient there)
+    int shard_lo[2] = {0, 0}, shard_hi[2] = {0, 0};
+    // emulated ranks on one device (egt_shard_emulate, tests): every rank's slice kernel runs
+    // into its own buffer and the collective is a local kernel over the `emu_world` buffers
+    int emu_world = 0, emu_fused = 0;
+    std::vector<DevPlayer> emu_dp[2];
+    std::vector<double*> emu_buf[2];   // [0] is GR[p]
+    double** emu_ptrs[2] = {nullptr, nullptr};  // device copy of emu_buf
     int esz = 8;                    // bytes per vector element (8: fp64, 4: fp32 mode)
     std::vector<void*> allocs;
     std::vector<void*> pool_allocs;  // stream-ordered allocations from the library pool (lib_pool)
@@ -91,7 +101,7 @@ struct egt_game {
     double* gapout = nullptr;       // [G]
     double* gapcur = nullptr;       // [G] eps_sad of the current EGT/as iterate (maintained)
     double* S[2] = {nullptr, nullptr};   // EGT state, 2 slots
-    double* C[2] = {nullptr, nullptr};   // EGT cache (behavioural smoothed BR), 2 slots
+    double* C[2] = {nullptr, nullptr};   // EGT cache (smoothed BR as behavioural logs, R16), 2 slots
     double* HAT[2] = {nullptr, nullptr};
     double* RESP[2] = {nullptr, nullptr};
     double* GR[2] = {nullptr, nullptr};
@@ -333,6 +343,33 @@ static int make_slice(egt_game* G, int p, int rank, int world, DevPlayer& out, s
     return 0;
 }
 
+// sequence bounds [lo, hi] of a slice's rows (lo > hi: the slice is empty)
+static void slice_bounds(const egt_game* G, int p, const DevPlayer& P, int& lo, int& hi) {
+    const PlayerLayout& L = G->host.pl[p];
+    const int r0 = (int)(P.rows_term - G->dp_full[p].rows_term);
+    if (P.n_rows_term == 0) {
+        lo = L.n_pub;
+        hi = L.n_pub - 1;
+        return;
+    }
+    lo = L.rows_term[r0];
+    hi = L.rows_term[r0 + P.n_rows_term - 1];
+}
+
+// zero every row of a gradient buffer outside [lo, hi] (all games): before a sharded
+// gradient whose result is summed over the ranks
+static cudaError_t zero_outside(const egt_game* G, int p, double* base, int lo, int hi, cudaStream_t st) {
+    const size_t es = (size_t)G->esz, Hp = (size_t)G->host.H_pad, pitch = es * (size_t)G->V[p];
+    const int np = G->host.pl[p].n_pub, Gn = G->host.n_games;
+    cudaError_t e = cudaSuccess;
+    if (lo > 0) e = cudaMemset2DAsync(base, pitch, 0, es * Hp * (size_t)std::min(lo, np), Gn, st);
+    if (e == cudaSuccess && hi + 1 < np && hi + 1 >= 0) {
+        char* b = reinterpret_cast<char*>(base) + es * Hp * (size_t)(hi + 1);
+        e = cudaMemset2DAsync(b, pitch, 0, es * Hp * (size_t)(np - hi - 1), Gn, st);
+    }
+    return e;
+}
+
 // ----------------------------------------------------------------------------- load
 extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     if (!spec || !out) return fail(EGT_E_ARG, "null argument");
@@ -399,6 +436,25 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(upload(G, &d_cent, cent));
     TRY(upload(G, &d_pcard, pcard));
     TRY(upload(G, &d_valid, valid));
+    // the card-domain gradient kernel's per-board plans (river games, one board state)
+    bool plans = nbs == 1;
+    for (const BoardTable& tb : H.tables) plans = plans && !tb.plan.pw.empty();
+    if (plans) {
+        std::vector<uint32_t> pw, pr, ln;
+        for (const BoardTable& tb : H.tables) {
+            pw.insert(pw.end(), tb.plan.pw.begin(), tb.plan.pw.end());
+            pr.insert(pr.end(), tb.plan.pr.begin(), tb.plan.pr.end());
+            ln.insert(ln.end(), tb.plan.lane.begin(), tb.plan.lane.end());
+        }
+        uint32_t *d_pw, *d_pr, *d_ln;
+        TRY(upload(G, &d_pw, pw));
+        TRY(upload(G, &d_pr, pr));
+        TRY(upload(G, &d_ln, ln));
+        G->dg.card_pw = d_pw;
+        G->dg.card_pr = d_pr;
+        G->dg.card_lane = d_ln;
+    }
+    G->dg.card_plan = plans ? 1 : 0;
     double *d_p0, *d_p1, *d_kg;
     if (G->esz == 8) {
         TRY(upload(G, &d_p0, H.prior[0]));
@@ -796,6 +852,7 @@ extern "C" int egt_shard(egt_game* G, int32_t rank, int32_t world, const uint8_t
     for (int p = 0; p < 2; ++p) {
         int r = make_slice(G, p, rank, world, G->dp[p], G->allocs);
         if (r) return r;
+        slice_bounds(G, p, G->dp[p], G->shard_lo[p], G->shard_hi[p]);
     }
     if (id) {  // world == 1 with an id still builds a (1-rank) communicator: the same path
         std::string err;
@@ -816,7 +873,7 @@ extern "C" int egt_shard(egt_game* G, int32_t rank, int32_t world, const uint8_t
 static TreeArgs base_args() { return TreeArgs(); }
 
 extern "C" int egt_smoothed_br(egt_game* G, int32_t player, const double* dg, double gsign, const double* dmu,
-                               double* dq, double* db, double* dval) {
+                               double* dq, double* db, double* dlb, double* dval) {
     if (!G || !dg || !dmu || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
     TreeArgs A = base_args();
     A.mode = TM_SBR;
@@ -825,6 +882,7 @@ extern "C" int egt_smoothed_br(egt_game* G, int32_t player, const double* dg, do
     A.mu = dmu;
     if (dq) A.out_q = vec(dq, G->V[player]);
     if (db) A.out_b = vec(db, G->V[player]);
+    if (dlb) A.out_lb = vec(dlb, G->V[player]);
     A.value = dval;
     A.partial = G->partial;
     A.counter = G->counter;
@@ -834,14 +892,14 @@ extern "C" int egt_smoothed_br(egt_game* G, int32_t player, const double* dg, do
 }
 
 extern "C" int egt_prox(egt_game* G, int32_t player, const double* dg, double gsign, const double* dstep,
-                        const double* dcenter_b, double* dq) {
-    if (!G || !dg || !dstep || !dcenter_b || !dq || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
+                        const double* dcenter_lb, double* dq) {
+    if (!G || !dg || !dstep || !dcenter_lb || !dq || player < 0 || player > 1) return fail(EGT_E_ARG, "bad argument");
     TreeArgs A = base_args();
     A.mode = TM_PROX;
     A.g = vec(const_cast<double*>(dg), G->V[player]);
     A.gsign = gsign;
     A.mu = dstep;
-    A.center = vec(const_cast<double*>(dcenter_b), G->V[player]);
+    A.center = vec(const_cast<double*>(dcenter_lb), G->V[player]);
     A.out_q = vec(dq, G->V[player]);
     if (begin(G)) return EGT_E_CUDA;
     CK(launch_tree(G->dg, G->dp[player], player, A, G->st));
@@ -993,16 +1051,96 @@ static cudaError_t peer_barrier(egt_game* G) {
     });
 }
 
-static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0) {
-    const bool fused = G->p2p && out.base == G->GR[p] && !out.slot_sel;
+static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask, int want, int all_rows);
+
+// One gradient of the solver.  Sharded (egt_shard), this rank computes its slice of the rows:
+//  * fused all-gather (egt_shard_peers): the kernel stores its rows into every rank's buffer;
+//    a peer barrier BEFORE the launch orders those stores after every rank's last read of
+//    the buffer (the previous gradient's consumers), one AFTER it makes every rank's rows
+//    visible before anyone reads them -- correct by construction whatever the launch order;
+//  * NCCL all-reduce: the rows outside the slice are zeroed first (they hold the previous
+//    gradient's sum), so the in-place sum adds exact zeros to every other rank's rows.
+// all_rows: every row is written (rows no terminal ends are 0), for buffers that are not
+// the solver's gradient buffers.
+static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0,
+                        int all_rows = 0) {
+    if (G->emu_world > 1) return emu_grad(G, p, in, out, mask, want, all_rows);
+    const bool fused = G->p2p && out.base == G->GR[p] && !out.slot_sel && !all_rows;
+    if (fused) {
+        cudaError_t e = peer_barrier(G);
+        if (e != cudaSuccess) return e;
+    } else if (G->comm && !all_rows) {
+        cudaError_t e = zero_outside(G, p, out.base, G->shard_lo[p], G->shard_hi[p], G->st);
+        if (e != cudaSuccess) return e;
+    }
     cudaError_t e = timed(
         G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
         [&] {
-            return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, 0, G->st, fused ? &G->peers[p] : nullptr);
+            return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, all_rows, G->st,
+                                   fused ? &G->peers[p] : nullptr);
         },
         G->timing ? grad_bytes_per_game(G, p) : 0.0);
     if (e != cudaSuccess) return e;
     return fused ? peer_barrier(G) : allreduce_grad(G, p, out);
+}
+
+// Emulated ranks (egt_shard_emulate): rank r's slice kernel writes buffer r (rank 0's is the
+// solver's output) exactly as on rank r; the collective is a local kernel over the buffers.
+static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask, int want, int all_rows) {
+    const int W = G->emu_world;
+    if (all_rows || out.slot_sel || out.base != G->GR[p]) {  // not a solver gradient buffer: unsharded
+        return launch_gradient(G->dg, G->dp_full[p], p, in, out, mask, want, all_rows, G->st, nullptr);
+    }
+    cudaError_t e = cudaSuccess;
+    for (int r = 0; r < W && e == cudaSuccess; ++r) {
+        const DevPlayer& P = G->emu_dp[p][r];
+        VecRef o = out;
+        o.base = G->emu_buf[p][r];
+        if (G->emu_fused) {
+            DevPeers pr;
+            pr.n = W;
+            for (int d = 0; d < W; ++d) pr.base[d] = G->emu_buf[p][d];
+            e = launch_gradient(G->dg, P, p, in, o, mask, want, 0, G->st, &pr);
+        } else {
+            int lo, hi;
+            slice_bounds(G, p, P, lo, hi);
+            e = zero_outside(G, p, o.base, lo, hi, G->st);
+            if (e == cudaSuccess) e = launch_gradient(G->dg, P, p, in, o, mask, want, 0, G->st, nullptr);
+        }
+    }
+    if (e == cudaSuccess && !G->emu_fused)
+        e = launch_emu_allreduce(G->emu_ptrs[p], W, (size_t)G->host.n_games * G->V[p], G->esz, G->st);
+    return e;
+}
+
+extern "C" int egt_shard_emulate(egt_game* G, int32_t world, int32_t fused) {
+    if (!G || world < 1 || world > EGT_MAX_PEERS) return fail(EGT_E_ARG, "bad argument");
+    if (G->solver != SOLVER_NONE) return fail(EGT_E_STATE, "egt_shard_emulate must precede egt_init / cfr_init");
+    if (G->comm || G->p2p) return fail(EGT_E_STATE, "game is already sharded over real ranks");
+    G->emu_world = world > 1 ? world : 0;
+    G->emu_fused = fused != 0;
+    for (int p = 0; p < 2; ++p) {
+        G->emu_dp[p].assign(world, DevPlayer());
+        G->emu_buf[p].assign(world, nullptr);
+        G->emu_buf[p][0] = G->GR[p];
+        for (int r = 0; r < world; ++r) {
+            int rc = make_slice(G, p, r, world, G->emu_dp[p][r], G->allocs);
+            if (rc) return rc;
+            if (r > 0) {
+                const size_t n = (size_t)G->host.n_games * G->V[p];
+                if (dalloc_vec(G, &G->emu_buf[p][r], n)) return EGT_E_CUDA;
+                CK(cudaMemsetAsync(G->emu_buf[p][r], 0, n * G->esz, G->st));
+            }
+        }
+        if (!G->emu_ptrs[p] && dalloc(G, &G->emu_ptrs[p], (size_t)EGT_MAX_PEERS)) return EGT_E_CUDA;
+        CK(cudaMemcpyAsync(G->emu_ptrs[p], G->emu_buf[p].data(), sizeof(double*) * world, cudaMemcpyHostToDevice, G->st));
+    }
+    CK(cudaStreamSynchronize(G->st));
+    if (G->graph) {
+        cudaGraphExecDestroy(G->graph);
+        G->graph = nullptr;
+    }
+    return 0;
 }
 template <class F>
 static cudaError_t scalar_k(egt_game* G, F&& launch) {
@@ -1018,14 +1156,16 @@ static int egt_omega_gradient(egt_game* G, double* out) {
     U.mode = TM_UNIFORM;
     U.out_q = vec(G->HAT[0], G->V[0]);
     CK(tree(G, 0, U));
-    CK(grad(G, 1, vec(G->HAT[0], G->V[0]), vec(out, G->V[1])));
+    // every row written: `out` is scratch whose terminal-free rows would otherwise be stale
+    CK(grad(G, 1, vec(G->HAT[0], G->V[0]), vec(out, G->V[1]), nullptr, 0, 1));
     return 0;
 }
 
 // Alg. 1 / 3 initialisation at the current mu: y0 = y_mu(x_omega), x0 = x_mu(y0) (cache C[0]),
 // y_mu(x0) (cache C[1]) and the values the excessive-gap check needs.  g_omega: A^T x_omega
-// already evaluated (the mu search), or nullptr to evaluate it here.
-static int egt_initial_point(egt_game* G, double* g_omega) {
+// already evaluated (the mu search), or nullptr to evaluate it here.  mask: only the games
+// with mask[g] == 1 (the mu scan's games still scanning), or nullptr for all.
+static int egt_initial_point(egt_game* G, double* g_omega, const int* mask = nullptr) {
     const int Gn = G->host.n_games;
     DevScalars& S = G->sc;
     if (!g_omega) {
@@ -1039,31 +1179,37 @@ static int egt_initial_point(egt_game* G, double* g_omega) {
     A.gsign = GSIGN[1];
     A.mu = S.mu + Gn;
     A.out_q = slot2(G, G->S[1], 1, 0);
+    A.mask = mask;
+    A.want = 1;
     CK(tree(G, 1, A));
     // x0 = x_{mu_x}(y0) (also the cache C[0]); phi_{mu_x}(y0)
-    CK(grad(G, 0, slot2(G, G->S[1], 1, 0), vec(G->GR[0], G->V[0])));
+    CK(grad(G, 0, slot2(G, G->S[1], 1, 0), vec(G->GR[0], G->V[0]), mask, 1));
     A = base_args();
     A.mode = TM_SBR;
     A.g = vec(G->GR[0], G->V[0]);
     A.gsign = GSIGN[0];
     A.mu = S.mu;
     A.out_q = slot2(G, G->S[0], 0, 0);
-    A.out_b = slot2(G, G->C[0], 0, 0);
+    A.out_lb = slot2(G, G->C[0], 0, 0);
     A.value = S.val;
     A.partial = G->partial;
     A.counter = G->counter;
+    A.mask = mask;
+    A.want = 1;
     CK(tree(G, 0, A));
     // y_{mu_y}(x0) (cache C[1]) and -f_{mu_y}(x0)
-    CK(grad(G, 1, slot2(G, G->S[0], 0, 0), vec(G->GR[1], G->V[1])));
+    CK(grad(G, 1, slot2(G, G->S[0], 0, 0), vec(G->GR[1], G->V[1]), mask, 1));
     A = base_args();
     A.mode = TM_SBR;
     A.g = vec(G->GR[1], G->V[1]);
     A.gsign = GSIGN[1];
     A.mu = S.mu + Gn;
-    A.out_b = slot2(G, G->C[1], 1, 0);
+    A.out_lb = slot2(G, G->C[1], 1, 0);
     A.value = S.val + Gn;
     A.partial = G->partial;
     A.counter = G->counter;
+    A.mask = mask;
+    A.want = 1;
     CK(tree(G, 1, A));
     return 0;
 }
@@ -1083,7 +1229,7 @@ static int record_egt_iteration(egt_game* G) {
     // player), so in graph mode player 2's chain runs on the second stream beside player 1's:
     // the half-empty masked launches of one chain fill the SMs the other leaves idle.  Not in
     // timing mode (per-kernel events) and not when sharded (one all-reduce order on all ranks).
-    const bool fork_focus = !G->timing && !G->comm;
+    const bool fork_focus = !G->timing && !G->comm && !G->emu_world;
     cudaStream_t main_st = G->st;
     struct Restore {  // G->st is the main stream again on every exit path
         egt_game* g;
@@ -1105,7 +1251,7 @@ static int record_egt_iteration(egt_game* G) {
             A.g = vec(G->GR[p], G->V[p]);
             A.gsign = GSIGN[p];
             A.mu = S.mu + (size_t)p * Gn;
-            A.out_b = slot2(G, G->C[p], p, 0);
+            A.out_lb = slot2(G, G->C[p], p, 0);
             A.mask = S.focus;
             A.want = p;
             CK(tree(G, p, A));
@@ -1160,7 +1306,7 @@ static int record_egt_iteration(egt_game* G) {
         // gradients A y+ and A^T x+.  The two players' chains are independent: in graph mode
         // player 1's runs on a second stream (own reduction scratch) beside player 0's -- not
         // when sharded, where both chains' all-reduces must keep one order on every rank.
-        const bool fork = !G->timing && !G->comm;
+        const bool fork = !G->timing && !G->comm && !G->emu_world;
         if (fork) {
             CK(cudaEventRecord(G->ev_fork, main_st));
             CK(cudaStreamWaitEvent(G->st2, G->ev_fork, 0));
@@ -1182,7 +1328,7 @@ static int record_egt_iteration(egt_game* G) {
                 A.g = vec(G->GR[p], G->V[p]);
                 A.gsign = GSIGN[p];
                 A.mu = S.mu_cand + (size_t)p * Gn;
-                A.out_b = slot2(G, G->C[p], p, 1);
+                A.out_lb = slot2(G, G->C[p], p, 1);
                 A.value = S.val + (size_t)p * Gn;
                 A.partial = partial;
                 A.counter = counter;
@@ -1274,40 +1420,45 @@ extern "C" int egt_init(egt_game* G, int32_t variant, double mu_x, double mu_y) 
     CK(cudaMemcpyAsync(G->sc.mu, mu.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
     G->grads = 0;
     if (!given && variant != EGT_THEORY) {
-        // DESIGN.md R14: the smallest mu = mu_theory * 2^-k, k in [0, 30], whose initial point
-        // satisfies the EGC, by bisection over k per game (the EGC holds at k = 0, the theory mu)
-        std::vector<int> lo(Gn, 0), hi(Gn, 30), mid(Gn, 0);
-        std::vector<double> chosen(mu), trial(mu);
-        std::vector<double> vals(2 * (size_t)Gn);
+        // DESIGN.md R14: mu = mu_theory * 2^-k with k the last of 0, 1, ..., 30 before the EGC
+        // at the initial point first fails -- a plain scan, every k evaluated in turn (no
+        // monotonicity assumed).  One round per k on the device for the games still scanning
+        // (masked launches: a game that failed costs nothing more); the host looks at the
+        // scan flags every few rounds to stop early.  A^T x_omega, independent of mu, once.
+        int *scan = nullptr, *kbest = nullptr;
+        double* mth_d = nullptr;
+        if (dalloc(G, &scan, (size_t)Gn) || dalloc(G, &kbest, (size_t)Gn) || dalloc(G, &mth_d, 2 * (size_t)Gn))
+            return EGT_E_CUDA;
+        std::vector<int> ones(Gn, 1), flags(Gn, 0);
+        CK(cudaMemcpyAsync(scan, ones.data(), sizeof(int) * Gn, cudaMemcpyHostToDevice, G->st));
+        CK(cudaMemsetAsync(kbest, 0, sizeof(int) * Gn, G->st));
+        CK(cudaMemcpyAsync(mth_d, mu.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
         if (egt_omega_gradient(G, G->RESP[1])) return EGT_E_CUDA;  // RESP is scratch until the first step
         G->grads += 1;
         omega = G->RESP[1];
-        for (int round = 0; round < 6; ++round) {
-            int any = 0;
-            for (int g = 0; g < Gn; ++g) {
-                mid[g] = lo[g] < hi[g] ? (lo[g] + hi[g] + 1) / 2 : lo[g];
-                any += lo[g] < hi[g];
-                trial[g] = mu[g] * std::ldexp(1.0, -mid[g]);
-                trial[Gn + g] = mu[Gn + g] * std::ldexp(1.0, -mid[g]);
-            }
-            if (!any) break;
-            CK(cudaMemcpyAsync(G->sc.mu, trial.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
-            if (egt_initial_point(G, omega)) return EGT_E_CUDA;
-            G->grads += 2;
-            CK(cudaMemcpyAsync(vals.data(), G->sc.val, sizeof(double) * 2 * Gn, cudaMemcpyDeviceToHost, G->st));
-            CK(cudaStreamSynchronize(G->st));
-            for (int g = 0; g < Gn; ++g) {
-                if (lo[g] >= hi[g]) continue;
-                if (vals[g] + vals[Gn + g] >= 0.0) lo[g] = mid[g];
-                else hi[g] = mid[g] - 1;
+        int rounds = 0;
+        for (int k = 0; k <= EGT_MU_SCAN_KMAX; ++k) {
+            CK(launch_mu_scan(Gn, k, 0, mth_d, G->sc.mu, scan, kbest, G->sc.val, G->st));
+            if (egt_initial_point(G, omega, scan)) return EGT_E_CUDA;
+            CK(launch_mu_scan(Gn, k, 1, mth_d, G->sc.mu, scan, kbest, G->sc.val, G->st));
+            ++rounds;
+            if (k % 4 == 3 || k == EGT_MU_SCAN_KMAX) {
+                CK(cudaMemcpyAsync(flags.data(), scan, sizeof(int) * Gn, cudaMemcpyDeviceToHost, G->st));
+                CK(cudaStreamSynchronize(G->st));
+                if (std::find(flags.begin(), flags.end(), 1) == flags.end()) break;
             }
         }
-        for (int g = 0; g < Gn; ++g) {
-            chosen[g] = mu[g] * std::ldexp(1.0, -lo[g]);
-            chosen[Gn + g] = mu[Gn + g] * std::ldexp(1.0, -lo[g]);
+        G->grads += 2LL * rounds;
+        CK(launch_mu_scan(Gn, 0, 2, mth_d, G->sc.mu, scan, kbest, G->sc.val, G->st));
+        CK(cudaStreamSynchronize(G->st));
+        for (void* q : {(void*)scan, (void*)kbest, (void*)mth_d}) {
+            auto it = std::find(G->pool_allocs.begin(), G->pool_allocs.end(), q);
+            if (it != G->pool_allocs.end()) {
+                CK(cudaFreeAsync(*it, G->st));
+                G->pool_allocs.erase(it);
+            }
         }
-        CK(cudaMemcpyAsync(G->sc.mu, chosen.data(), sizeof(double) * 2 * Gn, cudaMemcpyHostToDevice, G->st));
-        tr.mark("practical mu search (device, host waits per round)");
+        tr.mark("practical mu scan (device, host looks every 4 rounds)");
     }
     if (egt_initial_point(G, omega)) return EGT_E_CUDA;
     G->grads += omega ? 2 : 3;

@@ -4,6 +4,8 @@
 #include "game.h"
 
 #include <algorithm>
+#include <array>
+#include <stdexcept>
 #include <cmath>
 #include <functional>
 #include <numeric>
@@ -487,6 +489,10 @@ static std::vector<int> board_of(const HostGame& G, const std::vector<std::vecto
     return G.tree.board_cards[bs];
 }
 
+static void build_card_plan(const HostGame& G, const std::vector<std::vector<int>>& by_card,
+                            const std::vector<int16_t>& lo, const std::vector<std::array<int, 2>>& cards_of_pos,
+                            int nv, CardPlan& plan);
+
 static void build_table(const HostGame& G, int g, int bs, const std::vector<int>& board, BoardTable& tb) {
     const int H = G.H, Hp = G.H_pad, hs = G.hand_size;
     tb.valid.assign(Hp, 0);
@@ -544,6 +550,158 @@ static void build_table(const HostGame& G, int g, int bs, const std::vector<int>
             tb.pcard[2 * (size_t)i + k] = PC_PACK(start, relo, rehi, W - 1);
         }
         tb.cent[start] |= (uint16_t)CE_FIRST;
+    }
+    // river boards: the card-domain gradient kernel's conflict-free exchange plan
+    if (hs == 2 && G.n_cards <= CARD_NT / CARD_GL && G.n_cards - 6 <= CARD_GL * CARD_CH && nv <= CARD_NP &&
+        G.kind == EGT_GAME_RIVER) {
+        std::vector<std::array<int, 2>> cp(nv);
+        for (int i = 0; i < nv; ++i) {
+            const int* hc = &G.hand_cards[((size_t)g * H + v[i].second) * 2];
+            cp[i] = {std::min(hc[0], hc[1]), std::max(hc[0], hc[1])};
+        }
+        build_card_plan(G, by_card, tb.lo, cp, nv, tb.plan);
+    }
+}
+
+// Proper edge colouring of a bipartite multigraph with max degree <= 16 in 16 colours
+// (alternating-path method; exists by Koenig's theorem).  edges[k] = (left, right).
+static std::vector<int> colour_edges16(int n_left, int n_right, const std::vector<std::pair<int, int>>& edges) {
+    constexpr int C = 16;
+    std::vector<int> at_l((size_t)n_left * C, -1), at_r((size_t)n_right * C, -1), col(edges.size(), -1);
+    auto free_l = [&](int u) { for (int c = 0; c < C; ++c) if (at_l[(size_t)u * C + c] < 0) return c; return -1; };
+    auto free_r = [&](int v) { for (int c = 0; c < C; ++c) if (at_r[(size_t)v * C + c] < 0) return c; return -1; };
+    for (size_t k = 0; k < edges.size(); ++k) {
+        const int u = edges[k].first, v = edges[k].second;
+        const int a = free_l(u), b = free_r(v);
+        if (a < 0 || b < 0) throw std::runtime_error("edge colouring: degree above 16");
+        if (at_r[(size_t)v * C + a] >= 0) {
+            // a is taken at v: swap a and b along the alternating path that starts at v with
+            // colour a (it cannot reach u, where a is free), freeing a at v
+            std::vector<int> path;
+            int x = v, side = 1, c = a;
+            while (true) {
+                const int e = side ? at_r[(size_t)x * C + c] : at_l[(size_t)x * C + c];
+                if (e < 0) break;
+                path.push_back(e);
+                x = side ? edges[e].first : edges[e].second;
+                side ^= 1;
+                c = c == a ? b : a;
+            }
+            for (int e : path) {
+                at_l[(size_t)edges[e].first * C + col[e]] = -1;
+                at_r[(size_t)edges[e].second * C + col[e]] = -1;
+            }
+            for (int e : path) {
+                col[e] = col[e] == a ? b : a;
+                at_l[(size_t)edges[e].first * C + col[e]] = e;
+                at_r[(size_t)edges[e].second * C + col[e]] = e;
+            }
+        }
+        col[k] = a;
+        at_l[(size_t)u * C + a] = (int)k;
+        at_r[(size_t)v * C + a] = (int)k;
+    }
+    return col;
+}
+
+// addresses of a colouring: colour c, m-th edge of that colour -> 16 m + c
+static std::vector<int> colour_addresses(const std::vector<int>& col) {
+    std::vector<int> cnt(16, 0), addr(col.size());
+    for (size_t k = 0; k < col.size(); ++k) addr[k] = 16 * cnt[col[k]]++ + col[k];
+    return addr;
+}
+
+// The conflict-free plan of grad_card_kernel for one river board (see CardPlan in game.h).
+// by_card[c]: positions holding card c in strength order; lo[i]: tie group start of position i.
+static void build_card_plan(const HostGame& G, const std::vector<std::vector<int>>& by_card,
+                            const std::vector<int16_t>& lo, const std::vector<std::array<int, 2>>& cards_of_pos,
+                            int nv, CardPlan& plan) {
+    const int NT = CARD_NT, K = CARD_K, GLN = CARD_GL, CH = CARD_CH, NP = CARD_NP;
+    // slot (c, k) -> thread, slot index; the card index (0: lower card of its hand)
+    struct Slot { int c, k, pos, which, thread, s; };
+    std::vector<Slot> slots;
+    std::vector<std::array<int, 2>> slot_of_pos(nv, {-1, -1});
+    for (int c = 0; c < G.n_cards; ++c)
+        for (int k = 0; k < (int)by_card[c].size(); ++k) {
+            const int i = by_card[c][k];
+            const int which = cards_of_pos[i][0] == c ? 0 : 1;
+            slot_of_pos[i][which] = (int)slots.size();
+            slots.push_back({c, k, i, which, c * GLN + k / CH, k % CH});
+        }
+    // w1 / w2: left = position-lane write groups (array, half-warp, j), right = slot-lane read
+    // groups (half-warp, s) -- one colouring for both arrays, since a read group mixes them
+    const int n_wg = (NT / 16) * K, n_rg = (NT / 16) * CH;
+    std::vector<int> waddr[2];
+    {
+        std::vector<std::pair<int, int>> e(2 * (size_t)nv);
+        for (int a = 0; a < 2; ++a)
+            for (int i = 0; i < nv; ++i) {
+                const Slot& sl = slots[slot_of_pos[i][a]];
+                e[(size_t)a * nv + i] = {a * n_wg + (i / K / 16) * K + i % K, (sl.thread / 16) * CH + sl.s};
+            }
+        const std::vector<int> col = colour_edges16(2 * n_wg, n_rg, e);
+        for (int a = 0; a < 2; ++a)
+            waddr[a] = colour_addresses(std::vector<int>(col.begin() + (size_t)a * nv, col.begin() + (size_t)(a + 1) * nv));
+    }
+    // ex: left = slot-lane write groups (half-warp, s), right = position-lane read groups (half-warp, j, card)
+    std::vector<std::pair<int, int>> e(slots.size());
+    for (size_t q = 0; q < slots.size(); ++q) {
+        const int i = slots[q].pos;
+        e[q] = {(slots[q].thread / 16) * CH + slots[q].s, ((i / K / 16) * K + i % K) * 2 + slots[q].which};
+    }
+    const std::vector<int> xaddr = colour_addresses(colour_edges16(n_rg, n_wg * 2, e));
+    const int zero_cell = 2 * NP;  // w region: w1 [0, NP), w2 [NP, 2 NP), a zero cell
+    plan.pw.assign(NP, 0u);
+    plan.pr.assign(NP, 0u);
+    for (int i = 0; i < nv; ++i) {
+        plan.pw[i] = (uint32_t)(waddr[0][i] * 8) | ((uint32_t)((NP + waddr[1][i]) * 8) << 16);
+        plan.pr[i] = (uint32_t)xaddr[slot_of_pos[i][0]] | ((uint32_t)xaddr[slot_of_pos[i][1]] << 16);
+    }
+    plan.lane.assign((size_t)NT * 8, 0u);
+    for (int t = 0; t < NT; ++t) {
+        uint32_t* L = &plan.lane[(size_t)t * 8];
+        for (int s = 0; s < CH; ++s) {
+            const uint32_t z = (uint32_t)(zero_cell * 8);
+            L[s / 2] |= (s & 1) ? z << 16 : z;
+        }
+    }
+    // per segment: run heads / tails (tie-group changes inside the card's strength-ordered
+    // list) and, per lane, the lanes that hold the run open at its chunk's start / end
+    for (int c = 0; c < G.n_cards; ++c) {
+        const std::vector<int>& Lc = by_card[c];
+        const int len = (int)Lc.size();
+        std::vector<int> head(len), tail(len);
+        for (int k = 0; k < len; ++k) {
+            head[k] = k == 0 || lo[Lc[k]] != lo[Lc[k - 1]];
+            tail[k] = k == len - 1 || lo[Lc[k]] != lo[Lc[k + 1]];
+        }
+        for (int part = 0; part < GLN; ++part) {
+            const int t = c * GLN + part;
+            uint32_t* L = &plan.lane[(size_t)t * 8];
+            uint32_t flags = 0;
+            for (int s = 0; s < CH; ++s) {
+                const int k = part * CH + s;
+                if (k >= len) continue;
+                const int q = slot_of_pos[Lc[k]][cards_of_pos[Lc[k]][0] == c ? 0 : 1];
+                const uint32_t g = (uint32_t)(waddr[slots[q].which][Lc[k]] + slots[q].which * NP) * 8;
+                L[s / 2] = (s & 1) ? ((L[s / 2] & 0xFFFFu) | (g << 16)) : ((L[s / 2] & 0xFFFF0000u) | g);
+                L[3 + s / 2] |= (s & 1) ? (uint32_t)xaddr[q] << 16 : (uint32_t)xaddr[q];
+                flags |= 1u << s;
+                if (head[k]) flags |= 1u << (6 + s);
+                if (tail[k]) flags |= 1u << (12 + s);
+            }
+            L[6] = flags;
+            // src_lo: the nearest lane before this one (same segment) with a run head; src_hi:
+            // the nearest lane after it with a run tail (absolute lane indices in the warp)
+            int src_lo = t, src_hi = t;
+            for (int q = part - 1; q >= 0 && src_lo == t; --q)
+                for (int s = 0; s < CH; ++s)
+                    if (q * CH + s < len && head[q * CH + s]) src_lo = c * GLN + q;
+            for (int q = part + 1; q < GLN && src_hi == t; ++q)
+                for (int s = 0; s < CH; ++s)
+                    if (q * CH + s < len && tail[q * CH + s]) { src_hi = c * GLN + q; break; }
+            L[7] = (uint32_t)(src_lo & 31) | ((uint32_t)(src_hi & 31) << 8);
+        }
     }
 }
 

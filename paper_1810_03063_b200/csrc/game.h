@@ -92,8 +92,31 @@ struct Terminal {
 // Per position and card slot k (the hand's k-th card), pcard packs the card's segment
 // start in the card array, the segment indices of the hand's tie group [relo, rehi)
 // and the segment length (PC_* below).
+// Plan of the card-domain river gradient kernel (kernels.cu grad_card_kernel) for one board:
+// CARD_NT threads; thread t owns positions 3t..3t+2 (position domain) and slots
+// 6*(t%8)..6*(t%8)+5 of card t/8's segment (card domain).  Every shared-memory exchange
+// between the two domains goes through addresses chosen on the host so that no two lanes of a
+// half-warp touch the same 8-byte bank pair in one instruction (a proper 16-edge-colouring of
+// a bipartite graph of lane groups, which exists by Koenig's theorem):
+//   w1 / w2  position -> card:  position i writes its weight to w1 (read by the slot of its
+//            lower card) and w2 (higher card);
+//   ex       card -> position:  at a row end slot e writes its accumulated card term, and
+//            position i reads the slots of its two cards.
+constexpr int CARD_NT = 416, CARD_K = 3, CARD_GL = 8, CARD_CH = 6;
+constexpr int CARD_NP = CARD_NT * CARD_K;            // positions (>= H_pad)
+constexpr int CARD_WREGION = 2 * CARD_NP + 2;        // doubles: w1, w2, a zero cell (+ pad)
+constexpr int CARD_EX = CARD_NT * CARD_CH;           // doubles of the ex exchange
+struct CardPlan {
+    std::vector<uint32_t> pw;    // [CARD_NP] byte offsets into the w region: w1 | w2 << 16
+    std::vector<uint32_t> pr;    // [CARD_NP] ex element index of the lower-card slot | higher << 16
+    std::vector<uint32_t> lane;  // [CARD_NT][8] per thread: cg[3] (gather byte offsets, 2 x 16 bit),
+                                 // px[3] (ex element index, 2 x 16 bit), flags (valid 0-5, run head
+                                 // 6-11, run tail 12-17), src lanes (lo 0-4, hi 8-12)
+};
+
 struct BoardTable {
     int nvalid = 0;
+    CardPlan plan;               // river boards (hand_size 2, identity order) only
     std::vector<int16_t> order;  // [H_pad] position -> hand
     std::vector<int16_t> lo, hi; // [H_pad] per position: tie-group bounds [lo, hi)
     std::vector<uint32_t> lohi;  // [H_pad] lo | hi << 16

@@ -39,9 +39,16 @@ __device__ __forceinline__ T warp_incl_scan_lim(T v, int lane) {
 
 // exp(x) for x <= 0 to ~1 ulp: x = (64 k + j) ln2 / 64 + r, |r| <= ln2 / 128,
 // exp(x) = 2^k' * tab[j] * (1 + r + ... + r^5/120) (truncation < 4e-17 relative).
-// tab[j] = 2^(j/64) lives in shared memory.  Arguments below -707 give exp(-707).
+// tab[j] = 2^(j/64) lives in shared memory.  Results below the normal range underflow
+// gradually (subnormals, one rounding), and to 0 below -745.2 (also for x = -inf), as
+// IEEE exp does -- no floor (the oracle's numpy exp underflows the same way).
+__device__ __noinline__ double exp_subnormal(double v, int e) {
+    // v in [1, 2), 2^e below the normal range: scale in two exact-then-rounding steps
+    const double a = __hiloint2double((e + 600 + 1023) << 20, 0);  // 2^(e + 600), normal
+    return (v * a) * 0x1p-600;
+}
 __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict__ tab) {
-    x = fmax(x, -707.0);  // keeps 2^k' * v normal; exp(-707) ~ 1e-307 stands in for 0
+    if (!(x >= -745.2)) return 0.0;  // incl. -inf (NaN propagates as 0: inputs are finite)
     const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
     const double big = fma(x, 92.332482616893656877, magic);
     const int k = __double2loint(big);
@@ -54,7 +61,9 @@ __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict_
     p = fma(p, r, 1.0);
     p = fma(p, r, 1.0);
     const double v = tab[k & 63] * p;
-    return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));
+    const int e = k >> 6;
+    if (e < -1021) return exp_subnormal(v, e);
+    return __hiloint2double(__double2hiint(v) + (e << 20), __double2loint(v));
 }
 
 // fp32 mode: the library exp on non-positive arguments (<= 2 ulp)
@@ -331,14 +340,28 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
     }
 }
 
-// ------------------------------------------------------------------ staged river gradient
-// The same computation for games whose positions are the hands and where every hand is
-// valid (river endgames, Kuhn): one CTA per (chunk of sequences, game), persistent over
-// the chunk's terminals.  The game's tables and priors are staged in shared memory once
-// per CTA with bulk async copies (TMA engine, cp.async.bulk + mbarrier); each terminal's
-// opponent row is double-buffered -- the copy of terminal t+1's row overlaps terminal t.
-// Every global read is a bulk copy; a finished output row goes from registers straight to
-// global memory (each warp writes 96 consecutive positions), with no barrier at a row end.
+// ------------------------------------------------------------------ card-domain river gradient
+// River endgames (every hand valid, positions = hands in strength order, two cards per hand):
+// one CTA per (chunk of consecutive rows, game), persistent over the chunk's terminals, CARD_NT
+// threads playing two roles (game.h CardPlan):
+//  * position domain -- thread t holds positions 3t..3t+2: w = prior_opp * v_opp, its block
+//    prefix P, the position part of every hand's value (T - P[hi] - P[lo] for a showdown,
+//    T + w(h) for a fold), accumulated per position over the row's terminals;
+//  * card domain -- the 8 lanes of card c hold the hands holding c in strength order (6 slots
+//    each): their weights, the segment prefix Pc and total S_c, and each slot's card part
+//    (Pc[lo] + Pc[hi] - S_c for a showdown, -S_c for a fold) accumulated per slot over the
+//    row's terminals, never leaving registers until the row ends.
+// Pc[lo] / Pc[hi] are the segment prefixes at the start / end of the slot's tie run inside the
+// segment: in registers within a lane's 6 slots, and one shuffle from a host-planned source
+// lane (the run's head / tail lane) when the run crosses lanes.  A hand's value is its position
+// part plus the card parts of its two slots (PAPER.md:299 gradient, reading R13 payoffs):
+//   showdown  sign * [(T - P[hi] - P[lo]) + sum_{c in h} (Pc[lo] + Pc[hi] - S_c)]
+//   fold      T - S_c1 - S_c2 + w(h)            (inclusion-exclusion over the blocked cards)
+// Only two shared-memory exchanges cross the domains, both at host-planned addresses that are
+// bank-conflict free per half-warp: the weights (position -> card, once per opponent row) and
+// the card parts (card -> position, once per row).  The game's priors and each terminal's
+// opponent row arrive by bulk async copies (TMA engine, mbarrier); the next terminal's row is
+// in flight while this one is processed.
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -363,40 +386,36 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Card sums: every card's segment (seg_w slots) is scanned by one group of GL lanes (CH
-// slots each, GL * CH >= seg_w), so segments never straddle groups or warps.
-template <int NT, int K, int CH, int HS, int GLL, typename T>
-__global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
-                                                            VecRef gout, const int* __restrict__ mask, int want,
-                                                            int gl_log2, DevPeers peers) {
+__device__ __forceinline__ unsigned half16(unsigned v, int hi) { return hi ? v >> 16 : v & 0xFFFFu; }
+
+template <typename T>
+__global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
+                                                               VecRef gout, const int* __restrict__ mask, int want,
+                                                               DevPeers peers) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
-    T* sm = reinterpret_cast<T*>(sm_raw);
-    constexpr int NW = NT / 32, NP = NT * K;  // positions padded to NP
+    constexpr int NT = CARD_NT, K = CARD_K, CH = CARD_CH, NW = NT / 32, NP = CARD_NP;
     __shared__ T wtot[NW];
     __shared__ __align__(8) uint64_t bar[3];
-    // the chunk's terminals (<= GRAD_CHUNK_MAX_TERMS): opponent row, kind, weight, and the
-    // row each one completes (-1: more terminals of its row follow)
+    // the chunk's terminals: opponent row, kind, weight, and the row each one completes (-1: more
+    // terminals of its row follow)
     __shared__ int t_so[GRAD_CHUNK_MAX_TERMS], t_kind[GRAD_CHUNK_MAX_TERMS], t_end[GRAD_CHUNK_MAX_TERMS];
     __shared__ double t_w[GRAD_CHUNK_MAX_TERMS];
     const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (mask && mask[g] != want) return;
-    const int Hp = G.H_pad, H = G.H, n_ce = G.n_ce, W = G.seg_w;
-    T* popp = sm;                 // [NP] (0 beyond H)
-    T* pself = popp + NP;         // [Hp]
-    T* vb = pself + Hp;           // [2][NP] opponent rows (0 beyond Hp)
-    T* w = vb + 2 * NP;           // [NP + 4] (w[NP] = 0 stands in for empty card slots)
-    T* Pf = w + NP + 4;           // [NP + 4]
-    T* Ex = Pf + NP + 4;          // [n_ce] (Pf padded to keep 16-byte alignment)
-    uint2* pcard = reinterpret_cast<uint2*>(Ex + n_ce);              // [NP]
-    uint32_t* lohi = reinterpret_cast<uint32_t*>(pcard + NP);        // [NP]
-    uint16_t* cent = reinterpret_cast<uint16_t*>(lohi + NP);         // [n_ce]
+    const int Hp = G.H_pad, H = G.H;
+    T* popp = reinterpret_cast<T*>(sm_raw);  // [NP] (0 beyond H)
+    T* pself = popp + NP;                    // [NP]
+    T* vb = pself + NP;                      // [2][NP] opponent rows (0 beyond Hp)
+    T* wreg = vb + 2 * NP;                   // [CARD_WREGION] w1 | w2 | zero cell
+    T* Pf = wreg + CARD_WREGION;             // [NP + 4] exclusive prefixes of w by position
+    T* Ex = Pf + NP + 4;                     // [CARD_EX] card parts at a row end
+    unsigned char* const wbytes = reinterpret_cast<unsigned char*>(wreg);
     const int r0 = P.chunk_off[blockIdx.x], r1 = P.chunk_off[blockIdx.x + 1];
     const int T0 = P.term_off[P.rows_term[r0]], T1 = P.term_off[P.rows_term[r1 - 1] + 1];
     const T* __restrict__ vo = vin.at<T>(g);
-    const int* __restrict__ tidx = P.term_idx;
     const int nT = T1 - T0;
     for (int i = tid; i < nT; i += NT) {
-        const DevTerm tm = G.terms[tidx[T0 + i]];
+        const DevTerm tm = G.terms[P.term_idx[T0 + i]];
         t_so[i] = player ? tm.seq[0] : tm.seq[1];
         t_kind[i] = tm.kind;
         t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
@@ -408,29 +427,24 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
         mbar_init(&bar[2], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // padding beyond the copied ranges (never overwritten by the bulk copies)
-    for (int i = Hp + tid; i < NP; i += NT) {
+    for (int i = Hp + tid; i < NP; i += NT) {  // padding the bulk copies never write
         popp[i] = T(0);
+        pself[i] = T(0);
         vb[i] = T(0);
         vb[NP + i] = T(0);
-        pcard[i] = make_uint2(0u, 0u);
-        lohi[i] = 0u;
     }
-    if (tid < 4) w[NP + tid] = T(0);
+    if (tid < CARD_WREGION - 2 * NP) wreg[2 * NP + tid] = T(0);  // the zero cell padding slots read
+    if (tid < 4) Pf[NP + tid] = T(0);
     __syncthreads();
     for (int r = r0 + tid; r < r1; r += NT) {
         const int srow = P.rows_term[r];
         t_end[P.term_off[srow + 1] - 1 - T0] = srow;
     }
     if (tid == 0) {
-        const unsigned bD = Hp * sizeof(T), bU2 = Hp * sizeof(uint2), bU = Hp * sizeof(uint32_t),
-                       bC = n_ce * sizeof(uint16_t);
-        mbar_expect_tx(&bar[0], 2 * bD + bU2 + bU + bC);
+        const unsigned bD = Hp * sizeof(T);
+        mbar_expect_tx(&bar[0], 2 * bD);
         bulk_g2s(popp, static_cast<const T*>(player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp, bD, &bar[0]);
         bulk_g2s(pself, static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp, bD, &bar[0]);
-        bulk_g2s(pcard, G.tab_pcard + (size_t)g * Hp, bU2, &bar[0]);
-        bulk_g2s(lohi, G.tab_lohi + (size_t)g * Hp, bU, &bar[0]);
-        bulk_g2s(cent, G.tab_cent + (size_t)g * n_ce, bC, &bar[0]);
         for (int q = 0; q < 2 && T0 + q < T1; ++q) {
             const int so = t_so[q];
             if (so && !(q > 0 && so == t_so[q - 1])) {
@@ -439,67 +453,37 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             }
         }
     }
-    
+    // the board's plan, in registers for the whole chunk (game.h CardPlan)
+    const int base = tid * K, part = tid & (CARD_GL - 1);
+    // (the exchange addresses used once per opponent row or per row stay in L1: __ldg)
+    const uint32_t* __restrict__ lh_g = G.tab_lohi + (size_t)g * Hp + base;  // tie group [lo, hi) per position
+    const uint32_t* __restrict__ pw_g = G.card_pw + (size_t)g * NP + base;
+    const uint32_t* __restrict__ pr_g = G.card_pr + (size_t)g * NP + base;
+    const uint4* __restrict__ lane_g = reinterpret_cast<const uint4*>(G.card_lane) + ((size_t)g * NT + tid) * 2;
+    const uint4 la = __ldg(lane_g), lb = __ldg(lane_g + 1);
+    const uint32_t cg[3] = {la.x, la.y, la.z};
+    const uint32_t flags = lb.z;
+    const int src_lo = (int)(lb.w & 31u), src_hi = (int)((lb.w >> 8) & 31u);
     const T sd_sign = player == 0 ? T(1) : T(-1);
-    const int base = tid * K;
-    // card-array role: segment sgi, part of it [sbeg, sbeg + CH)
-    const int gll = GLL >= 0 ? GLL : gl_log2;
-    const int GL = 1 << gll;
-    const int sgi = tid >> gll, part = tid & (GL - 1);
-    const bool has_seg = sgi < G.n_cards;
-    const int sbeg = sgi * W + part * CH;
-    const int send = has_seg ? min(sgi * W + W, sbeg + CH) : sbeg;
-    T racc[K];
+    T racc[K], rc[CH], dsd[CH], x[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) racc[j] = T(0);
+    for (int j = 0; j < K; ++j) racc[j] = x[j] = T(0);
+#pragma unroll
+    for (int s = 0; s < CH; ++s) rc[s] = dsd[s] = T(0);
+    T total = T(0), pbase = T(0), segS = T(0);
     unsigned par = 0u;  // mbarrier phase bit of each opponent-row buffer
+    bool ex_dirty = false;  // the last row end's Ex reads are not yet behind a barrier
     mbar_wait(&bar[0], 0);
     __syncthreads();  // t_end
-    // the game's tables are the same for every terminal: this thread's card-array slots and
-    // its positions' card / tie-group indices live in registers for the whole chunk
-    // (cpos: byte offsets into w, empty slots read the zero at w[NP]; the card-array slots
-    // this thread writes: all of them (bits 0-7 of masks) or only its segment's end slot (bits 8-15);
-    // bits 16+ mark positions alone in their tie group)
-    static_assert(NP * sizeof(T) < 65536, "card slot offsets are packed in 16 bits");
-    unsigned cpos[(CH + 1) / 2];  // two 16-bit offsets per register
-    unsigned masks = 0u;
-    const int end_slot = sgi * W + W - 1;
-#pragma unroll
-    for (int j = 0; j < CH; ++j) {
-        const int e = sbeg + j;
-        const unsigned c = e < send ? (cent[e] & CE_END) : CE_END;
-        const unsigned off = (c == CE_END ? (unsigned)NP : c) * (unsigned)sizeof(T);
-        if (j & 1) cpos[j / 2] |= off << 16;
-        else cpos[j / 2] = off;
-        if (has_seg && e < send) {
-            masks |= 1u << j;
-            if (e == end_slot) masks |= 1u << (8 + j);
-        }
-    }
-    T* const exs = Ex + sbeg;
-    const unsigned char* const wbytes = reinterpret_cast<const unsigned char*>(w);
-    uint2 pcr[K];
-    uint32_t lhr[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        pcr[j] = pcard[base + j];
-        lhr[j] = lohi[base + j];
-        if ((int)(lhr[j] & 0xFFFFu) == base + j && (int)(lhr[j] >> 16) == base + j + 1) masks |= 1u << (16 + j);
-    }
-    // w's chunk, its total and this thread's prefix survive a terminal: the next terminal
-    // reuses them (and the card sums) when it reads the same opponent row (a fold / call pair
-    // of one decision node); the first of such a pair then writes the full card-array prefixes
-    T x[K];
-    T total = T(0), pbase = T(0);
     for (int ti = T0; ti < T1; ++ti) {
         const int q = (ti - T0) & 1, li = ti - T0;
         const int so = t_so[li];
         const bool sd = t_kind[li] == 2;
         const bool reuse = li > 0 && so == t_so[li - 1];
+        // the run values of a showdown, also computed by the first of a fold / call pair on the
+        // same opponent row when the call follows
         const bool full = sd || (li + 1 < nT && t_so[li + 1] == so && t_kind[li + 1] == 2);
-        // prefetch terminal ti+1's row into the other buffer (its previous reader, terminal
-        // ti-1, finished phase A before that terminal's first barrier)
-        if (tid == 0 && ti > T0 && ti + 1 < T1) {
+        if (tid == 0 && ti > T0 && ti + 1 < T1) {  // terminal ti+1's row into the other buffer
             const int so1 = t_so[li + 1];
             if (so1 && so1 != so) {
                 fence_proxy_async();
@@ -511,109 +495,147 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
             mbar_wait(&bar[1 + q], (par >> q) & 1u);
             par ^= 1u << q;
         }
-        if (!reuse) {  // warp-uniform (the whole CTA takes the same branch)
-        const T* vrow = vb + q * NP;
-        // ---- phase A: w = prior_opp * v_opp in chunks of K positions, warp scan of the chunk sums
-        T run = T(0);
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            x[j] = so ? popp[base + j] * vrow[base + j] : popp[base + j];
-            w[base + j] = x[j];
-            run += x[j];
-        }
-        const T incl = warp_incl_scan(run, lane);
-        if (lane == 31) wtot[wid] = incl;
-        __syncthreads();
-        // ---- phase B: card sums (segment scans inside lane groups) and the block prefix of w
-        {
-            T y[CH];
-            T ssum = T(0);
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-                y[j] = *reinterpret_cast<const T*>(wbytes + ((j & 1) ? (cpos[j / 2] >> 16) : (cpos[j / 2] & 0xFFFFu)));
-                ssum += y[j];
-            }
-            // exclusive scan of the part sums inside the segment's lane group
-            T inc = ssum;
-            if (GLL >= 0) {
-#pragma unroll
-                for (int o = 1; o < (1 << (GLL >= 0 ? GLL : 0)); o <<= 1) {
-                    const T u = __shfl_up_sync(0xffffffffu, inc, o, GL);
-                    if (part >= o) inc += u;
-                }
-            } else {
-                for (int o = 1; o < GL; o <<= 1) {
-                    const T u = __shfl_up_sync(0xffffffffu, inc, o, GL);
-                    if (part >= o) inc += u;
-                }
-            }
-            // the same accumulation order in both cases, so a segment total never depends on
-            // whether the terminal needs the full prefixes (folds: end slot only)
-            const unsigned wm = full ? masks : masks >> 8;
-            T run2 = inc - ssum;
-#pragma unroll
-            for (int j = 0; j < CH; ++j) {
-                if (wm & (1u << j)) exs[j] = run2;
-                run2 += y[j];
-            }
-        }
-        // block prefix of the warp totals: one load per lane, a warp scan, two shuffles
-        const T wsc = warp_incl_scan_lim<(NW <= 16 ? 16 : 32)>(lane < NW ? wtot[lane] : T(0), lane);
-        const T wpre_incl = __shfl_sync(0xffffffffu, wsc, (wid + 31) & 31);
-        const T wpre = wid ? wpre_incl : T(0);
-        total = __shfl_sync(0xffffffffu, wsc, NW - 1);
-        pbase = wpre + incl - run;
-        if (full) {
-            T p = pbase;
+        if (!reuse) {  // CTA-uniform
+            // ---- position domain: w, its two conflict-free copies for the card lanes, warp scan
+            const T* vrow = vb + q * NP;
+            T run = T(0);
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                Pf[base + j] = p;
-                p += x[j];
-            }
-        }
-        __syncthreads();
-        }  // !reuse
-        // ---- phase C (positions beyond H compute on padding and are never stored)
-        const T scale = (T)t_w[li];
-        T pre = pbase;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const uint2 pc = pcr[j];
-            T v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)];
-            if (HS == 2) v -= Ex[PC_START(pc.y) + PC_LEN(pc.y)];
-            if (sd) {
-                const uint32_t lh = lhr[j];
-                const int lo = lh & 0xFFFFu, hi = lh >> 16;
-                if (masks & (1u << (16 + j))) {
-                    const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)];
-                    v += -(pre + (pre + x[j])) + (ca + (ca + x[j]));
-                    if (HS == 2) {
-                        const T cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
-                        v += cb + (cb + x[j]);
-                    }
-                } else {
-                    v += -(Pf[lo] + Pf[hi]) + Ex[PC_START(pc.x) + PC_RELO(pc.x)] + Ex[PC_START(pc.x) + PC_REHI(pc.x)];
-                    if (HS == 2) v += Ex[PC_START(pc.y) + PC_RELO(pc.y)] + Ex[PC_START(pc.y) + PC_REHI(pc.y)];
+                x[j] = so ? popp[base + j] * vrow[base + j] : popp[base + j];
+                run += x[j];
+                if (base + j < H) {
+                    const uint32_t pw = __ldg(pw_g + j);
+                    *reinterpret_cast<T*>(wbytes + half16(pw, 0)) = x[j];
+                    *reinterpret_cast<T*>(wbytes + half16(pw, 1)) = x[j];
                 }
-                v *= sd_sign;
-            } else if (HS == 2) {
-                v += x[j];
             }
-            racc[j] += scale * v;
-            pre += x[j];
+            const T incl = warp_incl_scan(run, lane);
+            if (lane == 31) wtot[wid] = incl;
+            __syncthreads();
+            // ---- card domain: the segment's weights, prefix (8-lane group scan) and total
+            T y[CH], ssum = T(0);
+#pragma unroll
+            for (int s = 0; s < CH; ++s) {
+                y[s] = *reinterpret_cast<const T*>(wbytes + half16(cg[s / 2], s & 1));
+                ssum += y[s];
+            }
+            T inc = ssum;
+#pragma unroll
+            for (int o = 1; o < CARD_GL; o <<= 1) {
+                const T u = __shfl_up_sync(0xffffffffu, inc, o, CARD_GL);
+                if (part >= o) inc += u;
+            }
+            segS = __shfl_sync(0xffffffffu, inc, lane | (CARD_GL - 1));
+            if (full) {
+                T ex[CH];
+                T r = inc - ssum;
+#pragma unroll
+                for (int s = 0; s < CH; ++s) {
+                    ex[s] = r;
+                    r += y[s];
+                }
+                // this lane's last run head / first run tail, for lanes whose runs cross into it
+                T lh = T(0), ft = T(0);
+#pragma unroll
+                for (int s = 0; s < CH; ++s)
+                    if ((flags >> (6 + s)) & 1u) lh = ex[s];
+#pragma unroll
+                for (int s = CH - 1; s >= 0; --s)
+                    if ((flags >> (12 + s)) & 1u) ft = ex[s] + y[s];
+                const T clo = __shfl_sync(0xffffffffu, lh, src_lo);
+                const T chi = __shfl_sync(0xffffffffu, ft, src_hi);
+                T cur = clo;
+#pragma unroll
+                for (int s = 0; s < CH; ++s) {
+                    if ((flags >> (6 + s)) & 1u) cur = ex[s];
+                    dsd[s] = cur;  // Pc at the run's start
+                }
+                cur = chi;
+#pragma unroll
+                for (int s = CH - 1; s >= 0; --s) {
+                    if ((flags >> (12 + s)) & 1u) cur = ex[s] + y[s];
+                    dsd[s] += cur - segS;  // + Pc at the run's end - S_c
+                }
+            }
+            // ---- position domain: block prefix of w
+            const T wsc = warp_incl_scan_lim<(NW <= 16 ? 16 : 32)>(lane < NW ? wtot[lane] : T(0), lane);
+            const T wpre_incl = __shfl_sync(0xffffffffu, wsc, (wid + 31) & 31);
+            const T wpre = wid ? wpre_incl : T(0);
+            total = __shfl_sync(0xffffffffu, wsc, NW - 1);
+            pbase = wpre + incl - run;
+            if (full) {
+                T pp = pbase;
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    Pf[base + j] = pp;
+                    pp += x[j];
+                }
+                if (tid == 0) Pf[NP] = total;
+            }
+            __syncthreads();
+            ex_dirty = false;
         }
-        // ---- row end: prior_self * acc straight from registers to the output row(s): each warp's
-        // 96 consecutive positions form one contiguous 768-byte span (coalesced in L2), and no
-        // staging buffer means no barrier at a row end
+        // ---- this terminal's contribution: position parts and card parts
+        const T scale = (T)t_w[li];
+        if (sd) {
+            const T pp1 = pbase + x[0], pp2 = pp1 + x[1];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const uint32_t lh = base + j < Hp ? __ldg(lh_g + j) : 0u;
+                const int lo = (int)(lh & 0xFFFFu), hi = (int)(lh >> 16);
+                T plo, phi;
+                if (lo >= base && hi <= base + K) {  // the tie group lies inside this thread's positions
+                    const int a = lo - base, b = hi - base;
+                    plo = a == 0 ? pbase : a == 1 ? pp1 : pp2;
+                    phi = b == 1 ? pp1 : b == 2 ? pp2 : pp2 + x[2];
+                } else {
+                    plo = Pf[lo];
+                    phi = Pf[hi];
+                }
+                racc[j] += scale * (sd_sign * (total - phi - plo));
+            }
+            const T sc2 = scale * sd_sign;
+#pragma unroll
+            for (int s = 0; s < CH; ++s) rc[s] += sc2 * dsd[s];
+        } else {
+#pragma unroll
+            for (int j = 0; j < K; ++j) racc[j] += scale * (total + x[j]);
+            const T sS = scale * segS;
+#pragma unroll
+            for (int s = 0; s < CH; ++s) rc[s] -= sS;
+        }
+        // ---- row end: card parts to the positions of their hands, then the output row
         const int srow = t_end[li];
         if (srow >= 0) {
+            if (ex_dirty) __syncthreads();
+            {
+                const uint4 lx = __ldg(lane_g);
+                const uint4 ly = __ldg(lane_g + 1);
+                const uint32_t px[3] = {lx.w, ly.x, ly.y};
+#pragma unroll
+                for (int s = 0; s < CH; ++s) {
+                    if ((flags >> s) & 1u) Ex[half16(px[s / 2], s & 1)] = rc[s];
+                    rc[s] = T(0);
+                }
+            }
+            __syncthreads();
+            T outv[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const int i = base + j;
+                outv[j] = T(0);
+                if (i < H) {
+                    const uint32_t pr = __ldg(pr_g + j);
+                    outv[j] = pself[i] * (racc[j] + Ex[half16(pr, 0)] + Ex[half16(pr, 1)]);
+                }
+                racc[j] = T(0);
+            }
+            ex_dirty = true;
             if (peers.n == 0) {
                 T* __restrict__ dst = gout.at<T>(g) + (size_t)srow * Hp;
 #pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    const int i = base + j;
-                    if (i < Hp) dst[i] = i < H ? pself[i] * racc[j] : T(0);
-                }
+                for (int j = 0; j < K; ++j)
+                    if (base + j < Hp) dst[base + j] = outv[j];
             } else {
                 // fused all-gather: the finished row goes straight into every shard's gradient
                 // buffer (peer memory over NVLink), overlapping the next terminals
@@ -623,15 +645,11 @@ __global__ void __launch_bounds__(NT, 2) grad_staged_kernel(DevGame G, DevPlayer
                     if (d < peers.n) {
                         T* __restrict__ dst = reinterpret_cast<T*>(peers.base[d]) + off;
 #pragma unroll
-                        for (int j = 0; j < K; ++j) {
-                            const int i = base + j;
-                            if (i < Hp) dst[i] = i < H ? pself[i] * racc[j] : T(0);
-                        }
+                        for (int j = 0; j < K; ++j)
+                            if (base + j < Hp) dst[base + j] = outv[j];
                     }
                 }
             }
-#pragma unroll
-            for (int j = 0; j < K; ++j) racc[j] = T(0);
         }
     }
 }
@@ -642,43 +660,21 @@ static size_t grad_smem_bytes(const DevGame& G) {
     return (size_t)G.esz * (size_t)(3 * G.H_pad + 1 + G.n_ce);
 }
 
-#ifndef STG_CH_DEF
-#define STG_CH_DEF 6
-#endif
-static constexpr int STG_NT = 416, STG_K = 3, STG_CH = STG_CH_DEF;  // positions <= 1248, card segments <= 6 x 8 lanes
-
-static size_t grad_staged_smem_bytes(const DevGame& G) {
-    const size_t Hp = G.H_pad, NP = (size_t)STG_NT * STG_K;
-    return (size_t)G.esz * (Hp + 5 * NP + 8 + G.n_ce) + sizeof(uint2) * NP + sizeof(uint32_t) * NP +
-           sizeof(uint16_t) * G.n_ce + 16;
+static size_t card_smem_bytes(const DevGame& G) {
+    return (size_t)G.esz * (4 * (size_t)CARD_NP + CARD_WREGION + CARD_NP + 4 + CARD_EX);
 }
 
-static int staged_gl_log2(const DevGame& G) {
-    int l = 0;
-    while ((1 << l) * STG_CH < G.seg_w) ++l;
-    return l;
-}
-
-static bool staged_ok(const DevGame& G) {
-    return G.ident && G.all_valid && G.n_bs == 1 && G.H_pad <= STG_NT * STG_K && (G.hand_size == 1 || G.hand_size == 2) &&
-           (G.n_cards << staged_gl_log2(G)) <= STG_NT && (1 << staged_gl_log2(G)) <= 32;
+static bool card_ok(const DevGame& G) {
+    return G.card_plan && G.ident && G.all_valid && G.n_bs == 1 && G.hand_size == 2 && G.H_pad <= CARD_NP;
 }
 
 template <class T>
 static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
                                      const int* mask, int want, cudaStream_t st, const DevPeers& peers) {
-    if (staged_ok(G) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
+    if (card_ok(G) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
-        const int gl = staged_gl_log2(G);
-        const size_t sm = grad_staged_smem_bytes(G);
-        // the river's card segments (47 slots = 8 lanes x 6) get a fully unrolled lane-group scan
-        if (G.hand_size == 2 && gl == 3)
-            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, 3, T><<<grid, STG_NT, sm, st>>>(G, P, player, vin, gout, mask, want, gl, peers);
-        else if (G.hand_size == 2)
-            grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, -1, T><<<grid, STG_NT, sm, st>>>(G, P, player, vin, gout, mask, want, gl, peers);
-        else
-            grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, -1, T><<<grid, STG_NT, sm, st>>>(G, P, player, vin, gout, mask, want, gl, peers);
+        grad_card_kernel<T><<<grid, CARD_NT, card_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, peers);
         return cudaGetLastError();
     }
     dim3 grid(P.n_rows_term, G.n_games);
@@ -742,6 +738,7 @@ struct TreeNodeCtx {
     T mu;
     const double* __restrict__ exptab;
     T cfr_scale;  // CFR: max |g| over the hand's sequences (the noise floor of reading R15)
+    T* __restrict__ lbo;  // SBR: behavioural log-probabilities output (nullptr: none)
 };
 
 // Bottom-up work of simplex (node m, hand h) on its column; returns the simplex value.
@@ -753,37 +750,43 @@ __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlay
     for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= sc;  // the objective's scale (see tree_kernel)
     if (mode == TM_SBR) {
         // qbar_i ~ exp(-g_i / w), value = g_{i*} + w log qbar_{i*} + w log n with
-        // i* = argmax qbar, w = mu beta_j
+        // i* = argmax qbar, w = mu beta_j; log qbar_i = arg_i - log S
         T mn = big_value<T>();
         for (int a = 0; a < n; ++a) mn = fmin(mn, col[a * TH_HANDS]);
         T S = T(0);
         for (int a = 0; a < n; ++a) {
-            const T e = exp_nonpos((mn - col[a * TH_HANDS]) * iw, C.exptab);
-            col[a * TH_HANDS] = e;
-            S += e;
+            const T arg = (mn - col[a * TH_HANDS]) * iw;
+            col[a * TH_HANDS] = arg;
+            S += exp_nonpos(arg, C.exptab);
         }
-        const T inv = T(1) / S;
-        for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
-        return mn - wgt * (log(S) - logn);
+        const T inv = T(1) / S, lS = log(S);
+        for (int a = 0; a < n; ++a) {
+            const T arg = col[a * TH_HANDS];
+            if (C.lbo) C.lbo[(size_t)(first + a) * Hp + h] = arg - lS;
+            col[a * TH_HANDS] = exp_nonpos(arg, C.exptab) * inv;
+        }
+        return mn - wgt * (lS - logn);
     }
     if (mode == TM_PROX) {
-        // shifted-gradient SBR in multiplicative form (R16):
-        // qbar_i ~ zbar_i exp(-g_i / beta), value = -beta log sum_i zbar_i exp(-g_i / beta)
+        // shifted-gradient SBR with the centre's behavioural logs
+        // (R16): qbar_i ~ exp(lb_i - g_i / beta), value = -beta log sum_i exp(lb_i - g_i / beta)
         const T beta = wgt, ib = iw;
         const T* __restrict__ zr = cz + (size_t)first * Hp + h;
-        T mn = big_value<T>();
-        for (int a = 0; a < n; ++a)
-            if (zr[(size_t)a * Hp] > T(0)) mn = fmin(mn, col[a * TH_HANDS]);
+        T m = -big_value<T>();
+        for (int a = 0; a < n; ++a) {
+            const T e = zr[(size_t)a * Hp] - col[a * TH_HANDS] * ib;
+            col[a * TH_HANDS] = e;
+            m = fmax(m, e);
+        }
         T S = T(0);
         for (int a = 0; a < n; ++a) {
-            const T za = zr[(size_t)a * Hp];
-            const T e = za > T(0) ? za * exp_nonpos((mn - col[a * TH_HANDS]) * ib, C.exptab) : T(0);
+            const T e = exp_nonpos(col[a * TH_HANDS] - m, C.exptab);
             col[a * TH_HANDS] = e;
             S += e;
         }
         const T inv = T(1) / S;
         for (int a = 0; a < n; ++a) col[a * TH_HANDS] *= inv;
-        return mn - beta * log(S);
+        return -beta * (m + log(S));
     }
     if (mode == TM_BR) {
         int best = 0;
@@ -837,36 +840,41 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
         T mn = x[0];
 #pragma unroll
         for (int a = 1; a < N; ++a) mn = fmin(mn, x[a]);
-        T S = T(0);
+        T S = T(0), e[N];
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            x[a] = exp_nonpos((mn - x[a]) * iw, C.exptab);
-            S += x[a];
+            x[a] = (mn - x[a]) * iw;  // log qbar_a + log S
+            e[a] = exp_nonpos(x[a], C.exptab);
+            S += e[a];
         }
-        const T inv = rcp_pos(S);
+        const T inv = rcp_pos(S), lS = log_ge1(S, C.exptab);
+        if (C.lbo) {
 #pragma unroll
-        for (int a = 0; a < N; ++a) x[a] *= inv;
-        value = mn - wgt * (log_ge1(S, C.exptab) - logn);
+            for (int a = 0; a < N; ++a) C.lbo[(size_t)(first + a) * Hp + h] = x[a] - lS;
+        }
+#pragma unroll
+        for (int a = 0; a < N; ++a) x[a] = e[a] * inv;
+        value = mn - wgt * (lS - logn);
     } else if (mode == TM_PROX) {
+        // centre by its behavioural logs (R16): qbar_a ~ exp(lb_a - g_a / beta)
         const T beta = wgt, ib = iw;
         const T* __restrict__ zr = cz + (size_t)first * Hp + h;
-        T z[N];
+        T m = -big_value<T>();
 #pragma unroll
-        for (int a = 0; a < N; ++a) z[a] = zr[(size_t)a * Hp];
-        T mn = big_value<T>();
-#pragma unroll
-        for (int a = 0; a < N; ++a)
-            if (z[a] > T(0)) mn = fmin(mn, x[a]);
+        for (int a = 0; a < N; ++a) {
+            x[a] = zr[(size_t)a * Hp] - x[a] * ib;
+            m = fmax(m, x[a]);
+        }
         T S = T(0);
 #pragma unroll
         for (int a = 0; a < N; ++a) {
-            x[a] = z[a] > T(0) ? z[a] * exp_nonpos((mn - x[a]) * ib, C.exptab) : T(0);
+            x[a] = exp_nonpos(x[a] - m, C.exptab);
             S += x[a];
         }
         const T inv = rcp_pos(S);
 #pragma unroll
         for (int a = 0; a < N; ++a) x[a] *= inv;
-        value = mn - beta * log(S);
+        value = -beta * (m + log_ge1(S, C.exptab));
     } else if (mode == TM_BR) {
         int best = 0;
         T mn = x[0];
@@ -938,6 +946,7 @@ __device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const Dev
 template <class T>
 struct TreeDownCtx {
     T tau, alpha;
+    const double* __restrict__ exptab;
     const T* __restrict__ bin;
     const T* __restrict__ ci;
     T* __restrict__ ob;
@@ -947,12 +956,12 @@ struct TreeDownCtx {
 };
 
 // OUTS: the set of output rows (TO_* bits) fixed at compile time, or 0 = decided at run time
-enum TreeOuts { TO_B = 1, TO_Q = 2, TO_COMB = 4, TO_AVG = 8, TO_FUSEBR = 16 };
+enum TreeOuts { TO_B = 1, TO_Q = 2, TO_COMB = 4, TO_AVG = 8, TO_FUSEBR = 16, TO_LB = 32 };
 
 template <int N, int MODE, int OUTS, class T>
 __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool ok, T qp, T unif, int first,
                                                  T* col, int h, int Hp) {
-    const bool wb = OUTS ? (OUTS & TO_B) != 0 : D.ob != nullptr;  // (TO_FUSEBR is a bottom-up flag)
+    const bool wb = OUTS ? (OUTS & TO_B) != 0 : D.ob != nullptr;  // (TO_FUSEBR, TO_LB: bottom-up flags)
     const bool wq = OUTS ? (OUTS & TO_Q) != 0 : D.oq != nullptr;
     const bool wc = OUTS ? (OUTS & TO_COMB) != 0 : D.co != nullptr;
     const bool wa = OUTS ? (OUTS & TO_AVG) != 0 : D.av != nullptr;
@@ -962,7 +971,7 @@ __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool o
     for (int a = 0; a < N; ++a) {
         if (!ok) b[a] = T(0);
         else if (MODE == TM_UNIFORM) b[a] = unif;
-        else if (MODE == TM_COMBINE) b[a] = D.bin[ix0 + (size_t)a * Hp];
+        else if (MODE == TM_COMBINE) b[a] = exp_nonpos(D.bin[ix0 + (size_t)a * Hp], D.exptab);  // centre: log qbar
         else b[a] = col[a * TH_HANDS];
         cv[a] = wc ? D.ci[ix0 + (size_t)a * Hp] : T(0);
         avv[a] = wa ? D.av[ix0 + (size_t)a * Hp] : T(0);
@@ -1130,6 +1139,10 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
     }
     C.mu = (mode == TM_SBR) ? (T)A.mu[g] : T(1);
     C.exptab = s_exptab;
+    // the smoothed response's behavioural logs (R16), written during the bottom-up
+    T* __restrict__ lbo = nullptr;
+    if (mode == TM_SBR && (OUTS ? (OUTS & TO_LB) != 0 : A.out_lb.ok())) lbo = A.out_lb.at<T>(g);
+    C.lbo = lbo;
     T* __restrict__ cz = A.center.ok() ? A.center.at<T>(g) : nullptr;
     T* __restrict__ rg = A.regret.ok() ? A.regret.at<T>(g) : nullptr;
     if (has_grad) {
@@ -1157,6 +1170,8 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
                         value = tree_node_up_any<MODE, T>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
                     } else {
                         for (int a = 0; a < n; ++a) col[a * TH_HANDS] = T(0);
+                        if (lbo && h < Hp)
+                            for (int a = 0; a < n; ++a) lbo[(size_t)(first + a) * Hp + h] = T(0);
                     }
                     if (rs >= 0) rootv[rs * TH_HANDS + c] = value;
                     else tile[par * TH_HANDS + c] += value * inv_sc;
@@ -1185,10 +1200,11 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
     }
 
     // ---- top-down, shallowest level first
-    const bool want_td = OUTS ? true : (A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR);
+    const bool want_td = OUTS ? (OUTS & ~(TO_FUSEBR | TO_LB)) != 0
+                              : (A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR);
     if (!want_td) return;
     T* __restrict__ ob = A.out_b.ok() ? A.out_b.at<T>(g) : nullptr;
-    if ((OUTS & ~TO_FUSEBR) == TO_B && has_grad) {
+    if ((OUTS & ~(TO_FUSEBR | TO_LB)) == TO_B && has_grad) {
         // behavioural output only: after the bottom-up every action column of the tile holds its
         // b (0 where the hand is blocked or past H), so no level-by-level descent is needed --
         // one coalesced row-by-row copy, row 0 = 1 for live hands.
@@ -1212,6 +1228,7 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
     TreeDownCtx<T> Dn;
     Dn.tau = tau;
     Dn.alpha = alpha;
+    Dn.exptab = s_exptab;
     Dn.bin = bin;
     Dn.ci = ci;
     Dn.ob = ob;
@@ -1266,7 +1283,8 @@ cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const 
     dim3 grid((G.H_pad + TH_HANDS - 1) / TH_HANDS, G.n_games);
     const size_t sm = tree_smem_bytes(P, G.esz);
     const int outs = (A.out_b.ok() ? TO_B : 0) | (A.out_q.ok() ? TO_Q : 0) | (A.comb_out.ok() ? TO_COMB : 0) |
-                     (A.avg.ok() ? TO_AVG : 0);
+                     (A.avg.ok() ? TO_AVG : 0) | (A.out_lb.ok() ? TO_LB : 0);
+    if (A.out_lb.ok() && A.mode != TM_SBR) return cudaErrorInvalidValue;
 #define EGT_TREE_GO(M, O)                                                                       \
     {                                                                                           \
         if (G.esz == 4) tree_kernel<float, M, O><<<grid, TH_NT, sm, st>>>(G, P, player, A);     \
@@ -1274,11 +1292,11 @@ cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const 
         return cudaGetLastError();                                                              \
     }
     if (A.br_value) {  // the fused stopping test exists for the excessive-gap check's SBR only
-        if (A.mode != TM_SBR || outs != TO_B) return cudaErrorInvalidValue;
-        EGT_TREE_GO(TM_SBR, TO_B | TO_FUSEBR)
+        if (A.mode != TM_SBR || outs != TO_LB) return cudaErrorInvalidValue;
+        EGT_TREE_GO(TM_SBR, TO_LB | TO_FUSEBR)
     }
     // the solver's hot (mode, outputs) combinations get fully specialised kernels
-    if (A.mode == TM_SBR && outs == TO_B) EGT_TREE_GO(TM_SBR, TO_B)
+    if (A.mode == TM_SBR && outs == TO_LB) EGT_TREE_GO(TM_SBR, TO_LB)
     if (A.mode == TM_SBR && outs == (TO_Q | TO_COMB)) EGT_TREE_GO(TM_SBR, TO_Q | TO_COMB)
     if (A.mode == TM_PROX && outs == TO_COMB) EGT_TREE_GO(TM_PROX, TO_COMB)
     if (A.mode == TM_COMBINE && outs == TO_COMB) EGT_TREE_GO(TM_COMBINE, TO_COMB)
@@ -1308,21 +1326,14 @@ static cudaError_t prepare_t() {
     cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, 3, T>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 2, -1, T>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(grad_staged_kernel<STG_NT, STG_K, STG_CH, 1, -1, T>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        e = cudaFuncSetAttribute(grad_card_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     const void* tk[] = {(const void*)tree_kernel<T, TM_SBR, 0>,     (const void*)tree_kernel<T, TM_PROX, 0>,
                         (const void*)tree_kernel<T, TM_BR, 0>,      (const void*)tree_kernel<T, TM_CFR, 0>,
                         (const void*)tree_kernel<T, TM_UNIFORM, 0>, (const void*)tree_kernel<T, TM_COMBINE, 0>,
-                        (const void*)tree_kernel<T, TM_SBR, TO_B>,  (const void*)tree_kernel<T, TM_SBR, TO_Q | TO_COMB>,
+                        (const void*)tree_kernel<T, TM_SBR, TO_LB>, (const void*)tree_kernel<T, TM_SBR, TO_Q | TO_COMB>,
                         (const void*)tree_kernel<T, TM_PROX, TO_COMB>, (const void*)tree_kernel<T, TM_COMBINE, TO_COMB>,
                         (const void*)tree_kernel<T, TM_CFR, TO_Q | TO_AVG>,
-                        (const void*)tree_kernel<T, TM_SBR, TO_B | TO_FUSEBR>};
+                        (const void*)tree_kernel<T, TM_SBR, TO_LB | TO_FUSEBR>};
     for (const void* f : tk)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     return e;
@@ -1410,6 +1421,53 @@ __global__ void gap_combine_kernel(int n, const double* __restrict__ val, double
 
 cudaError_t launch_gap_combine(int n, const double* val, double* out, cudaStream_t st) {
     gap_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, val, out);
+    return cudaGetLastError();
+}
+
+// The practical-mu scan of egt_init (R14), one thread per game.  phase 0: before
+// trial k, the trial mu = mu_theory * 2^-k of the games still scanning; phase 1: after it, the
+// EGC at the trial's initial point (EGV = val[g] + val[n + g] >= 0) keeps k, else the scan of
+// that game ends; phase 2: mu = mu_theory * 2^-k for the last k that kept it.
+__global__ void mu_scan_kernel(int n, int k, int phase, const double* __restrict__ mu_th, double* mu, int* scan,
+                               int* kbest, const double* __restrict__ val) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    if (phase == 0) {
+        if (scan[g]) {
+            mu[g] = mu_th[g] * ldexp(1.0, -k);
+            mu[n + g] = mu_th[n + g] * ldexp(1.0, -k);
+        }
+    } else if (phase == 1) {
+        if (scan[g]) {
+            if (val[g] + val[n + g] >= 0.0) kbest[g] = k;  // Alg. 4's test, EGV >= 0 (R8)
+            else scan[g] = 0;
+        }
+    } else {
+        mu[g] = mu_th[g] * ldexp(1.0, -kbest[g]);
+        mu[n + g] = mu_th[n + g] * ldexp(1.0, -kbest[g]);
+    }
+}
+
+cudaError_t launch_mu_scan(int n, int k, int phase, const double* mu_th, double* mu, int* scan, int* kbest,
+                           const double* val, cudaStream_t st) {
+    mu_scan_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, k, phase, mu_th, mu, scan, kbest, val);
+    return cudaGetLastError();
+}
+
+// Emulated all-reduce (egt_shard_emulate): every buffer becomes the elementwise sum of the
+// `world` buffers, in rank order.
+template <class T>
+__global__ void emu_allreduce_kernel(double* const* __restrict__ bufs, int world, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        T s = T(0);
+        for (int r = 0; r < world; ++r) s += reinterpret_cast<const T*>(bufs[r])[i];
+        for (int r = 0; r < world; ++r) reinterpret_cast<T*>(bufs[r])[i] = s;
+    }
+}
+
+cudaError_t launch_emu_allreduce(double* const* bufs, int world, size_t n, int esz, cudaStream_t st) {
+    if (esz == 4) emu_allreduce_kernel<float><<<148 * 8, 256, 0, st>>>(bufs, world, n);
+    else emu_allreduce_kernel<double><<<148 * 8, 256, 0, st>>>(bufs, world, n);
     return cudaGetLastError();
 }
 

@@ -45,6 +45,11 @@ struct DevGame {
     const uint16_t* tab_cent; // [G*n_bs][n_ce]      card array (CE_* packing, game.h)
     const uint2* tab_pcard;   // [G*n_bs][H_pad]     per position, per card: segment info (PC_*)
     const uint8_t* tab_valid; // [G*n_bs][H_pad]
+    // card-domain river gradient plan (game.h CardPlan), one per game; card_plan = 0: none
+    int card_plan;
+    const uint32_t* card_pw;    // [G][CARD_NP]
+    const uint32_t* card_pr;    // [G][CARD_NP]
+    const uint32_t* card_lane;  // [G][CARD_NT][8]
     const void* prior[2];     // [G][H_pad] in the game's precision
     const double* kappa_game; // [G]
     const DevTerm* terms;
@@ -92,13 +97,14 @@ struct TreeArgs {
     VecRef g;                  // gradient input (SBR/PROX/BR/CFR)
     double gsign = 1.0;        // objective uses gsign * g (min form; CFR: utility)
     const double* mu = nullptr;     // SBR: per-game mu; PROX: per-game step s
-    VecRef center;             // PROX: centre (behavioural); CFR: current z (in/out); COMBINE: behavioural input
+    VecRef center;             // PROX: centre (behavioural logs); CFR: current z (in/out); COMBINE: behavioural logs
     VecRef regret;             // CFR
     VecRef avg;                // CFR: running average (sequence form, in/out)
     const int* iter = nullptr; // CFR: per-game t (1-based)
     int cfr_plus = 0;          // CFR: 1 = RM+ threshold
     int avg_linear = 0;        // CFR: 1 = alpha_t = 2t/(t^2+t), else 1/t
     VecRef out_b;              // behavioural output
+    VecRef out_lb;             // SBR: log of the behavioural output (prox centres, R16)
     VecRef out_q;              // sequence-form output
     VecRef comb_in, comb_out;  // comb_out = (1 - tau) comb_in + tau q
     const double* tau = nullptr;
@@ -147,5 +153,9 @@ cudaError_t launch_egt_accept(int variant, int n_games, DevScalars S, cudaStream
 cudaError_t launch_tick(int n_games, int* t, const int* live, cudaStream_t st);  // live: nullptr = all
 cudaError_t launch_stop_at_target(int n_games, const double* gap, const double* target, int* live, cudaStream_t st);
 cudaError_t launch_gap_combine(int n, const double* val, double* out, cudaStream_t st);
+constexpr int EGT_MU_SCAN_KMAX = 30;  // the practical-mu scan tries mu_theory * 2^-k, k = 0..30
+cudaError_t launch_mu_scan(int n, int k, int phase, const double* mu_th, double* mu, int* scan, int* kbest,
+                           const double* val, cudaStream_t st);
+cudaError_t launch_emu_allreduce(double* const* bufs, int world, size_t n, int esz, cudaStream_t st);
 
 }  // namespace egt

@@ -28,3 +28,15 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+def pytest_terminal_summary(terminalreporter):
+    """Worst per-element relative CUDA-vs-oracle error of each parity check this session."""
+    try:
+        from tests.paritylib import REPORT
+    except Exception:
+        return
+    if REPORT:
+        terminalreporter.write_sep("-", "parity: worst per-element relative error (entries >= 1e-6 max)")
+        for k in sorted(REPORT):
+            terminalreporter.write_line("%-48s %.3e" % (k, REPORT[k]))

@@ -106,3 +106,47 @@ def random_behavioral(tp, rng, spread=1.0):
 def rel_err(got, want):
     scale = max(np.abs(want).max(), 1e-300)
     return np.abs(got - want).max() / scale
+
+
+# Worst per-element relative errors seen by assert_parity, by check name (printed at the end
+# of the session by tests/conftest.py).
+REPORT = {}
+
+FLOOR64, FLOOR32 = 1e-13, 1e-6
+
+
+def assert_parity(got, want, rtol, what, floor=None, mask=None):
+    """BASELINE.json north_star's bar, per element: |got - want| <= rtol * |want|, with an
+    absolute floor of floor * max|want| for entries that cancel to ~0 (a showdown entry is a
+    difference of prefix sums as large as the largest entry, so its rounding is ~ulp of the
+    largest entry, not of itself): floor = 1e-13 in fp64 (~450 ulp of the largest entry),
+    1e-6 in fp32 (~17 ulp).  Records the worst relative error among entries >= 1e-6 max|want|."""
+    got = np.asarray(got, dtype=float).ravel()
+    want = np.asarray(want, dtype=float).ravel()
+    if mask is not None:
+        got, want = got[np.asarray(mask).ravel()], want[np.asarray(mask).ravel()]
+    assert got.shape == want.shape
+    if floor is None:
+        floor = FLOOR64 if rtol < 1e-7 else FLOOR32
+    scale = np.abs(want).max() if want.size else 0.0
+    err = np.abs(got - want)
+    bad = ~(err <= rtol * np.abs(want) + floor * scale)
+    if bad.any():
+        i = int(np.argmax(np.where(bad, err / np.maximum(np.abs(want), 1e-300), -1.0)))
+        raise AssertionError("%s: %d of %d entries off (worst: got %r want %r, |want|max %g)"
+                             % (what, int(bad.sum()), got.size, got[i], want[i], scale))
+    big = np.abs(want) >= 1e-6 * scale
+    worst = float((err[big] / np.abs(want[big])).max()) if big.any() and scale > 0 else 0.0
+    key = what.split("[")[0]
+    REPORT[key] = max(REPORT.get(key, 0.0), worst)
+    return worst
+
+
+def assert_scalar(got, want, rtol, what, floor=1e-12):
+    """Per-game values / eps_sad: |got - want| <= rtol * |want| + floor (payoff units)."""
+    got, want = float(got), float(want)
+    if not abs(got - want) <= rtol * abs(want) + floor:
+        raise AssertionError("%s: got %r want %r" % (what, got, want))
+    key = what.split("[")[0]
+    if want != 0:
+        REPORT[key] = max(REPORT.get(key, 0.0), abs(got - want) / abs(want))

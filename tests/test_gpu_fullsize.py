@@ -11,7 +11,7 @@ import pytest
 
 from oracle import br, cfr, dgf, egt
 from paper_1810_03063_b200 import workloads
-from tests.paritylib import Pair, random_behavioral, rel_err
+from tests.paritylib import Pair, assert_parity, assert_scalar, random_behavioral
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -66,7 +66,7 @@ def test_bench_workload_gradient(bench_pair, p):
         want = sf.Ay(vals[g]) if p == 0 else sf.ATx(vals[g])
         got = pair.from_product(g, p, out[g])
         got[0] = out[g][:G.H_pad].sum()
-        assert rel_err(got, want) <= TOL
+        assert_parity(got, want, TOL, "bench-batch gradient")
 
 
 def test_bench_workload_sbr_and_br(bench_pair):
@@ -92,9 +92,9 @@ def test_bench_workload_sbr_and_br(bench_pair):
         q, vals, bvals = host(dq).reshape(G.n_games, -1), host(val), host(bval)
         for g in SAMPLE:
             (wq, wv), wb = wants[g]
-            assert np.abs(pair.from_product(g, p, q[g])[1:] - wq[1:]).max() <= TOL
-            assert abs(vals[g] - wv) <= TOL * max(1.0, abs(wv))
-            assert abs(bvals[g] - wb) <= TOL * max(1.0, abs(wb))
+            assert_parity(pair.from_product(g, p, q[g])[1:], wq[1:], TOL, "bench-batch sbr q")
+            assert_scalar(vals[g], wv, TOL, "bench-batch sbr value")
+            assert_scalar(bvals[g], wb, TOL, "bench-batch br value")
 
 
 def test_bench_workload_egt_as_iterations(bench_pair):
@@ -118,10 +118,10 @@ def test_bench_workload_egt_as_iterations(bench_pair):
     for _ in range(int(sc[g, 3])):
         egt.egt_iteration(prob, st, "as")
     assert int(sc[g, 3]) + int(sc[g, 5]) == 2 and st.backtracks == int(sc[g, 5])
-    assert np.abs(pair.from_product(g, 0, host(xs).reshape(G.n_games, -1)[g])[1:] - st.x[1:]).max() <= TOL
-    assert np.abs(pair.from_product(g, 1, host(ys).reshape(G.n_games, -1)[g])[1:] - st.y[1:]).max() <= TOL
+    assert_parity(pair.from_product(g, 0, host(xs).reshape(G.n_games, -1)[g])[1:], st.x[1:], TOL, "bench-batch egt/as x")
+    assert_parity(pair.from_product(g, 1, host(ys).reshape(G.n_games, -1)[g])[1:], st.y[1:], TOL, "bench-batch egt/as y")
     want = br.saddle_gap(sf, st.x, st.y)
-    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+    assert_scalar(gaps[g], want, TOL, "bench-batch egt/as eps_sad")
     assert np.all(gaps >= -1e-9 * np.abs(gaps).max())
 
 
@@ -138,10 +138,10 @@ def test_bench_workload_cfr_plus(bench_pair):
         avg.append(pair.from_product(g, p, host(d).reshape(G.n_games, -1)[g]))
     gaps = G.saddle_gap(1)
     st = cfr.run(pair.sf[g], "cfr_plus", 2)
-    assert np.abs(avg[0][1:] - st.xbar[1:]).max() <= TOL
-    assert np.abs(avg[1][1:] - st.ybar[1:]).max() <= TOL
+    assert_parity(avg[0][1:], st.xbar[1:], TOL, "bench-batch cfr+ xbar")
+    assert_parity(avg[1][1:], st.ybar[1:], TOL, "bench-batch cfr+ ybar")
     want = br.saddle_gap(pair.sf[g], st.xbar, st.ybar)
-    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+    assert_scalar(gaps[g], want, TOL, "bench-batch cfr+ eps_sad")
 
 
 # ------------------------------------------------------------------ edge cases
@@ -159,7 +159,7 @@ def _gradient_parity(pair, games=None):
             want = sf.Ay(vals[g]) if p == 0 else sf.ATx(vals[g])
             got = pair.from_product(g, p, out[g])
             got[0] = out[g][:G.H_pad].sum()
-            assert rel_err(got, want) <= TOL, (p, g)
+            assert_parity(got, want, TOL, "edge-case gradient")
             assert np.all(out[g][G.H:G.H_pad] == 0.0)
 
 
@@ -209,8 +209,8 @@ def test_reduced_decks_ragged_tiles(n_ranks, n_suits):
         G.egt_smoothed_br(p, dev(np.stack(gs).reshape(G.vec_shape(p))), gsign, dev(mus), dq, None, val)
         q, vals = host(dq).reshape(G.n_games, -1), host(val)
         for g in range(G.n_games):
-            assert np.abs(pair.from_product(g, p, q[g])[1:] - wants[g][0][1:]).max() <= TOL
-            assert abs(vals[g] - wants[g][1]) <= TOL * max(1.0, abs(wants[g][1]))
+            assert_parity(pair.from_product(g, p, q[g])[1:], wants[g][0][1:], TOL, "edge-case sbr q")
+            assert_scalar(vals[g], wants[g][1], TOL, "edge-case sbr value")
 
 
 @pytest.mark.parametrize("variant", ["cfr_rm", "cfr_rmp"])
@@ -229,10 +229,10 @@ def test_bench_workload_cfr_variants(bench_pair, variant):
         avg.append(pair.from_product(g, p, host(d).reshape(G.n_games, -1)[g]))
     gaps = G.saddle_gap(1)
     st = cfr.run(pair.sf[g], variant, 2)
-    assert np.abs(avg[0][1:] - st.xbar[1:]).max() <= TOL
-    assert np.abs(avg[1][1:] - st.ybar[1:]).max() <= TOL
+    assert_parity(avg[0][1:], st.xbar[1:], TOL, "bench-batch cfr avg x")
+    assert_parity(avg[1][1:], st.ybar[1:], TOL, "bench-batch cfr avg y")
     want = br.saddle_gap(pair.sf[g], st.xbar, st.ybar)
-    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+    assert_scalar(gaps[g], want, TOL, "bench-batch cfr eps_sad")
 
 
 def test_bench_workload_egt_balanced(bench_pair):
@@ -250,11 +250,11 @@ def test_bench_workload_egt_balanced(bench_pair):
     G.get_strategy_device(0, 0, xs)
     G.get_strategy_device(1, 0, ys)
     st, prob = egt.run(sf, "balanced", 2, mu=mu)
-    assert np.abs(pair.from_product(g, 0, host(xs).reshape(G.n_games, -1)[g])[1:] - st.x[1:]).max() <= TOL
-    assert np.abs(pair.from_product(g, 1, host(ys).reshape(G.n_games, -1)[g])[1:] - st.y[1:]).max() <= TOL
+    assert_parity(pair.from_product(g, 0, host(xs).reshape(G.n_games, -1)[g])[1:], st.x[1:], TOL, "bench-batch egt balanced x")
+    assert_parity(pair.from_product(g, 1, host(ys).reshape(G.n_games, -1)[g])[1:], st.y[1:], TOL, "bench-batch egt balanced y")
     gaps = G.saddle_gap(0)
     want = br.saddle_gap(sf, st.x, st.y)
-    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+    assert_scalar(gaps[g], want, TOL, "bench-batch egt balanced eps_sad")
 
 
 @pytest.mark.parametrize("solver", ["egt_as", "cfr_plus"])
@@ -292,8 +292,8 @@ def test_bench_workload_longer_runs(bench_pair, solver):
         d = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
         G.get_strategy_device(p, which, d)
         got.append(pair.from_product(g, p, host(d).reshape(G.n_games, -1)[g]))
-    assert np.abs(got[0][1:] - want_x[1:]).max() <= TOL
-    assert np.abs(got[1][1:] - want_y[1:]).max() <= TOL
+    assert_parity(got[0][1:], want_x[1:], TOL, "bench-batch long-run x")
+    assert_parity(got[1][1:], want_y[1:], TOL, "bench-batch long-run y")
     gaps = G.saddle_gap(which)
     want = br.saddle_gap(sf, want_x, want_y)
-    assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+    assert_scalar(gaps[g], want, TOL, "bench-batch long-run eps_sad")

@@ -9,7 +9,7 @@ import pytest
 
 from oracle import egt
 from paper_1810_03063_b200 import workloads
-from tests.paritylib import Pair, random_behavioral, rel_err
+from tests.paritylib import Pair, assert_parity, assert_scalar, random_behavioral
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -53,7 +53,7 @@ def test_random_river_configurations(case):
             want = pair.sf[g].Ay(vals[g]) if p == 0 else pair.sf[g].ATx(vals[g])
             got = pair.from_product(g, p, out[g])
             got[0] = out[g][:G.H_pad].sum()
-            assert rel_err(got, want) <= TOL, (case, p, g)
+            assert_parity(got, want, TOL, "fuzz gradient")
     # one EGT/as iteration from an explicit mu, game 1
     import paper_1810_03063_b200 as P
     sf = pair.sf[1]
@@ -69,7 +69,7 @@ def test_random_river_configurations(case):
     for _ in range(int(sc[1, 3])):
         egt.egt_iteration(prob, st, "as")
     got = pair.from_product(1, 0, xs.cpu().numpy().reshape(G.n_games, -1)[1])
-    assert np.abs(got[1:] - st.x[1:]).max() <= TOL
+    assert_parity(got[1:], st.x[1:], TOL, "fuzz egt/as x")
 
 
 @pytest.mark.parametrize("case", range(8))
@@ -91,7 +91,7 @@ def test_random_configurations_cfr_and_fp32(case):
         d = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
         G.get_strategy_device(p, 1, d)
         got = pair.from_product(0, p, d.cpu().numpy().reshape(G.n_games, -1)[0])
-        assert np.abs(got[1:] - want[1:]).max() <= TOL, (case, p)
+        assert_parity(got[1:], want[1:], TOL, "fuzz cfr+ avg")
     G32 = P.Game(P.RIVER, n_games=2, river=spec, boards=pair.boards, prior1=pair.priors[0], prior2=pair.priors[1],
                  n_ranks=n_ranks, n_suits=n_suits, precision="f32")
     for p in (0, 1):
@@ -108,5 +108,5 @@ def test_random_configurations_cfr_and_fp32(case):
         want = pair.sf[0].Ay(v) if p == 0 else pair.sf[0].ATx(v)
         got = pair.from_product(0, p, out)
         got[0] = out[:G.H_pad].sum()
-        assert rel_err(got, want) <= 1e-5, (case, p)
+        assert_parity(got, want, 1e-5, "fuzz fp32 gradient")
     G32.close()

@@ -1,16 +1,15 @@
 """Parity of the CUDA path (through the C ABI) with the CPU oracle, element by element.
 
-Tolerance: fp64 end to end; a vector result must
-satisfy max|cuda - oracle| <= 1e-9 * max|oracle| (norm-relative: the gradient's
-showdown terms are differences of prefix sums, so per-element relative error is
-not meaningful where an entry cancels to ~0); strategies (entries in [0, 1]) and
-scalar values to 1e-9 relative.  Integer/index work (layout) is compared exactly.
+Tolerance: fp64 end to end; every element of a vector
+result within 1e-9 relative of the oracle's, with an absolute floor of 1e-13 * max|oracle|
+for entries that cancel to ~0 (paritylib.assert_parity); per-game values and eps_sad 1e-9
+relative.  Integer/index work (layout) is compared exactly.
 """
 import numpy as np
 import pytest
 
 from oracle import br, cfr, dgf, egt
-from tests.paritylib import Pair, random_behavioral, rel_err
+from tests.paritylib import Pair, assert_parity, assert_scalar, random_behavioral
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -71,7 +70,7 @@ def test_gradient(pair, p):
     for g in range(G.n_games):
         got = pair.from_product(g, p, out[g])
         got[0] = out[g][:G.H_pad].sum()
-        assert rel_err(got, wants[g]) <= TOL
+        assert_parity(got, wants[g], TOL, "gradient[%s]" % pair.kind)
         invalid = ~pair.valid_mask(g, p)
         invalid[:G.H_pad] = False
         assert np.all(out[g][invalid] == 0.0)
@@ -91,22 +90,29 @@ def test_smoothed_best_response(pair, p, gsign):
         blk[0] = v[0]  # empty-sequence term on one hand column
         gs.append(blk)
         mus.append(mu)
-        wants.append(dgf.smoothed_best_response(tp, gsign * v, mu))
+        wants.append(dgf.smoothed_best_response(tp, gsign * v, mu, behavioral=True))
     dq = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
     db = torch.zeros_like(dq)
     val = torch.zeros(G.n_games, dtype=torch.float64, device="cuda")
-    G.egt_smoothed_br(p, dev(stack(pair, p, gs)), gsign, dev(mus), dq, db, val)
+    dlb = torch.zeros_like(dq)
+    G.egt_smoothed_br(p, dev(stack(pair, p, gs)), gsign, dev(mus), dq, db, val, lb=dlb)
     q = host(dq).reshape(G.n_games, -1)
+    b = host(db).reshape(G.n_games, -1)
+    lb = host(dlb).reshape(G.n_games, -1)
     vals = host(val)
     for g in range(G.n_games):
-        wq, wv = wants[g]
-        assert np.abs(pair.from_product(g, p, q[g])[1:] - wq[1:]).max() <= TOL
-        assert abs(vals[g] - wv) <= TOL * max(1.0, abs(wv))
+        wq, wv, wb, wlb = wants[g]
+        assert_parity(pair.from_product(g, p, q[g])[1:], wq[1:], TOL, "sbr q[%s]" % pair.kind)
+        assert_parity(pair.from_product(g, p, b[g])[1:], wb[1:], TOL, "sbr b[%s]" % pair.kind)
+        assert_parity(pair.from_product(g, p, lb[g])[1:], wlb[1:], TOL, "sbr log b[%s]" % pair.kind)
+        assert_scalar(vals[g], wv, TOL, "sbr value[%s]" % pair.kind)
 
 
 # ------------------------------------------------------------------ prox mapping
-@pytest.mark.parametrize("p,gsign", [(0, 1.0), (1, -1.0)])
-def test_prox(pair, p, gsign):
+@pytest.mark.parametrize("p,gsign,far", [(0, 1.0, False), (1, -1.0, False), (0, 1.0, True), (1, -1.0, True)])
+def test_prox(pair, p, gsign, far):
+    """Centres given by their behavioural logs (R16); `far`: entries at log ~ -800
+    (underflowing probabilities, the practical-mu regime) pulled back by large gradients."""
     G = pair.game
     rng = np.random.default_rng(30 + p)
     gs, steps, cbs, wants = [], [], [], []
@@ -114,17 +120,28 @@ def test_prox(pair, p, gsign):
         tp = pair.tp(g, p)
         v = rng.standard_normal(tp.n_seq)
         s = float(np.exp(rng.uniform(-2, 1)))
-        zb = random_behavioral(tp, rng, spread=1.5)
-        z = tp.behavioral_to_sequence(zb)
+        lb = np.log(random_behavioral(tp, rng, spread=1.5))
+        if far:  # centres at the bench's operating point: behavioural probabilities ~e^-800
+            for j in range(tp.n_simplex):
+                st_, n_ = tp.start[j], tp.size[j]
+                t = lb[st_:st_ + n_].copy()
+                keep = int(np.argmax(t))
+                for i in range(n_):
+                    if i != keep and rng.random() < 0.4:
+                        t[i] -= 800.0
+                        if rng.random() < 0.7:  # and a gradient that pulls it back into play
+                            v[st_ + i] = 0.99 * t[i] * tp.beta[j] / (s * gsign)
+                m = t.max()
+                lb[st_:st_ + n_] = t - (m + np.log(np.exp(t - m).sum()))
         gs.append(pair.to_product(g, p, v))
         steps.append(s)
-        cbs.append(pair.to_product(g, p, zb, row0=1.0))
-        wants.append(dgf.prox_mapping(tp, s * gsign * v, z))
+        cbs.append(pair.to_product(g, p, lb))
+        wants.append(dgf.prox_mapping(tp, s * gsign * v, lb_prev=lb))
     dq = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
     G.egt_prox(p, dev(stack(pair, p, gs)), gsign, dev(steps), dev(stack(pair, p, cbs)), dq)
     q = host(dq).reshape(G.n_games, -1)
     for g in range(G.n_games):
-        assert np.abs(pair.from_product(g, p, q[g])[1:] - wants[g][1:]).max() <= TOL
+        assert_parity(pair.from_product(g, p, q[g])[1:], wants[g][1:], TOL, "prox[%s]" % pair.kind)
 
 
 # ------------------------------------------------------------------ best response
@@ -145,7 +162,7 @@ def test_best_response(pair, p):
         G.egt_best_response(p, dev(stack(pair, p, gs)), gsign, val)
         got = host(val)
         for g in range(G.n_games):
-            assert abs(got[g] - wants[g][k]) <= TOL * max(1.0, abs(wants[g][k]))
+            assert_scalar(got[g], wants[g][k], TOL, "br value[%s]" % pair.kind)
 
 
 # ------------------------------------------------------------------ solvers
@@ -192,11 +209,14 @@ def test_egt_iterates(pair, variant, iters):
             assert st.backtracks == int(sc[g, 5])
         else:
             assert accepted == iters
-        assert np.abs(x_all[g][1:] - st.x[1:]).max() <= TOL
-        assert np.abs(y_all[g][1:] - st.y[1:]).max() <= TOL
-        assert abs(sc[g, 0] - st.mu_x) <= TOL * st.mu_x and abs(sc[g, 1] - st.mu_y) <= TOL * st.mu_y
+        assert_parity(x_all[g][1:], st.x[1:], TOL, "egt x[%s]" % pair.kind)
+        assert_parity(y_all[g][1:], st.y[1:], TOL, "egt y[%s]" % pair.kind)
+        assert_scalar(sc[g, 0], st.mu_x, TOL, "egt mu", floor=0)
+        assert_scalar(sc[g, 1], st.mu_y, TOL, "egt mu", floor=0)
+        if variant == "as":  # theory / balanced use tau_t = 2/(t+3), not the EGT/as state's tau
+            assert_scalar(sc[g, 2], st.tau, TOL, "egt tau", floor=0)
         want_gap = br.saddle_gap(sf, st.x, st.y)
-        assert abs(gaps[g] - want_gap) <= TOL * max(1.0, abs(want_gap))
+        assert_scalar(gaps[g], want_gap, TOL, "egt eps_sad[%s]" % pair.kind)
 
 
 @pytest.mark.parametrize("variant", ["cfr_rm", "cfr_rmp", "cfr_plus"])
@@ -212,12 +232,12 @@ def test_cfr_iterates(pair, variant):
     gaps = G.saddle_gap(1)
     for g in range(G.n_games):
         st = cfr.run(pair.sf[g], variant, iters)
-        assert np.abs(cur[0][g][1:] - st.x[1:]).max() <= TOL
-        assert np.abs(cur[1][g][1:] - st.y[1:]).max() <= TOL
-        assert np.abs(avg[0][g][1:] - st.xbar[1:]).max() <= TOL
-        assert np.abs(avg[1][g][1:] - st.ybar[1:]).max() <= TOL
+        assert_parity(cur[0][g][1:], st.x[1:], TOL, "cfr x[%s]" % pair.kind)
+        assert_parity(cur[1][g][1:], st.y[1:], TOL, "cfr y[%s]" % pair.kind)
+        assert_parity(avg[0][g][1:], st.xbar[1:], TOL, "cfr xbar[%s]" % pair.kind)
+        assert_parity(avg[1][g][1:], st.ybar[1:], TOL, "cfr ybar[%s]" % pair.kind)
         want = br.saddle_gap(pair.sf[g], st.xbar, st.ybar)
-        assert abs(gaps[g] - want) <= TOL * max(1.0, abs(want))
+        assert_scalar(gaps[g], want, TOL, "cfr eps_sad[%s]" % pair.kind)
 
 
 def test_avg_strategy_canonical_layout(pair):

@@ -159,3 +159,62 @@ def test_fused_allgather_solver_one_rank():
             G.timing(False)
             assert kt["comm"][1] >= 4 and kt["comm"][3] == 0      # barriers, no all-reduced bytes
     assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+# ------------------------------------------------------------------ emulated ranks, whole solver
+@pytest.mark.parametrize("solver", ["egt_as", "cfr_plus"])
+@pytest.mark.parametrize("world,fused", [(2, False), (3, False), (8, False), (2, True), (3, True)])
+def test_emulated_ranks_solver(world, fused, solver):
+    """The sharded SOLVER path on `world` emulated ranks (egt_shard_emulate): every gradient
+    runs each rank's slice kernel into that rank's own (reused) buffer, then the collective
+    (a local sum for the NCCL all-reduce, or the fused kernels' stores into every rank's
+    buffer).  Five EGT/as attempts (30 consecutive gradients) or five CFR+ iterations must equal the unsharded solver bit for bit
+    and the oracle at 1e-9.  Before the non-owned rows were zeroed, the all-reduce variant
+    summed stale rows of the previous gradient from the second gradient on."""
+    import paper_1810_03063_b200 as P
+    from oracle import br, cfr, egt
+    from tests.paritylib import assert_parity, assert_scalar
+    spec = workloads.river_spec("tiny", pot=2, stack=6, raise_cap=2)
+    pair = Pair("river", n_games=2, spec=spec, seed=21)
+    runs = []
+    for emulate in (False, True):
+        G = P.Game(P.RIVER, n_games=2, river=spec, boards=pair.boards, prior1=pair.priors[0],
+                   prior2=pair.priors[1])
+        if emulate:
+            G.shard_emulate(world, fused)
+        if solver == "egt_as":
+            mu = egt.theory_mu(pair.sf[0]) / 8.0
+            G.egt_init(P.EGT_AS, mu, mu)
+            G.egt_step(5)
+            which = 0
+        else:
+            G.cfr_init(P.CFR_PLUS)
+            G.cfr_step(5)
+            which = 1
+        vecs = []
+        for p in (0, 1):
+            d = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
+            G.get_strategy_device(p, which, d)
+            vecs.append(d.cpu().numpy())
+        runs.append((vecs, G.saddle_gap(which), G.egt_scalars()))
+    (v0, g0, s0), (v1, g1, s1) = runs
+    assert all(np.array_equal(a, b) for a, b in zip(v0, v1))
+    assert np.array_equal(g0, g1)
+    cols = slice(0, 7) if solver == "egt_as" else slice(3, 4)  # CFR keeps only t among the scalars
+    assert np.array_equal(s0[:, cols], s1[:, cols])
+    sf = pair.sf[0]
+    if solver == "egt_as":
+        prob = egt.Problem(sf)
+        x, y = egt.initialize(prob, mu, mu)
+        st = egt.EGTState(x, y, mu, mu)
+        for _ in range(int(s1[0, 3])):
+            egt.egt_iteration(prob, st, "as")
+        assert int(s1[0, 5]) == st.backtracks
+        want = (st.x, st.y)
+    else:
+        st = cfr.run(sf, "cfr_plus", 5)
+        want = (st.xbar, st.ybar)
+    for p in (0, 1):
+        assert_parity(pair.from_product(0, p, v1[p].reshape(2, -1)[0])[1:], want[p][1:], 1e-9,
+                      "emulated-rank solver")
+    assert_scalar(g1[0], br.saddle_gap(sf, *want), 1e-9, "emulated-rank solver eps_sad")

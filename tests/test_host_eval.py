@@ -19,3 +19,20 @@ def test_direct_evaluator_matches_subset_maximum(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout
     assert "mismatches 0" in out.stdout
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="needs g++")
+def test_card_plan_conflict_free_and_exact(tmp_path):
+    """The card-domain gradient kernel's host plan (game.cpp build_card_plan) on 48 random
+    river boards (one where every hand ties): every shared-memory exchange is bank-conflict
+    free per half-warp, delivers each slot its hand's weight and each position its own slots,
+    and the run heads / tails / source lanes give the brute-force segment prefixes at the start
+    and end of every tie run (index work: exact)."""
+    exe = tmp_path / "plan_check"
+    csrc = os.path.join(ROOT, "paper_1810_03063_b200", "csrc")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-pthread", "-I", os.path.join(ROOT, "include"), "-I", csrc,
+                    os.path.join(ROOT, "tests", "cpp", "card_plan_check.cpp"), os.path.join(csrc, "game.cpp"),
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "48"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout
+    assert "violations 0" in out.stdout

@@ -55,3 +55,20 @@ def test_binding_fails_loudly_without_device(lib_path):
         pass
     with pytest.raises(P.EGTError):
         P.Game(P.KUHN)
+
+
+def test_every_declaration_cites_its_passage():
+    """SURVEY-less §8(b): each exported call's comment cites the PAPER.md passage that defines
+    the operation (or, for plumbing, the passage whose data it handles)."""
+    src = open(os.path.join(ROOT, "include", "egt_b200.h")).read()
+    decls = [(m.start(), m.group(1)) for m in re.finditer(r"^(?:int|void|const char\*)\s+(\w+)\(", src, re.M)]
+    assert len(decls) == len(header_functions())
+    prev = 0
+    missing = []
+    for pos, name in decls:
+        chunk = src[prev:pos]
+        comment = chunk[chunk.rfind("/*"):] if "/*" in chunk else ""
+        if "PAPER.md:" not in comment:
+            missing.append(name)
+        prev = pos
+    assert not missing, missing
