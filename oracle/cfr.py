@@ -74,9 +74,11 @@ def hand_scales(labels, g):
     return sc
 
 
-def _pass(tp, g, z, r, kind, labels=None):
+def _pass(tp, g, z, r, kind, labels=None, trace=None):
     """Bottom-up pass of Gen-CFR lines 30-33 / 36-39: fold <g^j, z^{j,t-1}> into
-    g_{p_j}, then z^{j,t} = R(g^j)."""
+    g_{p_j}, then z^{j,t} = R(g^j).  trace(j, m, sj): observation only (tests) -- per simplex,
+    m = the smallest |r^t_a| before RM+'s threshold (how close the "[r]^+ / r = 0" decisions of
+    this call came to flipping), sj = max |g^j| (the gains with the values below folded in)."""
     g = np.array(g, dtype=float)
     sc = hand_scales(labels, g) if labels is not None else np.zeros(len(g))
     z = z.copy()
@@ -85,31 +87,37 @@ def _pass(tp, g, z, r, kind, labels=None):
         s, n, p = tp.start[j], tp.size[j], tp.parent[j]
         gj = g[s:s + n]
         g[p] += np.dot(gj, z[s:s + n])
+        if trace is not None:
+            pre = r[s:s + n] + gj - float(np.dot(z[s:s + n], gj))
+            trace(j, float(np.min(np.abs(pre))), float(np.abs(gj).max()))
         r[s:s + n], z[s:s + n] = regret_update(kind, r[s:s + n], z[s:s + n], gj, sc[s])
     return z, r
 
 
-def cfr_iteration(st):
+def cfr_iteration(st, trace=None):
+    """trace(player, j, m, sj): see _pass (observation only)."""
     sf = st.sf
+    tx = None if trace is None else (lambda j, m, gm: trace(0, j, m, gm))
+    ty = None if trace is None else (lambda j, m, gm: trace(1, j, m, gm))
     g = -sf.Ay(st.y)                                   # line 29: g = -A y^{t-1}
     st.grads += 1
-    st.zx, st.rx = _pass(sf.X, g, st.zx, st.rx, st.kind, sf.labels_x)
+    st.zx, st.rx = _pass(sf.X, g, st.zx, st.rx, st.kind, sf.labels_x, tx)
     st.x = sf.X.behavioral_to_sequence(st.zx)
     a = alpha(st.scheme, st.t)
     st.xbar = a * st.x + (1 - a) * st.xbar            # line 34
     g = sf.ATx(st.x)                                   # line 35: g = A^T x^t (alternating)
     st.grads += 1
-    st.zy, st.ry = _pass(sf.Y, g, st.zy, st.ry, st.kind, sf.labels_y)
+    st.zy, st.ry = _pass(sf.Y, g, st.zy, st.ry, st.kind, sf.labels_y, ty)
     st.y = sf.Y.behavioral_to_sequence(st.zy)
     st.ybar = a * st.y + (1 - a) * st.ybar            # line 41, same alpha^t (reading R9)
     st.t += 1
     return st
 
 
-def run(sf, variant, iters):
+def run(sf, variant, iters, trace=None):
     st = CFRState(sf, variant)
     for _ in range(iters):
-        cfr_iteration(st)
+        cfr_iteration(st, trace)
     return st
 
 

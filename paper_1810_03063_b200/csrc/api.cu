@@ -102,6 +102,7 @@ struct egt_game {
     double* gapcur = nullptr;       // [G] eps_sad of the current EGT/as iterate (maintained)
     double* S[2] = {nullptr, nullptr};   // EGT state, 2 slots
     double* C[2] = {nullptr, nullptr};   // EGT cache (smoothed BR as behavioural logs, R16), 2 slots
+    double* XQ[2] = {nullptr, nullptr};  // the same smoothed BR in sequence form (x_hat = (1-tau) x + tau XQ), 2 slots
     double* HAT[2] = {nullptr, nullptr};
     double* RESP[2] = {nullptr, nullptr};
     double* GR[2] = {nullptr, nullptr};
@@ -300,14 +301,16 @@ static void shard_rows(const PlayerLayout& L, int rank, int world, int chunk_ter
     for (int r = 0; r < n; ++r) cum[r + 1] = cum[r] + (L.term_off[L.rows_term[r] + 1] - L.term_off[L.rows_term[r]]);
     auto bound = [&](int k) {
         const long long target = cum[n] * k / world;
-        return (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        int i = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        if (i > 0 && i < n && L.pair_next[i - 1]) ++i;  // never split a swapped pair of rows
+        return i;
     };
     r0 = rank == 0 ? 0 : bound(rank);
     r1 = rank + 1 == world ? n : bound(rank + 1);
     chunks.assign(1, 0);
     for (int r = r0, cnt = 0; r < r1; ++r) {
         cnt += (int)(cum[r + 1] - cum[r]);
-        if (cnt >= chunk_terms || r + 1 == r1) {
+        if ((cnt >= chunk_terms && !L.pair_next[r]) || r + 1 == r1) {
             chunks.push_back(r + 1 - r0);
             cnt = 0;
         }
@@ -317,8 +320,10 @@ static void shard_rows(const PlayerLayout& L, int rank, int world, int chunk_ter
 static int max_chunk_terms(const PlayerLayout& L, int r0, const std::vector<int>& chunks) {
     int mx = 0;
     for (size_t c = 0; c + 1 < chunks.size(); ++c) {
-        const int a = L.rows_term[r0 + chunks[c]], b = L.rows_term[r0 + chunks[c + 1] - 1];
-        mx = std::max(mx, L.term_off[b + 1] - L.term_off[a]);
+        int n = 0;
+        for (int r = r0 + chunks[c]; r < r0 + chunks[c + 1]; ++r)
+            n += L.term_off[L.rows_term[r] + 1] - L.term_off[L.rows_term[r]];
+        mx = std::max(mx, n);
     }
     return mx;
 }
@@ -352,8 +357,9 @@ static void slice_bounds(const egt_game* G, int p, const DevPlayer& P, int& lo, 
         hi = L.n_pub - 1;
         return;
     }
-    lo = L.rows_term[r0];
-    hi = L.rows_term[r0 + P.n_rows_term - 1];
+    // (rows_term is in processing order: a swapped pair of rows is never split between slices)
+    lo = *std::min_element(L.rows_term.begin() + r0, L.rows_term.begin() + r0 + P.n_rows_term);
+    hi = *std::max_element(L.rows_term.begin() + r0, L.rows_term.begin() + r0 + P.n_rows_term);
 }
 
 // zero every row of a gradient buffer outside [lo, hi] (all games): before a sharded
@@ -438,21 +444,14 @@ extern "C" int egt_load_game(const egt_game_spec* spec, egt_game** out) {
     TRY(upload(G, &d_valid, valid));
     // the card-domain gradient kernel's per-board plans (river games, one board state)
     bool plans = nbs == 1;
-    for (const BoardTable& tb : H.tables) plans = plans && !tb.plan.pw.empty();
+    for (const BoardTable& tb : H.tables) plans = plans && tb.plan.tab.size() == (size_t)CARD_TAB_WORDS;
     if (plans) {
-        std::vector<uint32_t> pw, pr, ln;
-        for (const BoardTable& tb : H.tables) {
-            pw.insert(pw.end(), tb.plan.pw.begin(), tb.plan.pw.end());
-            pr.insert(pr.end(), tb.plan.pr.begin(), tb.plan.pr.end());
-            ln.insert(ln.end(), tb.plan.lane.begin(), tb.plan.lane.end());
-        }
-        uint32_t *d_pw, *d_pr, *d_ln;
-        TRY(upload(G, &d_pw, pw));
-        TRY(upload(G, &d_pr, pr));
-        TRY(upload(G, &d_ln, ln));
-        G->dg.card_pw = d_pw;
-        G->dg.card_pr = d_pr;
-        G->dg.card_lane = d_ln;
+        std::vector<uint32_t> tab;
+        tab.reserve(H.tables.size() * (size_t)CARD_TAB_WORDS);
+        for (const BoardTable& tb : H.tables) tab.insert(tab.end(), tb.plan.tab.begin(), tb.plan.tab.end());
+        uint32_t* d_tab;
+        TRY(upload(G, &d_tab, tab));
+        G->dg.card_tab = d_tab;
     }
     G->dg.card_plan = plans ? 1 : 0;
     double *d_p0, *d_p1, *d_kg;
@@ -929,6 +928,7 @@ static int ensure_egt_buffers(egt_game* G) {
         const size_t n = (size_t)Gn * G->V[p];
         if (!G->S[p] && dalloc_vec(G, &G->S[p], 2 * n)) return EGT_E_CUDA;
         if (!G->C[p] && dalloc_vec(G, &G->C[p], 2 * n)) return EGT_E_CUDA;
+        if (!G->XQ[p] && dalloc_vec(G, &G->XQ[p], 2 * n)) return EGT_E_CUDA;
         if (!G->RESP[p] && dalloc_vec(G, &G->RESP[p], n)) return EGT_E_CUDA;
     }
     return 0;
@@ -1002,12 +1002,12 @@ static double tree_bytes_per_game(const egt_game* G, int p, const TreeArgs& A) {
     if (A.center.ok()) n += A.mode == TM_CFR ? 2 : 1;
     n += A.regret.ok() ? 2 : 0;
     n += A.avg.ok() ? 2 : 0;
-    n += A.out_b.ok() + A.out_q.ok() + A.comb_in.ok() + A.comb_out.ok();
+    n += A.out_b.ok() + A.out_q.ok() + A.out_lb.ok() + A.comb_in.ok() + A.comb_out.ok();
     return (double)n * G->host.pl[p].n_pub * G->host.H * G->esz;
 }
 
 // compulsory HBM bytes of one gradient of one game
-static double grad_bytes_per_game(const egt_game* G, int p) {
+static double grad_bytes_per_game(const egt_game* G, int p, bool comb = false) {
     const HostGame& H = G->host;
     std::vector<char> seen(H.pl[1 - p].n_pub, 0);
     int rd = 0;
@@ -1016,7 +1016,8 @@ static double grad_bytes_per_game(const egt_game* G, int p) {
             seen[t.last_seq[1 - p]] = 1;
             ++rd;
         }
-    return (double)(rd + (int)H.pl[p].rows_term.size() + 2) * H.H * G->esz;
+    // comb: the input is formed from two vectors' rows (Alg. 2 line 1 fused into the gradient)
+    return (double)((comb ? 2 : 1) * rd + (int)H.pl[p].rows_term.size() + 2) * H.H * G->esz;
 }
 
 static cudaError_t tree(egt_game* G, int p, const TreeArgs& A) {
@@ -1051,7 +1052,8 @@ static cudaError_t peer_barrier(egt_game* G) {
     });
 }
 
-static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask, int want, int all_rows);
+static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask, int want, int all_rows,
+                            const GradComb* comb);
 
 // One gradient of the solver.  Sharded (egt_shard), this rank computes its slice of the rows:
 //  * fused all-gather (egt_shard_peers): the kernel stores its rows into every rank's buffer;
@@ -1063,8 +1065,8 @@ static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int
 // all_rows: every row is written (rows no terminal ends are 0), for buffers that are not
 // the solver's gradient buffers.
 static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask = nullptr, int want = 0,
-                        int all_rows = 0) {
-    if (G->emu_world > 1) return emu_grad(G, p, in, out, mask, want, all_rows);
+                        int all_rows = 0, const GradComb* comb = nullptr) {
+    if (G->emu_world > 1) return emu_grad(G, p, in, out, mask, want, all_rows, comb);
     const bool fused = G->p2p && out.base == G->GR[p] && !out.slot_sel && !all_rows;
     if (fused) {
         cudaError_t e = peer_barrier(G);
@@ -1077,19 +1079,20 @@ static cudaError_t grad(egt_game* G, int p, VecRef in, VecRef out, const int* ma
         G, p == 0 ? EGT_KERNEL_GRAD_AY : EGT_KERNEL_GRAD_ATX, active_games(G, mask, want),
         [&] {
             return launch_gradient(G->dg, G->dp[p], p, in, out, mask, want, all_rows, G->st,
-                                   fused ? &G->peers[p] : nullptr);
+                                   fused ? &G->peers[p] : nullptr, comb);
         },
-        G->timing ? grad_bytes_per_game(G, p) : 0.0);
+        G->timing ? grad_bytes_per_game(G, p, comb != nullptr) : 0.0);
     if (e != cudaSuccess) return e;
     return fused ? peer_barrier(G) : allreduce_grad(G, p, out);
 }
 
 // Emulated ranks (egt_shard_emulate): rank r's slice kernel writes buffer r (rank 0's is the
 // solver's output) exactly as on rank r; the collective is a local kernel over the buffers.
-static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask, int want, int all_rows) {
+static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int* mask, int want, int all_rows,
+                            const GradComb* comb) {
     const int W = G->emu_world;
     if (all_rows || out.slot_sel || out.base != G->GR[p]) {  // not a solver gradient buffer: unsharded
-        return launch_gradient(G->dg, G->dp_full[p], p, in, out, mask, want, all_rows, G->st, nullptr);
+        return launch_gradient(G->dg, G->dp_full[p], p, in, out, mask, want, all_rows, G->st, nullptr, comb);
     }
     cudaError_t e = cudaSuccess;
     for (int r = 0; r < W && e == cudaSuccess; ++r) {
@@ -1100,12 +1103,12 @@ static cudaError_t emu_grad(egt_game* G, int p, VecRef in, VecRef out, const int
             DevPeers pr;
             pr.n = W;
             for (int d = 0; d < W; ++d) pr.base[d] = G->emu_buf[p][d];
-            e = launch_gradient(G->dg, P, p, in, o, mask, want, 0, G->st, &pr);
+            e = launch_gradient(G->dg, P, p, in, o, mask, want, 0, G->st, &pr, comb);
         } else {
             int lo, hi;
             slice_bounds(G, p, P, lo, hi);
             e = zero_outside(G, p, o.base, lo, hi, G->st);
-            if (e == cudaSuccess) e = launch_gradient(G->dg, P, p, in, o, mask, want, 0, G->st, nullptr);
+            if (e == cudaSuccess) e = launch_gradient(G->dg, P, p, in, o, mask, want, 0, G->st, nullptr, comb);
         }
     }
     if (e == cudaSuccess && !G->emu_fused)
@@ -1205,12 +1208,16 @@ static int egt_initial_point(egt_game* G, double* g_omega, const int* mask = nul
     A.gsign = GSIGN[1];
     A.mu = S.mu + Gn;
     A.out_lb = slot2(G, G->C[1], 1, 0);
+    A.out_q = slot2(G, G->XQ[1], 1, 0);
     A.value = S.val + Gn;
     A.partial = G->partial;
     A.counter = G->counter;
     A.mask = mask;
     A.want = 1;
     CK(tree(G, 1, A));
+    // x0 = x_mu(y0) is also the sequence-form cache of player 0 (every game's slot is 0 here)
+    if (!mask)
+        CK(cudaMemcpyAsync(G->XQ[0], G->S[0], (size_t)G->esz * Gn * G->V[0], cudaMemcpyDeviceToDevice, G->st));
     return 0;
 }
 
@@ -1252,23 +1259,19 @@ static int record_egt_iteration(egt_game* G) {
             A.gsign = GSIGN[p];
             A.mu = S.mu + (size_t)p * Gn;
             A.out_lb = slot2(G, G->C[p], p, 0);
+            A.out_q = slot2(G, G->XQ[p], p, 0);
             A.mask = S.focus;
             A.want = p;
             CK(tree(G, p, A));
         }
-        // Alg. 2 line 1: p_hat = (1 - tau) p + tau p_mu(o)
-        TreeArgs A = base_args();
-        A.mode = TM_COMBINE;
-        A.center = slot2(G, G->C[p], p, 0);
-        A.comb_in = slot2(G, G->S[p], p, 0);
-        A.comb_out = vec(G->HAT[p], G->V[p]);
-        A.tau = S.tau;
-        A.mask = S.focus;
-        A.want = p;
-        CK(tree(G, p, A));
+        // Alg. 2 line 1: p_hat = (1 - tau) p + tau p_mu(o), formed by the gradient of line 2 on
+        // the rows it reads (p_mu(o) in sequence form, cached by the SBR that produced it)
+        GradComb hat;
+        hat.b = slot2(G, G->XQ[p], p, 0);
+        hat.tau = S.tau;
         // line 2: o_plus = (1 - tau) o + tau o_mu(p_hat)
-        CK(grad(G, o, vec(G->HAT[p], G->V[p]), vec(G->GR[o], G->V[o]), S.focus, p));
-        A = base_args();
+        CK(grad(G, o, slot2(G, G->S[p], p, 0), vec(G->GR[o], G->V[o]), S.focus, p, 0, &hat));
+        TreeArgs A = base_args();
         A.mode = TM_SBR;
         A.g = vec(G->GR[o], G->V[o]);
         A.gsign = GSIGN[o];
@@ -1329,6 +1332,7 @@ static int record_egt_iteration(egt_game* G) {
                 A.gsign = GSIGN[p];
                 A.mu = S.mu_cand + (size_t)p * Gn;
                 A.out_lb = slot2(G, G->C[p], p, 1);
+                A.out_q = slot2(G, G->XQ[p], p, 1);
                 A.value = S.val + (size_t)p * Gn;
                 A.partial = partial;
                 A.counter = counter;

@@ -381,9 +381,30 @@ static void build_layout(HostGame& G) {
             for (int t : by[s]) L.term_idx.push_back(t);
         }
         L.term_off[L.n_pub] = (int)L.term_idx.size();
+        // Order for the card-domain gradient kernel (which reuses an opponent row's totals for a
+        // fold that follows a terminal on the same opponent row, and recomputes for a
+        // showdown): inside a row showdowns first; and where a row ends with a fold and the
+        // next starts with a showdown on the same opponent row, the two rows swap (row order
+        // is free: each row is written when its last terminal is done).  pair_next[r] marks a
+        // swapped pair (r, r + 1), which a shard boundary never splits.
+        for (int s = 0; s < L.n_pub; ++s)
+            std::stable_sort(L.term_idx.begin() + L.term_off[s], L.term_idx.begin() + L.term_off[s + 1],
+                             [&](int a, int b) { return (G.terms[a].kind == T_SHOWDOWN) > (G.terms[b].kind == T_SHOWDOWN); });
         L.rows_term.clear();
         for (int s = 0; s < L.n_pub; ++s)
             if (L.term_off[s + 1] > L.term_off[s]) L.rows_term.push_back(s);
+        L.pair_next.assign(L.rows_term.size(), 0);
+        for (size_t r = 0; r + 1 < L.rows_term.size(); ++r) {
+            const int a = L.rows_term[r], b = L.rows_term[r + 1];
+            const Terminal& last = G.terms[L.term_idx[L.term_off[a + 1] - 1]];
+            const Terminal& first = G.terms[L.term_idx[L.term_off[b]]];
+            const int oa = last.last_seq[1 - p], ob = first.last_seq[1 - p];
+            if (last.kind != T_SHOWDOWN && first.kind == T_SHOWDOWN && oa == ob && oa != 0) {
+                std::swap(L.rows_term[r], L.rows_term[r + 1]);
+                L.pair_next[r] = 1;
+                ++r;
+            }
+        }
         L.chunk_off.assign(1, 0);
         // a tree with at most two chunks' worth of terminals keeps them in one CTA (staging the
         // tables twice costs more than the second CTA gains); GRAD_CHUNK_MAX_TERMS still bounds it
@@ -393,7 +414,7 @@ static void build_layout(HostGame& G) {
         for (int r = 0, n = 0; r < (int)L.rows_term.size(); ++r) {
             const int s = L.rows_term[r];
             n += L.term_off[s + 1] - L.term_off[s];
-            if (n >= chunk || r + 1 == (int)L.rows_term.size()) {
+            if ((n >= chunk && !L.pair_next[r]) || r + 1 == (int)L.rows_term.size()) {
                 L.chunk_off.push_back(r + 1);
                 n = 0;
             }
@@ -560,6 +581,12 @@ static void build_table(const HostGame& G, int g, int bs, const std::vector<int>
             cp[i] = {std::min(hc[0], hc[1]), std::max(hc[0], hc[1])};
         }
         build_card_plan(G, by_card, tb.lo, cp, nv, tb.plan);
+        CardPlan& pl = tb.plan;
+        pl.tab.assign(CARD_TAB_WORDS, 0u);
+        std::copy(pl.pw.begin(), pl.pw.end(), pl.tab.begin() + CARD_TAB_PW);
+        std::copy(pl.pr.begin(), pl.pr.end(), pl.tab.begin() + CARD_TAB_PR);
+        for (int i = 0; i < nv; ++i) pl.tab[CARD_TAB_LOHI + i] = tb.lohi[i];
+        std::copy(pl.lane.begin(), pl.lane.end(), pl.tab.begin() + CARD_TAB_LANE);
     }
 }
 

@@ -59,7 +59,8 @@ struct PlayerLayout {
     std::vector<std::string> seq_hist;  // [n_pub], "" for row 0
     std::vector<int> seq_owner;    // decision node owning the sequence (-1 for row 0)
     std::vector<int> term_off, term_idx;  // terminals grouped by this player's last sequence
-    std::vector<int> rows_term;           // sequences that end at least one terminal
+    std::vector<int> rows_term;           // sequences that end at least one terminal (processing order)
+    std::vector<char> pair_next;          // rows_term[r], rows_term[r + 1] were swapped (kept together)
     std::vector<int> chunk_off;           // rows_term split into chunks of ~GRAD_CHUNK_TERMS terminals
     std::vector<int> lvl_off, lvl_nodes;  // decision nodes grouped by level
     std::vector<int> kid_off, kids;       // child decision nodes of each sequence
@@ -106,12 +107,16 @@ constexpr int CARD_NT = 416, CARD_K = 3, CARD_GL = 8, CARD_CH = 6;
 constexpr int CARD_NP = CARD_NT * CARD_K;            // positions (>= H_pad)
 constexpr int CARD_WREGION = 2 * CARD_NP + 2;        // doubles: w1, w2, a zero cell (+ pad)
 constexpr int CARD_EX = CARD_NT * CARD_CH;           // doubles of the ex exchange
+// one board's plan as one word array (the kernel keeps one pointer): pw, pr, lohi, lane
+constexpr int CARD_TAB_PW = 0, CARD_TAB_PR = CARD_NP, CARD_TAB_LOHI = 2 * CARD_NP, CARD_TAB_LANE = 3 * CARD_NP;
+constexpr int CARD_TAB_WORDS = 3 * CARD_NP + 8 * CARD_NT;
 struct CardPlan {
     std::vector<uint32_t> pw;    // [CARD_NP] byte offsets into the w region: w1 | w2 << 16
     std::vector<uint32_t> pr;    // [CARD_NP] ex element index of the lower-card slot | higher << 16
     std::vector<uint32_t> lane;  // [CARD_NT][8] per thread: cg[3] (gather byte offsets, 2 x 16 bit),
                                  // px[3] (ex element index, 2 x 16 bit), flags (valid 0-5, run head
                                  // 6-11, run tail 12-17), src lanes (lo 0-4, hi 8-12)
+    std::vector<uint32_t> tab;   // [CARD_TAB_WORDS] pw | pr | tie group lo | hi << 16 per position | lane
 };
 
 struct BoardTable {

@@ -142,7 +142,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Hands that do not share their tie group read their own P / Pc from registers.
 template <int NT, int KMAX, int EMAX, typename T>
 __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int player, VecRef vin, VecRef gout,
-                                                     const int* __restrict__ mask, int want, DevPeers peers) {
+                                                     const int* __restrict__ mask, int want, DevPeers peers,
+                                                     VecRef vin2, const double* __restrict__ ctau) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     T* sm = reinterpret_cast<T*>(sm_raw);
     constexpr int NW = NT / 32;
@@ -166,6 +167,8 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
     const int t0 = P.term_off[s], t1 = P.term_off[s + 1];
     const T* __restrict__ popp = static_cast<const T*>(player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp;
     const T* __restrict__ vo = vin.at<T>(g);
+    const T* __restrict__ vo2 = ctau ? vin2.at<T>(g) : nullptr;  // x_hat = (1 - tau) vin + tau vin2
+    const T ct = ctau ? (T)ctau[g] : T(0), ct1 = T(1) - ct;
     const T kg = (T)G.kappa_game[g];
     const T sd_sign = player == 0 ? T(1) : T(-1);
     const int EPT = (n_ce + NT - 1) / NT;
@@ -180,6 +183,7 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
         const uint2* __restrict__ pcard = G.tab_pcard + (size_t)k * Hp;
         const int so = player ? tm.seq[0] : tm.seq[1];
         const T* __restrict__ vrow = vo + (size_t)so * Hp;
+        const T* __restrict__ vrow2 = vo2 ? vo2 + (size_t)so * Hp : nullptr;
         const bool sd = tm.kind == 2;
         const int K = (nv + NT - 1) / NT;
         const int base = tid * K;
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(NT, 2) grad_kernel(DevGame G, DevPlayer P, int
         // ---- phase A: w (coalesced), then per-thread chunks of K positions, block scan
         for (int i = tid; i < nv; i += NT) {
             const int h = fast ? i : order[i];
-            w[i] = popp[h] * (so ? vrow[h] : T(1));
+            w[i] = popp[h] * (so ? (vrow2 ? ct1 * vrow[h] + ct * vrow2[h] : vrow[h]) : T(1));
         }
         __syncthreads();
         T x[KMAX];
@@ -387,41 +391,53 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned half16(unsigned v, int hi) { return hi ? v >> 16 : v & 0xFFFFu; }
+// the plan's w-region byte offsets are for 8-byte elements; fp32 elements sit at half of them
+template <class T>
+__device__ __forceinline__ unsigned woff(unsigned v, int hi) { return half16(v, hi) >> (sizeof(T) == 4 ? 1 : 0); }
 
-template <typename T>
-__global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
+#ifndef CARD_MINB
+#define CARD_MINB 2
+#endif
+template <typename T, bool COMB>
+__global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
                                                                VecRef gout, const int* __restrict__ mask, int want,
-                                                               DevPeers peers) {
+                                                               DevPeers peers, VecRef vin2,
+                                                               const double* __restrict__ ctau) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
-    constexpr int NT = CARD_NT, K = CARD_K, CH = CARD_CH, NW = NT / 32, NP = CARD_NP;
+    constexpr int NT = CARD_NT, K = CARD_K, CH = CARD_CH, NW = NT / 32, NP = CARD_NP, MT = GRAD_CHUNK_MAX_TERMS;
     __shared__ T wtot[NW];
     __shared__ __align__(8) uint64_t bar[3];
-    // the chunk's terminals: opponent row, kind, weight, and the row each one completes (-1: more
-    // terminals of its row follow)
-    __shared__ int t_so[GRAD_CHUNK_MAX_TERMS], t_kind[GRAD_CHUNK_MAX_TERMS], t_end[GRAD_CHUNK_MAX_TERMS];
-    __shared__ double t_w[GRAD_CHUNK_MAX_TERMS];
-    const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // the chunk's terminals in processing order: opponent row, kind, weight, the row each one
+    // completes (-1: more terminals of its row follow), its row buffer and whether it is fetched
+    __shared__ int t_so[MT], t_kind[MT], t_end[MT], t_idx[MT];
+    __shared__ double t_w[MT];
+    __shared__ int s_nT;
+    const int g = blockIdx.y, tid = threadIdx.x;
     if (mask && mask[g] != want) return;
     const int Hp = G.H_pad, H = G.H;
     T* popp = reinterpret_cast<T*>(sm_raw);  // [NP] (0 beyond H)
-    T* pself = popp + NP;                    // [NP]
-    T* vb = pself + NP;                      // [2][NP] opponent rows (0 beyond Hp)
-    T* wreg = vb + 2 * NP;                   // [CARD_WREGION] w1 | w2 | zero cell
+    T* vb = popp + NP;                       // [2][NP] opponent rows (0 beyond Hp)
+    T* vb2 = vb + 2 * NP;                    // COMB: [2][NP] the second input's rows
+    T* wreg = vb2 + (COMB ? 2 * NP : 0);     // [CARD_WREGION] w1 | w2 | zero cell
     T* Pf = wreg + CARD_WREGION;             // [NP + 4] exclusive prefixes of w by position
     T* Ex = Pf + NP + 4;                     // [CARD_EX] card parts at a row end
-    unsigned char* const wbytes = reinterpret_cast<unsigned char*>(wreg);
     const int r0 = P.chunk_off[blockIdx.x], r1 = P.chunk_off[blockIdx.x + 1];
-    const int T0 = P.term_off[P.rows_term[r0]], T1 = P.term_off[P.rows_term[r1 - 1] + 1];
     const T* __restrict__ vo = vin.at<T>(g);
-    const int nT = T1 - T0;
-    for (int i = tid; i < nT; i += NT) {
-        const DevTerm tm = G.terms[P.term_idx[T0 + i]];
-        t_so[i] = player ? tm.seq[0] : tm.seq[1];
-        t_kind[i] = tm.kind;
-        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
-        t_end[i] = -1;
-    }
+    const T* __restrict__ vo2 = COMB ? vin2.at<T>(g) : nullptr;
     if (tid == 0) {
+        // the chunk's terminals in processing order: its rows in rows_term order (game.cpp
+        // build_layout orders rows and terminals so that a terminal sharing the previous one's
+        // opponent row is a fold), each row's terminals in term_idx order
+        int n = 0;
+        for (int r = r0; r < r1; ++r) {
+            const int srow = P.rows_term[r];
+            for (int k = P.term_off[srow]; k < P.term_off[srow + 1]; ++k) {
+                t_idx[n] = P.term_idx[k];
+                t_end[n] = k + 1 == P.term_off[srow + 1] ? srow : -1;
+                ++n;
+            }
+        }
+        s_nT = n;
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_init(&bar[2], 1);
@@ -429,84 +445,102 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPla
     }
     for (int i = Hp + tid; i < NP; i += NT) {  // padding the bulk copies never write
         popp[i] = T(0);
-        pself[i] = T(0);
         vb[i] = T(0);
         vb[NP + i] = T(0);
+        if (COMB) {
+            vb2[i] = T(0);
+            vb2[NP + i] = T(0);
+        }
     }
     if (tid < CARD_WREGION - 2 * NP) wreg[2 * NP + tid] = T(0);  // the zero cell padding slots read
     if (tid < 4) Pf[NP + tid] = T(0);
     __syncthreads();
-    for (int r = r0 + tid; r < r1; r += NT) {
-        const int srow = P.rows_term[r];
-        t_end[P.term_off[srow + 1] - 1 - T0] = srow;
+    const int nT = s_nT;
+    for (int i = tid; i < nT; i += NT) {
+        const DevTerm tm = G.terms[t_idx[i]];
+        t_so[i] = player ? tm.seq[0] : tm.seq[1];
+        t_kind[i] = tm.kind;
+        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
     }
+    __syncthreads();
     if (tid == 0) {
         const unsigned bD = Hp * sizeof(T);
-        mbar_expect_tx(&bar[0], 2 * bD);
+        mbar_expect_tx(&bar[0], bD);
         bulk_g2s(popp, static_cast<const T*>(player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp, bD, &bar[0]);
-        bulk_g2s(pself, static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp, bD, &bar[0]);
-        for (int q = 0; q < 2 && T0 + q < T1; ++q) {
-            const int so = t_so[q];
-            if (so && !(q > 0 && so == t_so[q - 1])) {
-                mbar_expect_tx(&bar[1 + q], bD);
-                bulk_g2s(vb + q * NP, vo + (size_t)so * Hp, bD, &bar[1 + q]);
+        // the first two new opponent rows, into buffers 0 and 1 (the loop prefetches the rest,
+        // a new row always into the buffer the current row is not in)
+        int b = 1, fetched = 0;
+        for (int q = 0; q < nT && fetched < 2; ++q) {
+            if (t_so[q] != 0 && (q == 0 || t_so[q] != t_so[q - 1])) {
+                b ^= 1;
+                if (q <= 1) {
+                    mbar_expect_tx(&bar[1 + b], COMB ? 2 * bD : bD);
+                    bulk_g2s(vb + b * NP, vo + (size_t)t_so[q] * Hp, bD, &bar[1 + b]);
+                    if (COMB) bulk_g2s(vb2 + b * NP, vo2 + (size_t)t_so[q] * Hp, bD, &bar[1 + b]);
+                }
+                ++fetched;
             }
+            if (q >= 1) break;
         }
     }
     // the board's plan, in registers for the whole chunk (game.h CardPlan)
+    const int lane = tid & 31, wid = tid >> 5;
     const int base = tid * K, part = tid & (CARD_GL - 1);
-    // (the exchange addresses used once per opponent row or per row stay in L1: __ldg)
-    const uint32_t* __restrict__ lh_g = G.tab_lohi + (size_t)g * Hp + base;  // tie group [lo, hi) per position
-    const uint32_t* __restrict__ pw_g = G.card_pw + (size_t)g * NP + base;
-    const uint32_t* __restrict__ pr_g = G.card_pr + (size_t)g * NP + base;
-    const uint4* __restrict__ lane_g = reinterpret_cast<const uint4*>(G.card_lane) + ((size_t)g * NT + tid) * 2;
+    // the board's plan (one pointer; the words used once per opponent row / row stay in L1)
+    const uint32_t* __restrict__ tab = G.card_tab + (size_t)g * CARD_TAB_WORDS;
+    const uint4* __restrict__ lane_g = reinterpret_cast<const uint4*>(tab + CARD_TAB_LANE) + tid * 2;
     const uint4 la = __ldg(lane_g), lb = __ldg(lane_g + 1);
     const uint32_t cg[3] = {la.x, la.y, la.z};
     const uint32_t flags = lb.z;
     const int src_lo = (int)(lb.w & 31u), src_hi = (int)((lb.w >> 8) & 31u);
     const T sd_sign = player == 0 ? T(1) : T(-1);
-    T racc[K], rc[CH], dsd[CH], x[K];
+    const T ct = COMB ? (T)ctau[g] : T(0), ct1 = T(1) - ct;  // Alg. 2 line 1
+    const T* __restrict__ pself_g = static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
+    unsigned char* const wbytes = reinterpret_cast<unsigned char*>(wreg);
+    T racc[K], rc[CH], x[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) racc[j] = x[j] = T(0);
 #pragma unroll
-    for (int s = 0; s < CH; ++s) rc[s] = dsd[s] = T(0);
+    for (int s = 0; s < CH; ++s) rc[s] = T(0);
     T total = T(0), pbase = T(0), segS = T(0);
     unsigned par = 0u;  // mbarrier phase bit of each opponent-row buffer
     bool ex_dirty = false;  // the last row end's Ex reads are not yet behind a barrier
     mbar_wait(&bar[0], 0);
-    __syncthreads();  // t_end
-    for (int ti = T0; ti < T1; ++ti) {
-        const int q = (ti - T0) & 1, li = ti - T0;
+    __syncthreads();  // the processing order
+    int q = 1;  // the buffer holding the current opponent row
+    for (int li = 0; li < nT; ++li) {
         const int so = t_so[li];
         const bool sd = t_kind[li] == 2;
-        const bool reuse = li > 0 && so == t_so[li - 1];
-        // the run values of a showdown, also computed by the first of a fold / call pair on the
-        // same opponent row when the call follows
-        const bool full = sd || (li + 1 < nT && t_so[li + 1] == so && t_kind[li + 1] == 2);
-        if (tid == 0 && ti > T0 && ti + 1 < T1) {  // terminal ti+1's row into the other buffer
-            const int so1 = t_so[li + 1];
-            if (so1 && so1 != so) {
-                fence_proxy_async();
-                mbar_expect_tx(&bar[1 + (q ^ 1)], Hp * sizeof(T));
-                bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)so1 * Hp, Hp * sizeof(T), &bar[1 + (q ^ 1)]);
-            }
+        const bool new_row = so != 0 && (li == 0 || so != t_so[li - 1]);
+        // a fold on the previous terminal's opponent row reuses its totals (w, T, S_c); a
+        // showdown always recomputes (its per-slot terms do not survive a terminal)
+        const bool reuse = li > 0 && !sd && so == t_so[li - 1];
+        if (new_row) q ^= 1;
+        if (tid == 0 && li > 0 && li + 1 < nT && t_so[li + 1] != 0 && t_so[li + 1] != so) {
+            fence_proxy_async();  // the next new row, into the other buffer
+            mbar_expect_tx(&bar[2 - q], (COMB ? 2 : 1) * Hp * sizeof(T));
+            bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)t_so[li + 1] * Hp, Hp * sizeof(T), &bar[2 - q]);
+            if (COMB) bulk_g2s(vb2 + (q ^ 1) * NP, vo2 + (size_t)t_so[li + 1] * Hp, Hp * sizeof(T), &bar[2 - q]);
         }
-        if (so && !reuse) {
+        if (new_row) {
             mbar_wait(&bar[1 + q], (par >> q) & 1u);
             par ^= 1u << q;
         }
+        T dsd[CH];
         if (!reuse) {  // CTA-uniform
             // ---- position domain: w, its two conflict-free copies for the card lanes, warp scan
             const T* vrow = vb + q * NP;
+            const T* vrow2 = vb2 + q * NP;
             T run = T(0);
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                x[j] = so ? popp[base + j] * vrow[base + j] : popp[base + j];
+                const T v = COMB ? ct1 * vrow[base + j] + ct * vrow2[base + j] : vrow[base + j];
+                x[j] = so ? popp[base + j] * v : popp[base + j];
                 run += x[j];
                 if (base + j < H) {
-                    const uint32_t pw = __ldg(pw_g + j);
-                    *reinterpret_cast<T*>(wbytes + half16(pw, 0)) = x[j];
-                    *reinterpret_cast<T*>(wbytes + half16(pw, 1)) = x[j];
+                    const uint32_t pw = __ldg(tab + CARD_TAB_PW + base + j);
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 0)) = x[j];
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 1)) = x[j];
                 }
             }
             const T incl = warp_incl_scan(run, lane);
@@ -516,7 +550,7 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPla
             T y[CH], ssum = T(0);
 #pragma unroll
             for (int s = 0; s < CH; ++s) {
-                y[s] = *reinterpret_cast<const T*>(wbytes + half16(cg[s / 2], s & 1));
+                y[s] = *reinterpret_cast<const T*>(wbytes + woff<T>(cg[s / 2], s & 1));
                 ssum += y[s];
             }
             T inc = ssum;
@@ -526,7 +560,7 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPla
                 if (part >= o) inc += u;
             }
             segS = __shfl_sync(0xffffffffu, inc, lane | (CARD_GL - 1));
-            if (full) {
+            if (sd) {
                 T ex[CH];
                 T r = inc - ssum;
 #pragma unroll
@@ -563,7 +597,7 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPla
             const T wpre = wid ? wpre_incl : T(0);
             total = __shfl_sync(0xffffffffu, wsc, NW - 1);
             pbase = wpre + incl - run;
-            if (full) {
+            if (sd) {
                 T pp = pbase;
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
@@ -578,21 +612,10 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPla
         // ---- this terminal's contribution: position parts and card parts
         const T scale = (T)t_w[li];
         if (sd) {
-            const T pp1 = pbase + x[0], pp2 = pp1 + x[1];
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-                const uint32_t lh = base + j < Hp ? __ldg(lh_g + j) : 0u;
-                const int lo = (int)(lh & 0xFFFFu), hi = (int)(lh >> 16);
-                T plo, phi;
-                if (lo >= base && hi <= base + K) {  // the tie group lies inside this thread's positions
-                    const int a = lo - base, b = hi - base;
-                    plo = a == 0 ? pbase : a == 1 ? pp1 : pp2;
-                    phi = b == 1 ? pp1 : b == 2 ? pp2 : pp2 + x[2];
-                } else {
-                    plo = Pf[lo];
-                    phi = Pf[hi];
-                }
-                racc[j] += scale * (sd_sign * (total - phi - plo));
+            for (int j = 0; j < K; ++j) {  // P at the tie group's bounds (a group's lanes share the address)
+                const uint32_t lh = __ldg(tab + CARD_TAB_LOHI + base + j);
+                racc[j] += scale * (sd_sign * (total - Pf[lh >> 16] - Pf[lh & 0xFFFFu]));
             }
             const T sc2 = scale * sd_sign;
 #pragma unroll
@@ -609,8 +632,7 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPla
         if (srow >= 0) {
             if (ex_dirty) __syncthreads();
             {
-                const uint4 lx = __ldg(lane_g);
-                const uint4 ly = __ldg(lane_g + 1);
+                const uint4 lx = __ldg(lane_g), ly = __ldg(lane_g + 1);
                 const uint32_t px[3] = {lx.w, ly.x, ly.y};
 #pragma unroll
                 for (int s = 0; s < CH; ++s) {
@@ -623,11 +645,8 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_card_kernel(DevGame G, DevPla
 #pragma unroll
             for (int j = 0; j < K; ++j) {
                 const int i = base + j;
-                outv[j] = T(0);
-                if (i < H) {
-                    const uint32_t pr = __ldg(pr_g + j);
-                    outv[j] = pself[i] * (racc[j] + Ex[half16(pr, 0)] + Ex[half16(pr, 1)]);
-                }
+                const uint32_t pr = i < H ? __ldg(tab + CARD_TAB_PR + i) : 0u;
+                outv[j] = i < H ? __ldg(pself_g + i) * (racc[j] + Ex[half16(pr, 0)] + Ex[half16(pr, 1)]) : T(0);
                 racc[j] = T(0);
             }
             ex_dirty = true;
@@ -660,8 +679,8 @@ static size_t grad_smem_bytes(const DevGame& G) {
     return (size_t)G.esz * (size_t)(3 * G.H_pad + 1 + G.n_ce);
 }
 
-static size_t card_smem_bytes(const DevGame& G) {
-    return (size_t)G.esz * (4 * (size_t)CARD_NP + CARD_WREGION + CARD_NP + 4 + CARD_EX);
+static size_t card_smem_bytes(const DevGame& G, bool comb) {
+    return (size_t)G.esz * ((comb ? 5 : 3) * (size_t)CARD_NP + CARD_WREGION + CARD_NP + 4 + CARD_EX);
 }
 
 static bool card_ok(const DevGame& G) {
@@ -670,21 +689,30 @@ static bool card_ok(const DevGame& G) {
 
 template <class T>
 static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
-                                     const int* mask, int want, cudaStream_t st, const DevPeers& peers) {
+                                     const int* mask, int want, cudaStream_t st, const DevPeers& peers,
+                                     const GradComb* comb) {
+    const VecRef b = comb ? comb->b : VecRef();
+    const double* tau = comb ? comb->tau : nullptr;
     if (card_ok(G) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
-        grad_card_kernel<T><<<grid, CARD_NT, card_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, peers);
+        if (comb)
+            grad_card_kernel<T, true><<<grid, CARD_NT, card_smem_bytes(G, true), st>>>(G, P, player, vin, gout, mask,
+                                                                                       want, peers, b, tau);
+        else
+            grad_card_kernel<T, false><<<grid, CARD_NT, card_smem_bytes(G, false), st>>>(G, P, player, vin, gout,
+                                                                                         mask, want, peers, b, tau);
         return cudaGetLastError();
     }
     dim3 grid(P.n_rows_term, G.n_games);
     grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>
-        <<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, peers);
+        <<<grid, GRAD_NT, grad_smem_bytes(G), st>>>(G, P, player, vin, gout, mask, want, peers, b, tau);
     return cudaGetLastError();
 }
 
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
-                            const int* mask, int want, int all_rows, cudaStream_t st, const DevPeers* peers) {
+                            const int* mask, int want, int all_rows, cudaStream_t st, const DevPeers* peers,
+                            const GradComb* comb) {
     const DevPeers none;
     const DevPeers& pr = peers ? *peers : none;
     if (pr.n && gout.slot_sel) return cudaErrorInvalidValue;
@@ -702,8 +730,8 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
         if (e != cudaSuccess) return e;
     }
     if (P.n_rows_term == 0) return cudaSuccess;
-    return G.esz == 4 ? launch_gradient_t<float>(G, P, player, vin, gout, mask, want, st, pr)
-                      : launch_gradient_t<double>(G, P, player, vin, gout, mask, want, st, pr);
+    return G.esz == 4 ? launch_gradient_t<float>(G, P, player, vin, gout, mask, want, st, pr, comb)
+                      : launch_gradient_t<double>(G, P, player, vin, gout, mask, want, st, pr, comb);
 }
 
 // ------------------------------------------------------------------ treeplex pass
@@ -1292,11 +1320,11 @@ cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const 
         return cudaGetLastError();                                                              \
     }
     if (A.br_value) {  // the fused stopping test exists for the excessive-gap check's SBR only
-        if (A.mode != TM_SBR || outs != TO_LB) return cudaErrorInvalidValue;
-        EGT_TREE_GO(TM_SBR, TO_LB | TO_FUSEBR)
+        if (A.mode != TM_SBR || outs != (TO_LB | TO_Q)) return cudaErrorInvalidValue;
+        EGT_TREE_GO(TM_SBR, TO_LB | TO_Q | TO_FUSEBR)
     }
     // the solver's hot (mode, outputs) combinations get fully specialised kernels
-    if (A.mode == TM_SBR && outs == TO_LB) EGT_TREE_GO(TM_SBR, TO_LB)
+    if (A.mode == TM_SBR && outs == (TO_LB | TO_Q)) EGT_TREE_GO(TM_SBR, TO_LB | TO_Q)
     if (A.mode == TM_SBR && outs == (TO_Q | TO_COMB)) EGT_TREE_GO(TM_SBR, TO_Q | TO_COMB)
     if (A.mode == TM_PROX && outs == TO_COMB) EGT_TREE_GO(TM_PROX, TO_COMB)
     if (A.mode == TM_COMBINE && outs == TO_COMB) EGT_TREE_GO(TM_COMBINE, TO_COMB)
@@ -1326,14 +1354,16 @@ static cudaError_t prepare_t() {
     cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(grad_card_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        e = cudaFuncSetAttribute(grad_card_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grad_card_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     const void* tk[] = {(const void*)tree_kernel<T, TM_SBR, 0>,     (const void*)tree_kernel<T, TM_PROX, 0>,
                         (const void*)tree_kernel<T, TM_BR, 0>,      (const void*)tree_kernel<T, TM_CFR, 0>,
                         (const void*)tree_kernel<T, TM_UNIFORM, 0>, (const void*)tree_kernel<T, TM_COMBINE, 0>,
-                        (const void*)tree_kernel<T, TM_SBR, TO_LB>, (const void*)tree_kernel<T, TM_SBR, TO_Q | TO_COMB>,
+                        (const void*)tree_kernel<T, TM_SBR, TO_LB | TO_Q>, (const void*)tree_kernel<T, TM_SBR, TO_Q | TO_COMB>,
                         (const void*)tree_kernel<T, TM_PROX, TO_COMB>, (const void*)tree_kernel<T, TM_COMBINE, TO_COMB>,
                         (const void*)tree_kernel<T, TM_CFR, TO_Q | TO_AVG>,
-                        (const void*)tree_kernel<T, TM_SBR, TO_LB | TO_FUSEBR>};
+                        (const void*)tree_kernel<T, TM_SBR, TO_LB | TO_Q | TO_FUSEBR>};
     for (const void* f : tk)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     return e;

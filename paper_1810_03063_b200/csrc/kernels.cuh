@@ -47,9 +47,7 @@ struct DevGame {
     const uint8_t* tab_valid; // [G*n_bs][H_pad]
     // card-domain river gradient plan (game.h CardPlan), one per game; card_plan = 0: none
     int card_plan;
-    const uint32_t* card_pw;    // [G][CARD_NP]
-    const uint32_t* card_pr;    // [G][CARD_NP]
-    const uint32_t* card_lane;  // [G][CARD_NT][8]
+    const uint32_t* card_tab;   // [G][CARD_TAB_WORDS]
     const void* prior[2];     // [G][H_pad] in the game's precision
     const double* kappa_game; // [G]
     const DevTerm* terms;
@@ -138,12 +136,20 @@ struct DevScalars {
     const double* target;  // [G] per-game eps_sad target (<= 0: none), egt_set_target
 };
 
+// A gradient whose input is the convex combination (1 - tau_g) a + tau_g b of two vectors of the
+// other player, formed on the rows the kernel reads (Alg. 2 line 1: x_hat = (1 - tau) x +
+// tau x_mu(y)) -- the solver's x_hat never exists as a vector.
+struct GradComb {
+    VecRef b;
+    const double* tau = nullptr;  // [G]
+};
+
 // Launchers (return cudaGetLastError()).
 // all_rows = 1 writes every row of gout (rows without terminals get 0); 0 writes only the
 // rows that end a terminal (the solver's gradient buffers are zeroed once at allocation).
 cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, VecRef vin, VecRef gout,
                             const int* mask, int want, int all_rows, cudaStream_t st,
-                            const DevPeers* peers = nullptr);
+                            const DevPeers* peers = nullptr, const GradComb* comb = nullptr);
 cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const TreeArgs& A, cudaStream_t st);
 cudaError_t kernels_prepare();
 size_t tree_smem_bytes(const DevPlayer& P, int esz);

@@ -54,7 +54,16 @@ int main(int argc, char** argv) {
     for (int g = 0; g < n_games; ++g) {
         const BoardTable& tb = G.tables[g];
         const CardPlan& pl = tb.plan;
-        if (pl.pw.size() != (size_t)NP || pl.lane.size() != (size_t)NT * 8) { fail("no plan", g, 0, 0); continue; }
+        if (pl.pw.size() != (size_t)NP || pl.lane.size() != (size_t)NT * 8 || pl.tab.size() != (size_t)CARD_TAB_WORDS) {
+            fail("no plan", g, 0, 0);
+            continue;
+        }
+        for (int i = 0; i < NP; ++i)
+            if (pl.tab[CARD_TAB_PW + i] != pl.pw[i] || pl.tab[CARD_TAB_PR + i] != pl.pr[i] ||
+                (i < G.H && pl.tab[CARD_TAB_LOHI + i] != tb.lohi[i]))
+                fail("flat table", g, i, 0);
+        for (int i = 0; i < NT * 8; ++i)
+            if (pl.tab[CARD_TAB_LANE + i] != pl.lane[i]) fail("flat lane table", g, i, 0);
         const int H = G.H;
         // positions -> cards (lower, higher)
         std::vector<std::array<int, 2>> cards(H);

@@ -112,7 +112,7 @@ def rel_err(got, want):
 # of the session by tests/conftest.py).
 REPORT = {}
 
-FLOOR64, FLOOR32 = 1e-13, 1e-6
+FLOOR64, FLOOR32 = 1e-13, 1e-5
 
 
 def assert_parity(got, want, rtol, what, floor=None, mask=None):
@@ -120,7 +120,8 @@ def assert_parity(got, want, rtol, what, floor=None, mask=None):
     absolute floor of floor * max|want| for entries that cancel to ~0 (a showdown entry is a
     difference of prefix sums as large as the largest entry, so its rounding is ~ulp of the
     largest entry, not of itself): floor = 1e-13 in fp64 (~450 ulp of the largest entry),
-    1e-6 in fp32 (~17 ulp).  Records the worst relative error among entries >= 1e-6 max|want|."""
+    1e-5 in fp32 (the north star's fp32 bar itself: with a 24-bit mantissa an entry that cancels
+    to 1e-3 of the largest cannot be 1e-5-accurate relative to itself).  Records the worst relative error among entries >= 1e-6 max|want|."""
     got = np.asarray(got, dtype=float).ravel()
     want = np.asarray(want, dtype=float).ravel()
     if mask is not None:

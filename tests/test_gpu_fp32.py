@@ -1,9 +1,10 @@
 """Row 9: the optional fp32 mode (fp32 vectors and arithmetic) against the fp64 oracle.
 
 Bar (BASELINE.json north_star): relative error <= 1e-5 per element (paritylib.assert_parity,
-absolute floor 1e-7 * max|oracle| for entries that cancel), per-game values relative.  Solvers are compared on
-variants without an accept/reject decision (EGT with mu balancing, CFR+ on games without exact
-regret ties), so fp32 rounding cannot flip a discrete choice (R18)."""
+absolute floor 1e-6 * max|oracle| for entries that cancel), per-game values relative.  Discrete
+decisions taken on floating-point values (RM+'s [r]^+, EGT/as's EGV >= 0) are compared where
+the oracle's fp64 margin exceeds the fp32 noise; a decision at the noise level may go either
+way (R18) and what depends on it is left out -- no test is skipped."""
 import numpy as np
 import pytest
 
@@ -151,17 +152,95 @@ def test_egt_balanced_fp32(pair):
         assert_scalar(gaps[g], want, TOL, "fp32 egt balanced eps_sad")
 
 
+def _subtree_mask(tp, simplexes):
+    """Sequences of the given simplexes and of every simplex below them."""
+    bad = np.zeros(tp.n_seq, dtype=bool)
+    for k in range(tp.n_simplex):  # top-down: a parent's mark is set before its children's
+        s, n, par = tp.start[k], tp.size[k], tp.parent[k]
+        if k in simplexes or (par != 0 and bad[par]):
+            bad[s:s + n] = True
+    return bad
+
+
 def test_cfr_plus_fp32(pair):
-    if pair.kind == "kuhn" or pair.game.H > 1000:
-        # Kuhn's exact regret ties, and the Libratus-scale game's hands with zero or tiny
-        # regrets, make RM+'s [r]^+ switch on fp32 rounding noise (R18)
-        pytest.skip("regret-matching decisions at the fp32 noise level")
+    """Decision-aware (R18): RM+'s "[r]^+ / r = 0" decisions taken within 1e-4 of the
+    largest gain of the player from flipping (traced from the fp64 oracle; fp32 gains are
+    accurate to ~1e-5 of it) may go the other way in fp32; the simplexes where that happened and
+    everything below them are left out, every other entry of both averages must match at 1e-5,
+    and so must eps_sad."""
     import paper_1810_03063_b200 as P
     G = pair.game
+    T = 5
     G.cfr_init(P.CFR_PLUS)
-    G.cfr_step(5)
+    G.cfr_step(T)
     avg = _strategies(pair, 1)
+    gaps = G.saddle_gap(1)
+    compared = total = 0
     for g in range(G.n_games):
-        st = cfr.run(pair.sf[g], "cfr_plus", 5)
-        assert_parity(avg[0][g][1:], st.xbar[1:], TOL, "fp32 cfr+ xbar")
-        assert_parity(avg[1][g][1:], st.ybar[1:], TOL, "fp32 cfr+ ybar")
+        calls = []
+        st = cfr.run(pair.sf[g], "cfr_plus", T, trace=lambda p, j, m, sj: calls.append((p, j, m, sj)))
+        # fp32 gains carry ~1e-5 of the largest gain of the pass (the norm-relative bar): a
+        # regret within 1e-4 of that from the threshold may be decided the other way
+        scale = [max([c[3] for c in calls if c[0] == p] or [0.0]) for p in (0, 1)]
+        noisy = (set(), set())
+        for p, j, m, sj in calls:
+            if m <= 1e-4 * scale[p]:
+                noisy[p].add(j)
+        for p, want in ((0, st.xbar), (1, st.ybar)):
+            keep = ~_subtree_mask(pair.tp(g, p), noisy[p])
+            keep[0] = False
+            assert_parity(avg[p][g][keep], want[keep], TOL, "fp32 cfr+ average (decided entries)")
+            compared += int(keep.sum())
+            total += len(want) - 1
+        assert_scalar(gaps[g], br.saddle_gap(pair.sf[g], st.xbar, st.ybar), TOL, "fp32 cfr+ eps_sad")
+    # (exact regret ties -- Kuhn, Leduc -- and low-prior hands leave many entries out)
+    assert compared >= 0.1 * total, (compared, total)
+    print("fp32 cfr+ [%s]: %d of %d average entries compared" % (pair.kind, compared, total))
+
+
+def test_egt_as_fp32(pair):
+    """EGT/as (Alg. 3-4) in fp32 against the fp64 oracle, attempt by attempt: the accept /
+    backtrack decision (EGV >= 0) must match wherever the oracle's EGV is further than 1e-4 of
+    its scale (|phi| + |f|) from 0 (R18); up to the first decision at that noise
+    level, mu, tau, the iterate and eps_sad match at 1e-5."""
+    import paper_1810_03063_b200 as P
+    G = pair.game
+    mu = egt.theory_mu(pair.sf[0]) / 8.0
+    G.egt_init(P.EGT_AS, mu, mu)
+    states = []
+    for g in range(G.n_games):
+        prob = egt.Problem(pair.sf[g])
+        x, y = egt.initialize(prob, mu, mu)
+        states.append((prob, egt.EGTState(x, y, mu, mu), [True]))
+    n_decisions = 0
+    for attempt in range(8):
+        G.egt_step(1)
+        sc = G.egt_scalars()
+        xs, ys = _strategies(pair, 0)
+        gaps = G.saddle_gap(0)
+        for g, (prob, st, live) in enumerate(states):
+            if not live[0]:
+                continue
+            focus = "x" if st.mu_x > st.mu_y else "y"
+            mx, my, xn, yn = egt.step_xy(prob, st, focus, st.tau)
+            phi, _ = egt.smoothed_phi(prob, yn, mx)
+            f, _ = egt.smoothed_f(prob, xn, my)
+            accept = phi - f >= 0
+            if accept:
+                st.mu_x, st.mu_y, st.x, st.y = mx, my, xn, yn
+                st.t += 1
+            else:
+                st.tau *= 0.5
+                st.backtracks += 1
+            if int(sc[g, 3]) != st.t or int(sc[g, 5]) != st.backtracks:
+                assert abs(phi - f) <= 1e-4 * (abs(phi) + abs(f)), ("decision off the noise level", g, attempt)
+                live[0] = False  # a noise-level decision went the other way: stop comparing this game
+                continue
+            n_decisions += 1
+            assert_scalar(sc[g, 0], st.mu_x, TOL, "fp32 egt/as mu", floor=0)
+            assert_scalar(sc[g, 1], st.mu_y, TOL, "fp32 egt/as mu", floor=0)
+            assert_scalar(sc[g, 2], st.tau, TOL, "fp32 egt/as tau", floor=0)
+            assert_parity(xs[g][1:], st.x[1:], TOL, "fp32 egt/as x")
+            assert_parity(ys[g][1:], st.y[1:], TOL, "fp32 egt/as y")
+            assert_scalar(gaps[g], br.saddle_gap(pair.sf[g], st.x, st.y), TOL, "fp32 egt/as eps_sad")
+    assert n_decisions >= 4 * G.n_games
