@@ -676,7 +676,28 @@ static void build_card_plan(const HostGame& G, const std::vector<std::vector<int
         const int i = slots[q].pos;
         e[q] = {(slots[q].thread / 16) * CH + slots[q].s, ((i / K / 16) * K + i % K) * 2 + slots[q].which};
     }
-    const std::vector<int> xaddr = colour_addresses(colour_edges16(n_rg, n_wg * 2, e));
+    const std::vector<int> xcol = colour_edges16(n_rg, n_wg * 2, e);
+    const std::vector<int> xaddr = colour_addresses(xcol);
+    // padding slots also store (unconditionally): each gets a colour free in its write group and
+    // a fresh address of that colour, never read
+    std::vector<int> ccount(16, 0);
+    for (size_t q = 0; q < slots.size(); ++q) ccount[xcol[q]] = std::max(ccount[xcol[q]], xaddr[q] / 16 + 1);
+    std::vector<std::vector<char>> used((size_t)n_rg, std::vector<char>(16, 0));
+    for (size_t q = 0; q < slots.size(); ++q) used[(slots[q].thread / 16) * CH + slots[q].s][xcol[q]] = 1;
+    std::vector<int> pad_addr((size_t)NT * CH, -1);
+    for (int t = 0; t < NT; ++t)
+        for (int s2 = 0; s2 < CH; ++s2) {
+            const int c = t / GLN, k = (t % GLN) * CH + s2;
+            if (c < G.n_cards && k < (int)by_card[c].size()) continue;
+            std::vector<char>& u = used[(t / 16) * CH + s2];
+            int col = 0;
+            while (col < 16 && u[col]) ++col;
+            if (col == 16) throw std::runtime_error("card plan: no free colour for a padding slot");
+            u[col] = 1;
+            pad_addr[(size_t)t * CH + s2] = 16 * ccount[col]++ + col;
+        }
+    for (int col = 0; col < 16; ++col)
+        if (16 * ccount[col] > CARD_EX) throw std::runtime_error("card plan: ex exchange region too small");
     const int zero_cell = 2 * NP;  // w region: w1 [0, NP), w2 [NP, 2 NP), a zero cell
     plan.pw.assign(NP, 0u);
     plan.pr.assign(NP, 0u);
@@ -690,6 +711,8 @@ static void build_card_plan(const HostGame& G, const std::vector<std::vector<int
         for (int s = 0; s < CH; ++s) {
             const uint32_t z = (uint32_t)(zero_cell * 8);
             L[s / 2] |= (s & 1) ? z << 16 : z;
+            const int pa = pad_addr[(size_t)t * CH + s];
+            if (pa >= 0) L[3 + s / 2] |= (s & 1) ? (uint32_t)pa << 16 : (uint32_t)pa;
         }
     }
     // per segment: run heads / tails (tie-group changes inside the card's strength-ordered

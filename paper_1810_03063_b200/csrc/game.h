@@ -106,7 +106,8 @@ struct Terminal {
 constexpr int CARD_NT = 416, CARD_K = 3, CARD_GL = 8, CARD_CH = 6;
 constexpr int CARD_NP = CARD_NT * CARD_K;            // positions (>= H_pad)
 constexpr int CARD_WREGION = 2 * CARD_NP + 2;        // doubles: w1, w2, a zero cell (+ pad)
-constexpr int CARD_EX = CARD_NT * CARD_CH;           // doubles of the ex exchange
+constexpr int CARD_EX = 16 * 192;                    // doubles of the ex exchange (every slot, padding
+                                                     // included, has its own conflict-free address)
 // one board's plan as one word array (the kernel keeps one pointer): pw, pr, lohi, lane
 constexpr int CARD_TAB_PW = 0, CARD_TAB_PR = CARD_NP, CARD_TAB_LOHI = 2 * CARD_NP, CARD_TAB_LANE = 3 * CARD_NP;
 constexpr int CARD_TAB_WORDS = 3 * CARD_NP + 8 * CARD_NT;

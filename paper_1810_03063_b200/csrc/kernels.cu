@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
     // the chunk's terminals in processing order: opponent row, kind, weight, the row each one
     // completes (-1: more terminals of its row follow), its row buffer and whether it is fetched
     __shared__ int t_so[MT], t_kind[MT], t_end[MT], t_idx[MT];
+    __shared__ uint32_t t_meta[MT];  // so | (row + 1) << 12 | flags << 24 (one load per terminal)
     __shared__ double t_w[MT];
     __shared__ int s_nT;
     const int g = blockIdx.y, tid = threadIdx.x;
@@ -463,6 +464,19 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
         t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
     }
     __syncthreads();
+    // per terminal: its opponent row, the row it completes, and the decisions every thread
+    // would otherwise recompute: showdown, new opponent row, fold reusing the previous totals,
+    // the next terminal needs a new row (prefetch)
+    for (int i = tid; i < nT; i += NT) {
+        const int so = t_so[i];
+        const bool sd = t_kind[i] == 2;
+        const bool new_row = so != 0 && (i == 0 || so != t_so[i - 1]);
+        const bool reuse = i > 0 && !sd && so == t_so[i - 1];
+        const bool next_new = i + 1 < nT && t_so[i + 1] != 0 && t_so[i + 1] != so;
+        t_meta[i] = (uint32_t)so | ((uint32_t)(t_end[i] + 1) << 12) |
+                    ((uint32_t)sd << 24) | ((uint32_t)new_row << 25) | ((uint32_t)reuse << 26) | ((uint32_t)next_new << 27);
+    }
+    __syncthreads();
     if (tid == 0) {
         const unsigned bD = Hp * sizeof(T);
         mbar_expect_tx(&bar[0], bD);
@@ -509,14 +523,15 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
     __syncthreads();  // the processing order
     int q = 1;  // the buffer holding the current opponent row
     for (int li = 0; li < nT; ++li) {
-        const int so = t_so[li];
-        const bool sd = t_kind[li] == 2;
-        const bool new_row = so != 0 && (li == 0 || so != t_so[li - 1]);
+        const uint32_t meta = t_meta[li];
+        const int so = (int)(meta & 0xFFFu);
+        const bool sd = (meta >> 24) & 1u;
+        const bool new_row = (meta >> 25) & 1u;
         // a fold on the previous terminal's opponent row reuses its totals (w, T, S_c); a
         // showdown always recomputes (its per-slot terms do not survive a terminal)
-        const bool reuse = li > 0 && !sd && so == t_so[li - 1];
+        const bool reuse = (meta >> 26) & 1u;
         if (new_row) q ^= 1;
-        if (tid == 0 && li > 0 && li + 1 < nT && t_so[li + 1] != 0 && t_so[li + 1] != so) {
+        if (tid == 0 && li > 0 && ((meta >> 27) & 1u)) {
             fence_proxy_async();  // the next new row, into the other buffer
             mbar_expect_tx(&bar[2 - q], (COMB ? 2 : 1) * Hp * sizeof(T));
             bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)t_so[li + 1] * Hp, Hp * sizeof(T), &bar[2 - q]);
@@ -628,15 +643,15 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
             for (int s = 0; s < CH; ++s) rc[s] -= sS;
         }
         // ---- row end: card parts to the positions of their hands, then the output row
-        const int srow = t_end[li];
+        const int srow = (int)((meta >> 12) & 0xFFFu) - 1;
         if (srow >= 0) {
             if (ex_dirty) __syncthreads();
             {
                 const uint4 lx = __ldg(lane_g), ly = __ldg(lane_g + 1);
                 const uint32_t px[3] = {lx.w, ly.x, ly.y};
 #pragma unroll
-                for (int s = 0; s < CH; ++s) {
-                    if ((flags >> s) & 1u) Ex[half16(px[s / 2], s & 1)] = rc[s];
+                for (int s = 0; s < CH; ++s) {  // (padding slots own never-read addresses)
+                    Ex[half16(px[s / 2], s & 1)] = rc[s];
                     rc[s] = T(0);
                 }
             }
@@ -683,8 +698,10 @@ static size_t card_smem_bytes(const DevGame& G, bool comb) {
     return (size_t)G.esz * ((comb ? 5 : 3) * (size_t)CARD_NP + CARD_WREGION + CARD_NP + 4 + CARD_EX);
 }
 
-static bool card_ok(const DevGame& G) {
-    return G.card_plan && G.ident && G.all_valid && G.n_bs == 1 && G.hand_size == 2 && G.H_pad <= CARD_NP;
+static bool card_ok(const DevGame& G, const DevPlayer& P) {
+    // (terminal metadata packs sequence indices in 12 bits)
+    return G.card_plan && G.ident && G.all_valid && G.n_bs == 1 && G.hand_size == 2 && G.H_pad <= CARD_NP &&
+           P.n_pub < 4095;
 }
 
 template <class T>
@@ -693,7 +710,7 @@ static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int p
                                      const GradComb* comb) {
     const VecRef b = comb ? comb->b : VecRef();
     const double* tau = comb ? comb->tau : nullptr;
-    if (card_ok(G) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
+    if (card_ok(G, P) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
         if (comb)

@@ -103,17 +103,18 @@ int main(int argc, char** argv) {
                     for (int i = 0; i < H; ++i)
                         if (c < G.n_cards && (cards[i][0] == c || cards[i][1] == c)) hold.push_back(i);
                     if (valid != (k < (int)hold.size())) { fail("valid flag", g, t, s); continue; }
+                    const unsigned px = (s & 1) ? L[3 + s / 2] >> 16 : L[3 + s / 2] & 0xFFFFu;
+                    if (px >= (unsigned)CARD_EX) { fail("ex offset", g, t, s); continue; }
+                    if (!xbanks.insert(px % 16).second) fail("ex write conflict", g, hw, s);
+                    if (ex_slot_pos[px] != -1) fail("ex address shared", g, t, s);
                     if (!valid) {
                         if (cg / 8 != (unsigned)(2 * NP)) fail("padding slot not on the zero cell", g, t, s);
+                        ex_slot_pos[px] = -2;  // a padding slot's private address (never read)
                         continue;
                     }
                     const int i = hold[k];
                     if (w[cg / 8] != 1.0 + i) fail("gather delivers the wrong weight", g, t, s);
                     if (!rbanks.insert((cg / 8) % 16).second) fail("w read conflict", g, hw, s);
-                    const unsigned px = (s & 1) ? L[3 + s / 2] >> 16 : L[3 + s / 2] & 0xFFFFu;
-                    if (px >= (unsigned)CARD_EX) { fail("ex offset", g, t, s); continue; }
-                    if (!xbanks.insert(px % 16).second) fail("ex write conflict", g, hw, s);
-                    if (ex_slot_pos[px] >= 0) fail("ex address shared", g, t, s);
                     ex_slot_pos[px] = i;
                     ex_slot_card[px] = c;
                 }
