@@ -8,6 +8,8 @@
 //                 update PAPER.md:30-39/63-64/84-85), then top-down rescale by the
 //                 parent sequence with the EGT convex combinations fused.
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 
 #include "kernels.cuh"
@@ -688,6 +690,274 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
     }
 }
 
+// ------------------------------------------------------------------ staged river gradient
+// The same gradient with the card parts read per position instead of accumulated per slot
+// (round 1's design): every card's segment of the card array (its hands in strength order,
+// padding, an end slot) is scanned by 8 lanes and its exclusive prefixes are stored; phase C
+// reads, per position, the segment totals S_c and the prefixes at its tie group's bounds
+// Pc[lo], Pc[hi] (PC_* offsets), and the position prefixes P[lo], P[hi].  The position ->
+// card gather of phase B goes through the card plan's conflict-free w1 / w2 exchange (game.h
+// CardPlan); chunk terminal order, opponent-row double buffering and the fused x_hat input
+// (COMB) as in grad_card_kernel.  Measured faster than the card-domain kernel on the bench
+// workload, so it is the one the library launches.
+template <typename T, bool COMB>
+__global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevPlayer P, int player, VecRef vin,
+                                                                 VecRef gout, const int* __restrict__ mask, int want,
+                                                                 DevPeers peers, VecRef vin2,
+                                                                 const double* __restrict__ ctau) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    constexpr int NT = CARD_NT, K = CARD_K, CH = CARD_CH, NW = NT / 32, NP = CARD_NP, MT = GRAD_CHUNK_MAX_TERMS;
+    __shared__ T wtot[NW];
+    __shared__ __align__(8) uint64_t bar[3];
+    __shared__ int t_so[MT], t_kind[MT], t_end[MT], t_idx[MT];
+    __shared__ uint32_t t_meta[MT];  // so | (row + 1) << 12 | flags << 24
+    __shared__ double t_w[MT];
+    __shared__ int s_nT;
+    const int g = blockIdx.y, tid = threadIdx.x;
+    if (mask && mask[g] != want) return;
+    const int Hp = G.H_pad, H = G.H, W = G.seg_w, n_ce = G.n_ce;
+    T* popp = reinterpret_cast<T*>(sm_raw);  // [NP] (0 beyond H)
+    T* vb = popp + NP;                       // [2][NP] opponent rows (0 beyond Hp)
+    T* vb2 = vb + 2 * NP;                    // COMB: [2][NP] the second input's rows
+    T* wreg = vb2 + (COMB ? 2 * NP : 0);     // [CARD_WREGION] w1 | w2 | zero cell
+    T* Pf = wreg + CARD_WREGION;             // [NP + 4] exclusive prefixes of w by position
+    T* Ex = Pf + NP + 4;                     // [n_ce] card array: exclusive prefixes per segment
+    const int r0 = P.chunk_off[blockIdx.x], r1 = P.chunk_off[blockIdx.x + 1];
+    const T* __restrict__ vo = vin.at<T>(g);
+    const T* __restrict__ vo2 = COMB ? vin2.at<T>(g) : nullptr;
+    if (tid == 0) {
+        int n = 0;
+        for (int r = r0; r < r1; ++r) {
+            const int srow = P.rows_term[r];
+            for (int k = P.term_off[srow]; k < P.term_off[srow + 1]; ++k) {
+                t_idx[n] = P.term_idx[k];
+                t_end[n] = k + 1 == P.term_off[srow + 1] ? srow : -1;
+                ++n;
+            }
+        }
+        s_nT = n;
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = Hp + tid; i < NP; i += NT) {
+        popp[i] = T(0);
+        vb[i] = T(0);
+        vb[NP + i] = T(0);
+        if (COMB) {
+            vb2[i] = T(0);
+            vb2[NP + i] = T(0);
+        }
+    }
+    if (tid < CARD_WREGION - 2 * NP) wreg[2 * NP + tid] = T(0);
+    if (tid < 4) Pf[NP + tid] = T(0);
+    __syncthreads();
+    const int nT = s_nT;
+    for (int i = tid; i < nT; i += NT) {
+        const DevTerm tm = G.terms[t_idx[i]];
+        t_so[i] = player ? tm.seq[0] : tm.seq[1];
+        t_kind[i] = tm.kind;
+        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
+    }
+    __syncthreads();
+    for (int i = tid; i < nT; i += NT) {
+        const int so = t_so[i];
+        const bool sd = t_kind[i] == 2;
+        const bool new_row = so != 0 && (i == 0 || so != t_so[i - 1]);
+        const bool reuse = i > 0 && so == t_so[i - 1];
+        // the card-array prefixes and P are needed by a showdown, also one that follows on the
+        // same opponent row (then the first of the pair writes them)
+        const bool full = sd || (i + 1 < nT && t_so[i + 1] == so && t_kind[i + 1] == 2);
+        const bool next_new = i + 1 < nT && t_so[i + 1] != 0 && t_so[i + 1] != so;
+        t_meta[i] = (uint32_t)so | ((uint32_t)(t_end[i] + 1) << 12) | ((uint32_t)sd << 24) |
+                    ((uint32_t)new_row << 25) | ((uint32_t)reuse << 26) | ((uint32_t)next_new << 27) |
+                    ((uint32_t)full << 28);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned bD = Hp * sizeof(T);
+        mbar_expect_tx(&bar[0], bD);
+        bulk_g2s(popp, static_cast<const T*>(player ? G.prior[0] : G.prior[1]) + (size_t)g * Hp, bD, &bar[0]);
+        int b = 1;
+        for (int q = 0; q < 2 && q < nT; ++q)
+            if (t_so[q] != 0 && (q == 0 || t_so[q] != t_so[q - 1])) {
+                b ^= 1;
+                mbar_expect_tx(&bar[1 + b], COMB ? 2 * bD : bD);
+                bulk_g2s(vb + b * NP, vo + (size_t)t_so[q] * Hp, bD, &bar[1 + b]);
+                if (COMB) bulk_g2s(vb2 + b * NP, vo2 + (size_t)t_so[q] * Hp, bD, &bar[1 + b]);
+            }
+    }
+    const int lane = tid & 31, wid = tid >> 5;
+    const int base = tid * K, part = tid & (CARD_GL - 1), sgi = tid / CARD_GL;
+    const bool has_seg = sgi < G.n_cards;
+    const uint32_t* __restrict__ tab = G.card_tab + (size_t)g * CARD_TAB_WORDS;
+    const uint4 la = __ldg(reinterpret_cast<const uint4*>(tab + CARD_TAB_LANE) + tid * 2);
+    const uint32_t cg[3] = {la.x, la.y, la.z};
+    // the card-array slots this thread writes: all of them (bits 0-5) or only its segment's
+    // end slot (bits 8-13); bits 16+ mark positions alone in their tie group
+    unsigned masks = 0u;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+        const int e = part * CH + j;
+        if (has_seg && e < W) {
+            masks |= 1u << j;
+            if (e == W - 1) masks |= 1u << (8 + j);
+        }
+    }
+    T* const exs = Ex + sgi * W + part * CH;
+    uint2 pcr[K];
+    uint32_t lhr[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int i = base + j;
+        pcr[j] = i < Hp ? G.tab_pcard[(size_t)g * Hp + i] : make_uint2(0u, 0u);
+        lhr[j] = i < Hp ? G.tab_lohi[(size_t)g * Hp + i] : 0u;
+        if ((int)(lhr[j] & 0xFFFFu) == i && (int)(lhr[j] >> 16) == i + 1) masks |= 1u << (16 + j);
+    }
+    const uint32_t* __restrict__ pw_g = tab + CARD_TAB_PW + base;
+    const T* __restrict__ pself_g = static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
+    unsigned char* const wbytes = reinterpret_cast<unsigned char*>(wreg);
+    const T sd_sign = player == 0 ? T(1) : T(-1);
+    const T ct = COMB ? (T)ctau[g] : T(0), ct1 = T(1) - ct;  // Alg. 2 line 1
+    T racc[K], x[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) racc[j] = x[j] = T(0);
+    T total = T(0), pbase = T(0);
+    unsigned par = 0u;
+    int q = 1;
+    mbar_wait(&bar[0], 0);
+    __syncthreads();
+    for (int li = 0; li < nT; ++li) {
+        const uint32_t meta = t_meta[li];
+        const int so = (int)(meta & 0xFFFu);
+        const bool sd = (meta >> 24) & 1u, new_row = (meta >> 25) & 1u, reuse = (meta >> 26) & 1u;
+        const bool full = (meta >> 28) & 1u;
+        if (new_row) q ^= 1;
+        if (tid == 0 && li > 0 && ((meta >> 27) & 1u)) {
+            fence_proxy_async();
+            mbar_expect_tx(&bar[2 - q], (COMB ? 2 : 1) * Hp * sizeof(T));
+            bulk_g2s(vb + (q ^ 1) * NP, vo + (size_t)t_so[li + 1] * Hp, Hp * sizeof(T), &bar[2 - q]);
+            if (COMB) bulk_g2s(vb2 + (q ^ 1) * NP, vo2 + (size_t)t_so[li + 1] * Hp, Hp * sizeof(T), &bar[2 - q]);
+        }
+        if (new_row) {
+            mbar_wait(&bar[1 + q], (par >> q) & 1u);
+            par ^= 1u << q;
+        }
+        if (!reuse) {  // CTA-uniform
+            // ---- phase A: w = prior_opp * v_opp (COMB: v = x_hat), its conflict-free copies
+            const T* vrow = vb + q * NP;
+            const T* vrow2 = vb2 + q * NP;
+            T run = T(0);
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const T v = COMB ? ct1 * vrow[base + j] + ct * vrow2[base + j] : vrow[base + j];
+                x[j] = so ? popp[base + j] * v : popp[base + j];
+                run += x[j];
+                if (base + j < H) {
+                    const uint32_t pw = __ldg(pw_g + j);
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 0)) = x[j];
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 1)) = x[j];
+                }
+            }
+            const T incl = warp_incl_scan(run, lane);
+            if (lane == 31) wtot[wid] = incl;
+            __syncthreads();
+            // ---- phase B: card sums (segment scans inside lane groups) and the block prefix of w
+            {
+                T y[CH], ssum = T(0);
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    y[j] = *reinterpret_cast<const T*>(wbytes + woff<T>(cg[j / 2], j & 1));
+                    ssum += y[j];
+                }
+                T inc = ssum;
+#pragma unroll
+                for (int o = 1; o < CARD_GL; o <<= 1) {
+                    const T u = __shfl_up_sync(0xffffffffu, inc, o, CARD_GL);
+                    if (part >= o) inc += u;
+                }
+                // the same accumulation order in both cases, so a segment total never depends on
+                // whether the terminal needs the full prefixes (folds: end slot only)
+                const unsigned wm = full ? masks : masks >> 8;
+                T run2 = inc - ssum;
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    if (wm & (1u << j)) exs[j] = run2;
+                    run2 += y[j];
+                }
+            }
+            const T wsc = warp_incl_scan_lim<(NW <= 16 ? 16 : 32)>(lane < NW ? wtot[lane] : T(0), lane);
+            const T wpre_incl = __shfl_sync(0xffffffffu, wsc, (wid + 31) & 31);
+            const T wpre = wid ? wpre_incl : T(0);
+            total = __shfl_sync(0xffffffffu, wsc, NW - 1);
+            pbase = wpre + incl - run;
+            if (full) {
+                T pp = pbase;
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    Pf[base + j] = pp;
+                    pp += x[j];
+                }
+                if (tid == 0) Pf[NP] = total;
+            }
+            __syncthreads();
+        }
+        // ---- phase C (positions beyond H compute on padding and are never stored)
+        const T scale = (T)t_w[li];
+        T pre = pbase;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const uint2 pc = pcr[j];
+            T v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)] - Ex[PC_START(pc.y) + PC_LEN(pc.y)];
+            if (sd) {
+                const uint32_t lh = lhr[j];
+                if (masks & (1u << (16 + j))) {  // alone in its tie group: its own prefixes
+                    const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)], cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
+                    v += -(pre + (pre + x[j])) + (ca + (ca + x[j])) + (cb + (cb + x[j]));
+                } else {
+                    v += -(Pf[lh & 0xFFFFu] + Pf[lh >> 16]) + Ex[PC_START(pc.x) + PC_RELO(pc.x)] +
+                         Ex[PC_START(pc.x) + PC_REHI(pc.x)] + Ex[PC_START(pc.y) + PC_RELO(pc.y)] +
+                         Ex[PC_START(pc.y) + PC_REHI(pc.y)];
+                }
+                v *= sd_sign;
+            } else {
+                v += x[j];
+            }
+            racc[j] += scale * v;
+            pre += x[j];
+        }
+        // ---- row end: prior_self * acc straight from registers to the output row(s)
+        const int srow = (int)((meta >> 12) & 0xFFFu) - 1;
+        if (srow >= 0) {
+            T outv[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const int i = base + j;
+                outv[j] = i < H ? __ldg(pself_g + i) * racc[j] : T(0);
+                racc[j] = T(0);
+            }
+            if (peers.n == 0) {
+                T* __restrict__ dst = gout.at<T>(g) + (size_t)srow * Hp;
+#pragma unroll
+                for (int j = 0; j < K; ++j)
+                    if (base + j < Hp) dst[base + j] = outv[j];
+            } else {
+                const long long off = (long long)g * gout.game_stride + (long long)srow * Hp;
+#pragma unroll
+                for (int d = 0; d < EGT_MAX_PEERS; ++d) {
+                    if (d < peers.n) {
+                        T* __restrict__ dst = reinterpret_cast<T*>(peers.base[d]) + off;
+#pragma unroll
+                        for (int j = 0; j < K; ++j)
+                            if (base + j < Hp) dst[base + j] = outv[j];
+                    }
+                }
+            }
+        }
+    }
+}
+
 static constexpr int GRAD_NT = 512, GRAD_KMAX = 3, GRAD_EMAX = 6;  // H <= 1536, card array <= 3072
 
 static size_t grad_smem_bytes(const DevGame& G) {
@@ -696,6 +966,19 @@ static size_t grad_smem_bytes(const DevGame& G) {
 
 static size_t card_smem_bytes(const DevGame& G, bool comb) {
     return (size_t)G.esz * ((comb ? 5 : 3) * (size_t)CARD_NP + CARD_WREGION + CARD_NP + 4 + CARD_EX);
+}
+
+static size_t staged_smem_bytes(const DevGame& G, bool comb) {
+    return (size_t)G.esz * ((comb ? 5 : 3) * (size_t)CARD_NP + CARD_WREGION + CARD_NP + 4 + G.n_ce);
+}
+
+// EGT_GRAD_KERNEL=card selects the card-domain kernel (measurement); default: the staged one
+static bool use_card_kernel() {
+    static const bool card = [] {
+        const char* v = std::getenv("EGT_GRAD_KERNEL");
+        return v && std::strcmp(v, "card") == 0;
+    }();
+    return card;
 }
 
 static bool card_ok(const DevGame& G, const DevPlayer& P) {
@@ -710,6 +993,17 @@ static cudaError_t launch_gradient_t(const DevGame& G, const DevPlayer& P, int p
                                      const GradComb* comb) {
     const VecRef b = comb ? comb->b : VecRef();
     const double* tau = comb ? comb->tau : nullptr;
+    if (card_ok(G, P) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS && !use_card_kernel()) {
+        if (P.n_chunks == 0) return cudaSuccess;
+        dim3 grid(P.n_chunks, G.n_games);
+        if (comb)
+            grad_staged_kernel<T, true><<<grid, CARD_NT, staged_smem_bytes(G, true), st>>>(G, P, player, vin, gout,
+                                                                                           mask, want, peers, b, tau);
+        else
+            grad_staged_kernel<T, false><<<grid, CARD_NT, staged_smem_bytes(G, false), st>>>(G, P, player, vin, gout,
+                                                                                             mask, want, peers, b, tau);
+        return cudaGetLastError();
+    }
     if (card_ok(G, P) && P.max_chunk_terms <= GRAD_CHUNK_MAX_TERMS) {
         if (P.n_chunks == 0) return cudaSuccess;
         dim3 grid(P.n_chunks, G.n_games);
@@ -1370,6 +1664,10 @@ static cudaError_t prepare_t() {
     const int lim = 200 * 1024;
     cudaError_t e = cudaFuncSetAttribute(grad_kernel<GRAD_NT, GRAD_KMAX, GRAD_EMAX, T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grad_staged_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(grad_staged_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(grad_card_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     if (e == cudaSuccess)
