@@ -41,16 +41,12 @@ __device__ __forceinline__ T warp_incl_scan_lim(T v, int lane) {
 
 // exp(x) for x <= 0 to ~1 ulp: x = (64 k + j) ln2 / 64 + r, |r| <= ln2 / 128,
 // exp(x) = 2^k' * tab[j] * (1 + r + ... + r^5/120) (truncation < 4e-17 relative).
-// tab[j] = 2^(j/64) lives in shared memory.  Results below the normal range underflow
-// gradually (subnormals, one rounding), and to 0 below -745.2 (also for x = -inf), as
-// IEEE exp does -- no floor (the oracle's numpy exp underflows the same way).
-__device__ __noinline__ double exp_subnormal(double v, int e) {
-    // v in [1, 2), 2^e below the normal range: scale in two exact-then-rounding steps
-    const double a = __hiloint2double((e + 600 + 1023) << 20, 0);  // 2^(e + 600), normal
-    return (v * a) * 0x1p-600;
-}
+// tab[j] = 2^(j/64) lives in shared memory.  2^k' is applied as 2^(k'+600) * 2^-600, two exact
+// scalings for normal results and one rounding where the result is subnormal, so the result
+// underflows gradually and reaches 0 below -745.2 as IEEE exp does -- no floor, no branch (the
+// oracle's numpy exp underflows the same way); -inf (and anything below -800) gives 0.
 __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict__ tab) {
-    if (!(x >= -745.2)) return 0.0;  // incl. -inf (NaN propagates as 0: inputs are finite)
+    x = fmax(x, -800.0);
     const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
     const double big = fma(x, 92.332482616893656877, magic);
     const int k = __double2loint(big);
@@ -63,9 +59,8 @@ __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict_
     p = fma(p, r, 1.0);
     p = fma(p, r, 1.0);
     const double v = tab[k & 63] * p;
-    const int e = k >> 6;
-    if (e < -1021) return exp_subnormal(v, e);
-    return __hiloint2double(__double2hiint(v) + (e << 20), __double2loint(v));
+    const double scale = __hiloint2double(((k >> 6) + 600 + 1023) << 20, 0);  // 2^(k'+600), normal
+    return (v * scale) * 0x1p-600;
 }
 
 // fp32 mode: the library exp on non-positive arguments (<= 2 ulp)
@@ -715,7 +710,7 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
     __shared__ int s_nT;
     const int g = blockIdx.y, tid = threadIdx.x;
     if (mask && mask[g] != want) return;
-    const int Hp = G.H_pad, H = G.H, W = G.seg_w, n_ce = G.n_ce;
+    const int Hp = G.H_pad, H = G.H, W = G.seg_w;
     T* popp = reinterpret_cast<T*>(sm_raw);  // [NP] (0 beyond H)
     T* vb = popp + NP;                       // [2][NP] opponent rows (0 beyond Hp)
     T* vb2 = vb + 2 * NP;                    // COMB: [2][NP] the second input's rows
@@ -1166,7 +1161,7 @@ __device__ __forceinline__ T tree_node_up(const TreeNodeCtx<T>& C, const DevPlay
 
 // The same bottom-up work for a node with a compile-time number of actions N: the N
 // entries are read once into registers and written once.
-template <int N, int MODE, class T>
+template <int N, int MODE, class T, int LB>
 __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                  int m, int h, int Hp, T logn, T* __restrict__ cz,
                                                  T* __restrict__ rg, T sc, T wgt, T iw) {
@@ -1175,7 +1170,21 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
     for (int a = 0; a < N; ++a) x[a] = sc * col[a * TH_HANDS];
     constexpr int mode = MODE;
     T value;
-    if (mode == TM_SBR) {
+    if (mode == TM_SBR && LB == 0) {  // no log output: the exponentials overwrite x in place
+        T mn = x[0];
+#pragma unroll
+        for (int a = 1; a < N; ++a) mn = fmin(mn, x[a]);
+        T S = T(0);
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            x[a] = exp_nonpos((mn - x[a]) * iw, C.exptab);
+            S += x[a];
+        }
+        const T inv = rcp_pos(S);
+#pragma unroll
+        for (int a = 0; a < N; ++a) x[a] *= inv;
+        value = mn - wgt * (log_ge1(S, C.exptab) - logn);
+    } else if (mode == TM_SBR) {
         T mn = x[0];
 #pragma unroll
         for (int a = 1; a < N; ++a) mn = fmin(mn, x[a]);
@@ -1187,7 +1196,7 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
             S += e[a];
         }
         const T inv = rcp_pos(S), lS = log_ge1(S, C.exptab);
-        if (C.lbo) {
+        if (LB == 1 || C.lbo) {
 #pragma unroll
             for (int a = 0; a < N; ++a) C.lbo[(size_t)(first + a) * Hp + h] = x[a] - lS;
         }
@@ -1260,7 +1269,7 @@ __device__ __forceinline__ T tree_node_up_n(const TreeNodeCtx<T>& C, const DevPl
     return value;
 }
 
-template <int MODE, class T>
+template <int MODE, class T, int LB>
 __device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const DevPlayer& P, T* col, int first,
                                                    int n, int m, int h, int Hp, T logn, T* __restrict__ cz,
                                                    T* __restrict__ rg, T sc, T wgt, T iw) {
@@ -1270,7 +1279,7 @@ __device__ __forceinline__ T tree_node_up_any(const TreeNodeCtx<T>& C, const Dev
     switch (n) {  // warp-uniform: every lane works on the same node
 #define EGT_NODE_CASE(K) \
     case K:              \
-        if (K <= NMAX) return tree_node_up_n<(K <= NMAX ? K : 1), MODE, T>(C, P, col, first, m, h, Hp, logn, cz, rg, sc, wgt, iw); \
+        if (K <= NMAX) return tree_node_up_n<(K <= NMAX ? K : 1), MODE, T, LB>(C, P, col, first, m, h, Hp, logn, cz, rg, sc, wgt, iw); \
         break;
         EGT_NODE_CASE(1) EGT_NODE_CASE(2) EGT_NODE_CASE(3) EGT_NODE_CASE(4) EGT_NODE_CASE(5) EGT_NODE_CASE(6)
         EGT_NODE_CASE(7) EGT_NODE_CASE(8) EGT_NODE_CASE(9)
@@ -1506,7 +1515,9 @@ __global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, D
                             iw = T(1) / wgt;
                         }
                         if (MODE == TM_CFR) C.cfr_scale = cfr_scale[j];
-                        value = tree_node_up_any<MODE, T>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
+                        // the log output is known at compile time for the hot (mode, outputs) kernels
+                        constexpr int LB = OUTS ? ((OUTS & TO_LB) ? 1 : 0) : 2;
+                        value = tree_node_up_any<MODE, T, LB>(C, P, col, first, n, m, h, Hp, logn, cz, rg, sc, wgt, iw);
                     } else {
                         for (int a = 0; a < n; ++a) col[a * TH_HANDS] = T(0);
                         if (lbo && h < Hp)

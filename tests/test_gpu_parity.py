@@ -268,3 +268,42 @@ def _n_cards(pair):
 
 def _combo_index(c1, c2, n):
     return c1 * (2 * n - c1 - 1) // 2 + (c2 - c1 - 1)
+
+
+def test_card_domain_kernel_parity():
+    """The card-domain gradient kernel (EGT_GRAD_KERNEL=card; the library launches the staged
+    one by default) against the oracle, in a process of its own (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch
+from paper_1810_03063_b200 import workloads
+from tests.paritylib import Pair, assert_parity, random_behavioral
+for spec, seed, nr, ns in ((workloads.river_spec("libratus"), 4, 13, 4), (workloads.river_spec("simple"), 9, 8, 4)):
+    pair = Pair("river", n_games=2, spec=spec, seed=seed, n_ranks=nr, n_suits=ns, build_sparse=False)
+    G = pair.game
+    rng = np.random.default_rng(1)
+    for p in (0, 1):
+        o = 1 - p
+        blocks, vals = [], []
+        for g in range(G.n_games):
+            v = pair.tp(g, o).behavioral_to_sequence(random_behavioral(pair.tp(g, o), rng))
+            vals.append(v)
+            blocks.append(pair.to_product(g, o, v, row0=1.0))
+        din = torch.tensor(np.stack(blocks).reshape(G.vec_shape(o)), device="cuda")
+        dout = torch.full(G.vec_shape(p), np.nan, dtype=torch.float64, device="cuda")
+        G.egt_gradient(p, din, dout)
+        torch.cuda.synchronize()
+        out = dout.cpu().numpy().reshape(G.n_games, -1)
+        for g in range(G.n_games):
+            want = pair.sf[g].Ay(vals[g]) if p == 0 else pair.sf[g].ATx(vals[g])
+            got = pair.from_product(g, p, out[g])
+            got[0] = out[g][:G.H_pad].sum()
+            assert_parity(got, want, 1e-9, "card-domain gradient")
+print("card kernel ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EGT_GRAD_KERNEL="card", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "card kernel ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
