@@ -231,3 +231,32 @@ def test_practical_mu_bench_batch():
                   floor=1e-12 + 30.0 * abs(pert["gap"] - want["gap"]))
     print("bench batch: game %d, %d backtracks in %d attempts; games with a backtrack: %d"
           % (g_bt, want["backtracks"], N_ATTEMPTS, len(bt)))
+
+
+def test_egt_init_independent_of_previous_state():
+    """egt_init with the practical mu on a game that already ran CFR, and a second egt_init on
+    the same game, leave exactly the state a fresh game's egt_init does (no stale scratch: the
+    mu scan's omega gradient writes every row; round 1 read an unwritten buffer there), and that
+    state is the oracle's practical mu and initial point (Alg. 3 lines 1-2)."""
+    import paper_1810_03063_b200 as P
+    pair = Pair(kind="leduc", n_games=1)
+    G = pair.game
+    G.cfr_init(P.CFR_PLUS)
+    G.cfr_step(3)
+    states = []
+    for _ in range(2):
+        G.egt_init(P.EGT_AS)
+        xs, ys = _strategies(G)
+        states.append((G.egt_scalars()[:, :3].copy(), xs, ys))
+    fresh = Pair(kind="leduc", n_games=1).game
+    fresh.egt_init(P.EGT_AS)
+    fx, fy = _strategies(fresh)
+    for sc, xs, ys in states:
+        assert np.array_equal(sc, fresh.egt_scalars()[:, :3])
+        assert np.array_equal(xs, fx) and np.array_equal(ys, fy)
+    k, mu = egt.practical_mu(pair.sf[0])
+    prob = egt.Problem(pair.sf[0])
+    x0, y0 = egt.initialize(prob, mu, mu)
+    assert_scalar(states[0][0][0, 0], mu, 1e-14, "re-init practical mu", floor=0)
+    assert_parity(pair.from_product(0, 0, fx[0])[1:], x0[1:], TOL, "re-init x0")
+    assert_parity(pair.from_product(0, 1, fy[0])[1:], y0[1:], TOL, "re-init y0")
