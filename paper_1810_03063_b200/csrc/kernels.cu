@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
     const uint32_t* __restrict__ tab = G.card_tab + (size_t)g * CARD_TAB_WORDS;
     const uint4* __restrict__ lane_g = reinterpret_cast<const uint4*>(tab + CARD_TAB_LANE) + tid * 2;
     const uint4 la = __ldg(lane_g), lb = __ldg(lane_g + 1);
-    const uint32_t cg[3] = {la.x, la.y, la.z};
+    uint32_t cg[3] = {la.x, la.y, la.z};
     const uint32_t flags = lb.z;
     const int src_lo = (int)(lb.w & 31u), src_hi = (int)((lb.w >> 8) & 31u);
     const T sd_sign = player == 0 ? T(1) : T(-1);
@@ -753,7 +753,8 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
         const DevTerm tm = G.terms[t_idx[i]];
         t_so[i] = player ? tm.seq[0] : tm.seq[1];
         t_kind[i] = tm.kind;
-        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
+        // the showdown sign (+ for A y: player 2 wins with the stronger hand) goes into the weight
+        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount * (tm.kind == 2 && player ? -1.0 : 1.0);
     }
     __syncthreads();
     for (int i = tid; i < nT; i += NT) {
@@ -788,9 +789,9 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
     const bool has_seg = sgi < G.n_cards;
     const uint32_t* __restrict__ tab = G.card_tab + (size_t)g * CARD_TAB_WORDS;
     const uint4 la = __ldg(reinterpret_cast<const uint4*>(tab + CARD_TAB_LANE) + tid * 2);
-    const uint32_t cg[3] = {la.x, la.y, la.z};
+    uint32_t cg[3] = {la.x, la.y, la.z};
     // the card-array slots this thread writes: all of them (bits 0-5) or only its segment's
-    // end slot (bits 8-13); bits 16+ mark positions alone in their tie group
+    // end slot (bits 8-13)
     unsigned masks = 0u;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
@@ -801,20 +802,30 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
         }
     }
     T* const exs = Ex + sgi * W + part * CH;
-    uint2 pcr[K];
-    uint32_t lhr[K];
+    // phase C's shared-memory operands as byte offsets from Pf, two per word: [0] the segment
+    // ends of the hand's two cards (S_c), [1] / [2] card x's / card y's prefixes at the tie
+    // group's bounds, [3] the position prefixes at them
+    uint32_t pa[K][4], pwr[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         const int i = base + j;
-        pcr[j] = i < Hp ? G.tab_pcard[(size_t)g * Hp + i] : make_uint2(0u, 0u);
-        lhr[j] = i < Hp ? G.tab_lohi[(size_t)g * Hp + i] : 0u;
-        if ((int)(lhr[j] & 0xFFFFu) == i && (int)(lhr[j] >> 16) == i + 1) masks |= 1u << (16 + j);
+        const uint2 pc = i < Hp ? G.tab_pcard[(size_t)g * Hp + i] : make_uint2(0u, 0u);
+        const uint32_t lh = i < Hp ? G.tab_lohi[(size_t)g * Hp + i] : 0u;
+        const uint32_t e0 = (NP + 4) * sizeof(T);
+        const uint32_t sx = e0 + PC_START(pc.x) * sizeof(T), sy = e0 + PC_START(pc.y) * sizeof(T);
+        pa[j][0] = (sx + PC_LEN(pc.x) * sizeof(T)) | (sy + PC_LEN(pc.y) * sizeof(T)) << 16;
+        pa[j][1] = (sx + PC_RELO(pc.x) * sizeof(T)) | (sx + PC_REHI(pc.x) * sizeof(T)) << 16;
+        pa[j][2] = (sy + PC_RELO(pc.y) * sizeof(T)) | (sy + PC_REHI(pc.y) * sizeof(T)) << 16;
+        pa[j][3] = (lh & 0xFFFFu) * sizeof(T) | ((lh >> 16) * sizeof(T)) << 16;
+        pwr[j] = i < H ? __ldg(tab + CARD_TAB_PW + i) : 0u;
     }
-    const uint32_t* __restrict__ pw_g = tab + CARD_TAB_PW + base;
+    const unsigned char* const pfb = reinterpret_cast<const unsigned char*>(Pf);
+    auto ldo = [pfb](uint32_t v, int hi) { return *reinterpret_cast<const T*>(pfb + (hi ? v >> 16 : v & 0xFFFFu)); };
     const T* __restrict__ pself_g = static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
     unsigned char* const wbytes = reinterpret_cast<unsigned char*>(wreg);
-    const T sd_sign = player == 0 ? T(1) : T(-1);
     const T ct = COMB ? (T)ctau[g] : T(0), ct1 = T(1) - ct;  // Alg. 2 line 1
+    T* const gdst = gout.at<T>(g);
+    const long long goff = (long long)g * gout.game_stride;
     T racc[K], x[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) racc[j] = x[j] = T(0);
@@ -824,6 +835,17 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
     mbar_wait(&bar[0], 0);
     __syncthreads();
     for (int li = 0; li < nT; ++li) {
+        // the per-thread address words re-enter the loop as opaque values every terminal, so
+        // the compiler decodes each 16-bit field where it is used (one instruction) instead of
+        // keeping ~30 decoded addresses live across the loop (72 registers: spills and
+        // rematerialised index arithmetic otherwise, ~9 % slower)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) asm volatile("" : "+r"(pa[j][k]));
+            asm volatile("" : "+r"(pwr[j]));
+        }
+        asm volatile("" : "+r"(cg[0]), "+r"(cg[1]), "+r"(cg[2]));
         const uint32_t meta = t_meta[li];
         const int so = (int)(meta & 0xFFFu);
         const bool sd = (meta >> 24) & 1u, new_row = (meta >> 25) & 1u, reuse = (meta >> 26) & 1u;
@@ -850,9 +872,8 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
                 x[j] = so ? popp[base + j] * v : popp[base + j];
                 run += x[j];
                 if (base + j < H) {
-                    const uint32_t pw = __ldg(pw_g + j);
-                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 0)) = x[j];
-                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 1)) = x[j];
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pwr[j], 0)) = x[j];
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pwr[j], 1)) = x[j];
                 }
             }
             const T incl = warp_incl_scan(run, lane);
@@ -900,27 +921,16 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
         }
         // ---- phase C (positions beyond H compute on padding and are never stored)
         const T scale = (T)t_w[li];
-        T pre = pbase;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            const uint2 pc = pcr[j];
-            T v = total - Ex[PC_START(pc.x) + PC_LEN(pc.x)] - Ex[PC_START(pc.y) + PC_LEN(pc.y)];
+            T v = total - ldo(pa[j][0], 0) - ldo(pa[j][0], 1);
             if (sd) {
-                const uint32_t lh = lhr[j];
-                if (masks & (1u << (16 + j))) {  // alone in its tie group: its own prefixes
-                    const T ca = Ex[PC_START(pc.x) + PC_RELO(pc.x)], cb = Ex[PC_START(pc.y) + PC_RELO(pc.y)];
-                    v += -(pre + (pre + x[j])) + (ca + (ca + x[j])) + (cb + (cb + x[j]));
-                } else {
-                    v += -(Pf[lh & 0xFFFFu] + Pf[lh >> 16]) + Ex[PC_START(pc.x) + PC_RELO(pc.x)] +
-                         Ex[PC_START(pc.x) + PC_REHI(pc.x)] + Ex[PC_START(pc.y) + PC_RELO(pc.y)] +
-                         Ex[PC_START(pc.y) + PC_REHI(pc.y)];
-                }
-                v *= sd_sign;
+                v += -(ldo(pa[j][3], 0) + ldo(pa[j][3], 1)) + ldo(pa[j][1], 0) + ldo(pa[j][1], 1) +
+                     ldo(pa[j][2], 0) + ldo(pa[j][2], 1);
             } else {
-                v += x[j];
+                v += *reinterpret_cast<const T*>(wbytes + woff<T>(pwr[j], 0));
             }
             racc[j] += scale * v;
-            pre += x[j];
         }
         // ---- row end: prior_self * acc straight from registers to the output row(s)
         const int srow = (int)((meta >> 12) & 0xFFFu) - 1;
@@ -933,12 +943,12 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
                 racc[j] = T(0);
             }
             if (peers.n == 0) {
-                T* __restrict__ dst = gout.at<T>(g) + (size_t)srow * Hp;
+                T* __restrict__ dst = gdst + (size_t)srow * Hp;
 #pragma unroll
                 for (int j = 0; j < K; ++j)
                     if (base + j < Hp) dst[base + j] = outv[j];
             } else {
-                const long long off = (long long)g * gout.game_stride + (long long)srow * Hp;
+                const long long off = goff + (long long)srow * Hp;
 #pragma unroll
                 for (int d = 0; d < EGT_MAX_PEERS; ++d) {
                     if (d < peers.n) {
@@ -1058,6 +1068,9 @@ cudaError_t launch_gradient(const DevGame& G, const DevPlayer& P, int player, Ve
 static constexpr int TH_HPL = TREE_HPL, TH_HANDS = 32 * TH_HPL, TH_WARPS = TREE_WARPS, TH_NT = 32 * TH_WARPS;
 #ifndef TREE_MIN_CTAS
 #define TREE_MIN_CTAS 4
+#endif
+#ifndef TREE_MIN_CTAS_LB
+#define TREE_MIN_CTAS_LB 4
 #endif
 
 size_t tree_smem_bytes(const DevPlayer& P, int esz) {
@@ -1358,7 +1371,8 @@ __device__ __forceinline__ void tree_node_down_any(const TreeDownCtx<T>& D, bool
 }
 
 template <class T, int MODE, int OUTS>
-__global__ void __launch_bounds__(TH_NT, TREE_MIN_CTAS) tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
+__global__ void __launch_bounds__(TH_NT, (OUTS & TO_LB) ? TREE_MIN_CTAS_LB : TREE_MIN_CTAS)
+    tree_kernel(DevGame G, DevPlayer P, int player, TreeArgs A) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     double* s_exptab = reinterpret_cast<double*>(sm_raw);        // [64] 2^(j/64) (fp64 exp only)
     T* tile = reinterpret_cast<T*>(s_exptab + 64);                // [n_pub][TH_HANDS]
