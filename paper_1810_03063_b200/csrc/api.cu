@@ -1168,6 +1168,8 @@ static int egt_omega_gradient(egt_game* G, double* out) {
 // y_mu(x0) (cache C[1]) and the values the excessive-gap check needs.  g_omega: A^T x_omega
 // already evaluated (the mu search), or nullptr to evaluate it here.  mask: only the games
 // with mask[g] == 1 (the mu scan's games still scanning), or nullptr for all.
+// With a mask (a round of the practical-mu scan) only the values the excessive-gap test reads
+// are produced: the caches C and XQ come from the final, unmasked call.
 static int egt_initial_point(egt_game* G, double* g_omega, const int* mask = nullptr) {
     const int Gn = G->host.n_games;
     DevScalars& S = G->sc;
@@ -1193,7 +1195,7 @@ static int egt_initial_point(egt_game* G, double* g_omega, const int* mask = nul
     A.gsign = GSIGN[0];
     A.mu = S.mu;
     A.out_q = slot2(G, G->S[0], 0, 0);
-    A.out_lb = slot2(G, G->C[0], 0, 0);
+    if (!mask) A.out_lb = slot2(G, G->C[0], 0, 0);
     A.value = S.val;
     A.partial = G->partial;
     A.counter = G->counter;
@@ -1207,8 +1209,10 @@ static int egt_initial_point(egt_game* G, double* g_omega, const int* mask = nul
     A.g = vec(G->GR[1], G->V[1]);
     A.gsign = GSIGN[1];
     A.mu = S.mu + Gn;
-    A.out_lb = slot2(G, G->C[1], 1, 0);
-    A.out_q = slot2(G, G->XQ[1], 1, 0);
+    if (!mask) {
+        A.out_lb = slot2(G, G->C[1], 1, 0);
+        A.out_q = slot2(G, G->XQ[1], 1, 0);
+    }
     A.value = S.val + Gn;
     A.partial = G->partial;
     A.counter = G->counter;

@@ -698,7 +698,15 @@ static void build_card_plan(const HostGame& G, const std::vector<std::vector<int
         }
     for (int col = 0; col < 16; ++col)
         if (16 * ccount[col] > CARD_EX) throw std::runtime_error("card plan: ex exchange region too small");
-    const int zero_cell = 2 * NP;  // w region: w1 [0, NP), w2 [NP, 2 NP), a zero cell
+    // w region: w1 [0, NP), w2 [NP, 2 NP), then 16 zero cells, one per bank pair (2 NP is a
+    // multiple of 16): the padding slots of a read group gather from the zero cell of a bank
+    // pair no real slot of the group reads, so they never conflict (padding lanes of one group
+    // share that cell: a broadcast)
+    const int zero_cell = 2 * NP;
+    std::vector<uint32_t> group_used((size_t)n_rg, 0u);
+    for (size_t q = 0; q < slots.size(); ++q)
+        group_used[(size_t)(slots[q].thread / 16) * CH + slots[q].s] |=
+            1u << ((waddr[slots[q].which][slots[q].pos] + slots[q].which * NP) % 16);
     plan.pw.assign(NP, 0u);
     plan.pr.assign(NP, 0u);
     for (int i = 0; i < nv; ++i) {
@@ -709,7 +717,10 @@ static void build_card_plan(const HostGame& G, const std::vector<std::vector<int
     for (int t = 0; t < NT; ++t) {
         uint32_t* L = &plan.lane[(size_t)t * 8];
         for (int s = 0; s < CH; ++s) {
-            const uint32_t z = (uint32_t)(zero_cell * 8);
+            const uint32_t used = group_used[(size_t)(t / 16) * CH + s];
+            int free_col = 0;
+            while (free_col < 16 && ((used >> free_col) & 1u)) ++free_col;
+            const uint32_t z = (uint32_t)((zero_cell + (free_col & 15)) * 8);
             L[s / 2] |= (s & 1) ? z << 16 : z;
             const int pa = pad_addr[(size_t)t * CH + s];
             if (pa >= 0) L[3 + s / 2] |= (s & 1) ? (uint32_t)pa << 16 : (uint32_t)pa;

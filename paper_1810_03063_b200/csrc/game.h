@@ -105,7 +105,7 @@ struct Terminal {
 //            position i reads the slots of its two cards.
 constexpr int CARD_NT = 416, CARD_K = 3, CARD_GL = 8, CARD_CH = 6;
 constexpr int CARD_NP = CARD_NT * CARD_K;            // positions (>= H_pad)
-constexpr int CARD_WREGION = 2 * CARD_NP + 2;        // doubles: w1, w2, a zero cell (+ pad)
+constexpr int CARD_WREGION = 2 * CARD_NP + 16;       // doubles: w1, w2, 16 zero cells (one per bank pair)
 constexpr int CARD_EX = 16 * 192;                    // doubles of the ex exchange (every slot, padding
                                                      // included, has its own conflict-free address)
 // one board's plan as one word array (the kernel keeps one pointer): pw, pr, lohi, lane

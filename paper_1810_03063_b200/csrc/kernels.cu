@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
         const DevTerm tm = G.terms[t_idx[i]];
         t_so[i] = player ? tm.seq[0] : tm.seq[1];
         t_kind[i] = tm.kind;
-        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount;
+        t_w[i] = tm.kappa * G.kappa_game[g] * tm.amount * (tm.kind == 2 && player ? -1.0 : 1.0);  // + showdown sign
     }
     __syncthreads();
     // per terminal: its opponent row, the row it completes, and the decisions every thread
@@ -502,9 +502,19 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
     const uint4* __restrict__ lane_g = reinterpret_cast<const uint4*>(tab + CARD_TAB_LANE) + tid * 2;
     const uint4 la = __ldg(lane_g), lb = __ldg(lane_g + 1);
     uint32_t cg[3] = {la.x, la.y, la.z};
-    const uint32_t flags = lb.z;
-    const int src_lo = (int)(lb.w & 31u), src_hi = (int)((lb.w >> 8) & 31u);
-    const T sd_sign = player == 0 ? T(1) : T(-1);
+    uint32_t flags = lb.z, srcs = lb.w;
+    // per position: its w1 / w2 addresses and its tie group's bounds as byte offsets into Pf
+    uint32_t pwr[K], plh[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int i = base + j;
+        pwr[j] = i < H ? __ldg(tab + CARD_TAB_PW + i) : 0u;
+        const uint32_t lh = i < H ? __ldg(tab + CARD_TAB_LOHI + i) : 0u;
+        plh[j] = (lh & 0xFFFFu) * sizeof(T) | ((lh >> 16) * sizeof(T)) << 16;
+    }
+    const unsigned char* const pfb = reinterpret_cast<const unsigned char*>(Pf);
+    T* const gdst = gout.at<T>(g);
+    const long long goff = (long long)g * gout.game_stride;
     const T ct = COMB ? (T)ctau[g] : T(0), ct1 = T(1) - ct;  // Alg. 2 line 1
     const T* __restrict__ pself_g = static_cast<const T*>(player ? G.prior[1] : G.prior[0]) + (size_t)g * Hp;
     unsigned char* const wbytes = reinterpret_cast<unsigned char*>(wreg);
@@ -520,6 +530,11 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
     __syncthreads();  // the processing order
     int q = 1;  // the buffer holding the current opponent row
     for (int li = 0; li < nT; ++li) {
+        // per-thread words re-enter the loop opaque (decoded where used; see grad_staged_kernel)
+#pragma unroll
+        for (int j = 0; j < K; ++j) asm volatile("" : "+r"(pwr[j]), "+r"(plh[j]));
+        asm volatile("" : "+r"(cg[0]), "+r"(cg[1]), "+r"(cg[2]), "+r"(flags), "+r"(srcs));
+        const int src_lo = (int)(srcs & 31u), src_hi = (int)((srcs >> 8) & 31u);
         const uint32_t meta = t_meta[li];
         const int so = (int)(meta & 0xFFFu);
         const bool sd = (meta >> 24) & 1u;
@@ -538,7 +553,7 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
             mbar_wait(&bar[1 + q], (par >> q) & 1u);
             par ^= 1u << q;
         }
-        T dsd[CH];
+        const T scale = (T)t_w[li];
         if (!reuse) {  // CTA-uniform
             // ---- position domain: w, its two conflict-free copies for the card lanes, warp scan
             const T* vrow = vb + q * NP;
@@ -550,9 +565,8 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
                 x[j] = so ? popp[base + j] * v : popp[base + j];
                 run += x[j];
                 if (base + j < H) {
-                    const uint32_t pw = __ldg(tab + CARD_TAB_PW + base + j);
-                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 0)) = x[j];
-                    *reinterpret_cast<T*>(wbytes + woff<T>(pw, 1)) = x[j];
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pwr[j], 0)) = x[j];
+                    *reinterpret_cast<T*>(wbytes + woff<T>(pwr[j], 1)) = x[j];
                 }
             }
             const T incl = warp_incl_scan(run, lane);
@@ -590,17 +604,20 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
                     if ((flags >> (12 + s)) & 1u) ft = ex[s] + y[s];
                 const T clo = __shfl_sync(0xffffffffu, lh, src_lo);
                 const T chi = __shfl_sync(0xffffffffu, ft, src_hi);
+                // the slot's card part of this terminal, accumulated at once (nothing per slot
+                // stays live across the barrier): Pc at the run's start + Pc at its end - S_c
+                T dsd[CH];
                 T cur = clo;
 #pragma unroll
                 for (int s = 0; s < CH; ++s) {
                     if ((flags >> (6 + s)) & 1u) cur = ex[s];
-                    dsd[s] = cur;  // Pc at the run's start
+                    dsd[s] = cur;
                 }
                 cur = chi;
 #pragma unroll
                 for (int s = CH - 1; s >= 0; --s) {
                     if ((flags >> (12 + s)) & 1u) cur = ex[s] + y[s];
-                    dsd[s] += cur - segS;  // + Pc at the run's end - S_c
+                    rc[s] += scale * (dsd[s] + (cur - segS));
                 }
             }
             // ---- position domain: block prefix of w
@@ -621,20 +638,18 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
             __syncthreads();
             ex_dirty = false;
         }
-        // ---- this terminal's contribution: position parts and card parts
-        const T scale = (T)t_w[li];
+        // ---- this terminal's contribution: position parts (and a fold's card parts)
         if (sd) {
 #pragma unroll
             for (int j = 0; j < K; ++j) {  // P at the tie group's bounds (a group's lanes share the address)
-                const uint32_t lh = __ldg(tab + CARD_TAB_LOHI + base + j);
-                racc[j] += scale * (sd_sign * (total - Pf[lh >> 16] - Pf[lh & 0xFFFFu]));
+                const T phi = *reinterpret_cast<const T*>(pfb + (plh[j] >> 16));
+                const T plo = *reinterpret_cast<const T*>(pfb + (plh[j] & 0xFFFFu));
+                racc[j] += scale * (total - phi - plo);
             }
-            const T sc2 = scale * sd_sign;
-#pragma unroll
-            for (int s = 0; s < CH; ++s) rc[s] += sc2 * dsd[s];
         } else {
 #pragma unroll
-            for (int j = 0; j < K; ++j) racc[j] += scale * (total + x[j]);
+            for (int j = 0; j < K; ++j)  // w(h) back from the position's own w1 cell
+                racc[j] += scale * (total + *reinterpret_cast<const T*>(wbytes + woff<T>(pwr[j], 0)));
             const T sS = scale * segS;
 #pragma unroll
             for (int s = 0; s < CH; ++s) rc[s] -= sS;
@@ -663,14 +678,14 @@ __global__ void __launch_bounds__(CARD_NT, CARD_MINB) grad_card_kernel(DevGame G
             }
             ex_dirty = true;
             if (peers.n == 0) {
-                T* __restrict__ dst = gout.at<T>(g) + (size_t)srow * Hp;
+                T* __restrict__ dst = gdst + (size_t)srow * Hp;
 #pragma unroll
                 for (int j = 0; j < K; ++j)
                     if (base + j < Hp) dst[base + j] = outv[j];
             } else {
                 // fused all-gather: the finished row goes straight into every shard's gradient
                 // buffer (peer memory over NVLink), overlapping the next terminals
-                const long long off = (long long)g * gout.game_stride + (long long)srow * Hp;
+                const long long off = goff + (long long)srow * Hp;
 #pragma unroll
                 for (int d = 0; d < EGT_MAX_PEERS; ++d) {  // constant indices: no local copy of peers
                     if (d < peers.n) {
@@ -1317,7 +1332,7 @@ struct TreeDownCtx {
 };
 
 // OUTS: the set of output rows (TO_* bits) fixed at compile time, or 0 = decided at run time
-enum TreeOuts { TO_B = 1, TO_Q = 2, TO_COMB = 4, TO_AVG = 8, TO_FUSEBR = 16, TO_LB = 32 };
+enum TreeOuts { TO_B = 1, TO_Q = 2, TO_COMB = 4, TO_AVG = 8, TO_FUSEBR = 16, TO_LB = 32, TO_VAL = 64 };
 
 template <int N, int MODE, int OUTS, class T>
 __device__ __forceinline__ void tree_node_down_n(const TreeDownCtx<T>& D, bool ok, T qp, T unif, int first,
@@ -1564,7 +1579,7 @@ __global__ void __launch_bounds__(TH_NT, (OUTS & TO_LB) ? TREE_MIN_CTAS_LB : TRE
     }
 
     // ---- top-down, shallowest level first
-    const bool want_td = OUTS ? (OUTS & ~(TO_FUSEBR | TO_LB)) != 0
+    const bool want_td = OUTS ? (OUTS & ~(TO_FUSEBR | TO_LB | TO_VAL)) != 0
                               : (A.out_b.ok() || A.out_q.ok() || A.comb_out.ok() || mode == TM_CFR);
     if (!want_td) return;
     T* __restrict__ ob = A.out_b.ok() ? A.out_b.at<T>(g) : nullptr;
@@ -1661,6 +1676,8 @@ cudaError_t launch_tree(const DevGame& G, const DevPlayer& P, int player, const 
     }
     // the solver's hot (mode, outputs) combinations get fully specialised kernels
     if (A.mode == TM_SBR && outs == (TO_LB | TO_Q)) EGT_TREE_GO(TM_SBR, TO_LB | TO_Q)
+    if (A.mode == TM_SBR && outs == TO_Q) EGT_TREE_GO(TM_SBR, TO_Q)
+    if (A.mode == TM_SBR && outs == 0 && A.value) EGT_TREE_GO(TM_SBR, TO_VAL)  // value only: no descent
     if (A.mode == TM_SBR && outs == (TO_Q | TO_COMB)) EGT_TREE_GO(TM_SBR, TO_Q | TO_COMB)
     if (A.mode == TM_PROX && outs == TO_COMB) EGT_TREE_GO(TM_PROX, TO_COMB)
     if (A.mode == TM_COMBINE && outs == TO_COMB) EGT_TREE_GO(TM_COMBINE, TO_COMB)
@@ -1701,6 +1718,7 @@ static cudaError_t prepare_t() {
                         (const void*)tree_kernel<T, TM_BR, 0>,      (const void*)tree_kernel<T, TM_CFR, 0>,
                         (const void*)tree_kernel<T, TM_UNIFORM, 0>, (const void*)tree_kernel<T, TM_COMBINE, 0>,
                         (const void*)tree_kernel<T, TM_SBR, TO_LB | TO_Q>, (const void*)tree_kernel<T, TM_SBR, TO_Q | TO_COMB>,
+                        (const void*)tree_kernel<T, TM_SBR, TO_Q>, (const void*)tree_kernel<T, TM_SBR, TO_VAL>,
                         (const void*)tree_kernel<T, TM_PROX, TO_COMB>, (const void*)tree_kernel<T, TM_COMBINE, TO_COMB>,
                         (const void*)tree_kernel<T, TM_CFR, TO_Q | TO_AVG>,
                         (const void*)tree_kernel<T, TM_SBR, TO_LB | TO_Q | TO_FUSEBR>};

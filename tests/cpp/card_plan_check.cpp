@@ -93,6 +93,7 @@ int main(int argc, char** argv) {
         for (int hw = 0; hw < NT / 16; ++hw)
             for (int s = 0; s < CH; ++s) {
                 std::set<int> rbanks, xbanks;
+                std::set<unsigned> pad_cell;
                 for (int l = 0; l < 16; ++l) {
                     const int t = hw * 16 + l;
                     const uint32_t* L = &pl.lane[(size_t)t * 8];
@@ -108,7 +109,12 @@ int main(int argc, char** argv) {
                     if (!xbanks.insert(px % 16).second) fail("ex write conflict", g, hw, s);
                     if (ex_slot_pos[px] != -1) fail("ex address shared", g, t, s);
                     if (!valid) {
-                        if (cg / 8 != (unsigned)(2 * NP)) fail("padding slot not on the zero cell", g, t, s);
+                        if (cg / 8 < (unsigned)(2 * NP) || cg / 8 >= (unsigned)CARD_WREGION)
+                            fail("padding slot not on a zero cell", g, t, s);
+                        // padding lanes of a group may share their zero cell (a broadcast), but
+                        // no real lane of the group may use its bank pair
+                        if (pad_cell.insert(cg / 8).second && !rbanks.insert((cg / 8) % 16).second)
+                            fail("w read conflict (zero cell)", g, hw, s);
                         ex_slot_pos[px] = -2;  // a padding slot's private address (never read)
                         continue;
                     }
