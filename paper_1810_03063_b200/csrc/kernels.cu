@@ -936,12 +936,15 @@ __global__ void __launch_bounds__(CARD_NT, 2) grad_staged_kernel(DevGame G, DevP
         }
         // ---- phase C (positions beyond H compute on padding and are never stored)
         const T scale = (T)t_w[li];
+        T pg = T(0);  // P[lo] + P[hi] of the previous position's tie group
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             T v = total - ldo(pa[j][0], 0) - ldo(pa[j][0], 1);
             if (sd) {
-                v += -(ldo(pa[j][3], 0) + ldo(pa[j][3], 1)) + ldo(pa[j][1], 0) + ldo(pa[j][1], 1) +
-                     ldo(pa[j][2], 0) + ldo(pa[j][2], 1);
+                // a position in the same tie group as the thread's previous one reuses its P
+                // bounds (predicated-off lanes issue no shared-memory wavefronts)
+                if (j == 0 || pa[j][3] != pa[j - 1][3]) pg = ldo(pa[j][3], 0) + ldo(pa[j][3], 1);
+                v += -pg + ldo(pa[j][1], 0) + ldo(pa[j][1], 1) + ldo(pa[j][2], 0) + ldo(pa[j][2], 1);
             } else {
                 v += *reinterpret_cast<const T*>(wbytes + woff<T>(pwr[j], 0));
             }
