@@ -583,18 +583,24 @@ def run_b200(args):
             line["time_to_gap"] = conv
         # the whole batch to 10 mbb through solve(): every game until its own eps_sad <= 10 mbb,
         # solved games stopped on the device (egt_set_target); wall clock of the call
+        # Each solver runs twice on fresh games: the first call of a process after the batch runs
+        # above has shown host-side stalls of up to ~1.5 s (not in a process that only solves:
+        # scratch runs of 2026-10-19, 0.52 s for both solvers), so both calls are reported.
         solved = {}
         for sv in ("egt_as", "cfr_plus"):
-            gs = P.Game(P.RIVER, n_games=n, river=spec, boards=boards[:n], prior1=p1[:n], prior2=p2[:n],
-                        precision=args.precision)
-            gs.set_stream(torch.cuda.current_stream())
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            res = P.solve(gs, sv, eps_mbb=10.0, max_iters=args.converge_max_steps)
-            torch.cuda.synchronize()
-            solved[sv] = {"seconds": time.perf_counter() - t0, "iterations": int(res["iters"]),
+            secs = []
+            for _ in range(2):
+                gs = P.Game(P.RIVER, n_games=n, river=spec, boards=boards[:n], prior1=p1[:n], prior2=p2[:n],
+                            precision=args.precision)
+                gs.set_stream(torch.cuda.current_stream())
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = P.solve(gs, sv, eps_mbb=10.0, max_iters=args.converge_max_steps)
+                torch.cuda.synchronize()
+                secs.append(time.perf_counter() - t0)
+                gs.close()
+            solved[sv] = {"seconds": secs[1], "seconds_first_call": secs[0], "iterations": int(res["iters"]),
                           "max_gap_mbb": float(np.max(res["gap"])) / (spec["big_blind"] / 1000.0)}
-            gs.close()
         if rank == 0:
             line["solve_batch_to_10mbb"] = dict(solved, games=n, what="P.solve(..., eps_mbb=10) on the same "
                                                 "games from a cold start (incl. init and mu search): every game "
