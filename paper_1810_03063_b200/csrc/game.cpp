@@ -595,38 +595,45 @@ static void build_table(const HostGame& G, int g, int bs, const std::vector<int>
 static std::vector<int> colour_edges16(int n_left, int n_right, const std::vector<std::pair<int, int>>& edges) {
     constexpr int C = 16;
     std::vector<int> at_l((size_t)n_left * C, -1), at_r((size_t)n_right * C, -1), col(edges.size(), -1);
-    auto free_l = [&](int u) { for (int c = 0; c < C; ++c) if (at_l[(size_t)u * C + c] < 0) return c; return -1; };
-    auto free_r = [&](int v) { for (int c = 0; c < C; ++c) if (at_r[(size_t)v * C + c] < 0) return c; return -1; };
+    std::vector<uint32_t> used_l(n_left, 0u), used_r(n_right, 0u);  // colours in use at a vertex
+    std::vector<int> path;
+    auto set = [&](int e, int c) {
+        col[e] = c;
+        at_l[(size_t)edges[e].first * C + c] = e;
+        at_r[(size_t)edges[e].second * C + c] = e;
+        used_l[edges[e].first] |= 1u << c;
+        used_r[edges[e].second] |= 1u << c;
+    };
     for (size_t k = 0; k < edges.size(); ++k) {
         const int u = edges[k].first, v = edges[k].second;
-        const int a = free_l(u), b = free_r(v);
-        if (a < 0 || b < 0) throw std::runtime_error("edge colouring: degree above 16");
-        if (at_r[(size_t)v * C + a] >= 0) {
-            // a is taken at v: swap a and b along the alternating path that starts at v with
-            // colour a (it cannot reach u, where a is free), freeing a at v
-            std::vector<int> path;
-            int x = v, side = 1, c = a;
-            while (true) {
-                const int e = side ? at_r[(size_t)x * C + c] : at_l[(size_t)x * C + c];
-                if (e < 0) break;
-                path.push_back(e);
-                x = side ? edges[e].first : edges[e].second;
-                side ^= 1;
-                c = c == a ? b : a;
-            }
-            for (int e : path) {
-                at_l[(size_t)edges[e].first * C + col[e]] = -1;
-                at_r[(size_t)edges[e].second * C + col[e]] = -1;
-            }
-            for (int e : path) {
-                col[e] = col[e] == a ? b : a;
-                at_l[(size_t)edges[e].first * C + col[e]] = e;
-                at_r[(size_t)edges[e].second * C + col[e]] = e;
-            }
+        const uint32_t both = ~(used_l[u] | used_r[v]) & 0xFFFFu;
+        if (both) {  // a colour free at both ends: no recolouring
+            set((int)k, __builtin_ctz(both));
+            continue;
         }
-        col[k] = a;
-        at_l[(size_t)u * C + a] = (int)k;
-        at_r[(size_t)v * C + a] = (int)k;
+        const uint32_t fl = ~used_l[u] & 0xFFFFu, fr = ~used_r[v] & 0xFFFFu;
+        if (!fl || !fr) throw std::runtime_error("edge colouring: degree above 16");
+        const int a = __builtin_ctz(fl), b = __builtin_ctz(fr);
+        // a is taken at v: swap a and b along the alternating path that starts at v with colour
+        // a (it cannot reach u, where a is free), freeing a at v
+        path.clear();
+        int x = v, side = 1, c = a;
+        while (true) {
+            const int e = side ? at_r[(size_t)x * C + c] : at_l[(size_t)x * C + c];
+            if (e < 0) break;
+            path.push_back(e);
+            x = side ? edges[e].first : edges[e].second;
+            side ^= 1;
+            c = c == a ? b : a;
+        }
+        for (int e : path) {
+            at_l[(size_t)edges[e].first * C + col[e]] = -1;
+            at_r[(size_t)edges[e].second * C + col[e]] = -1;
+            used_l[edges[e].first] &= ~(1u << col[e]);
+            used_r[edges[e].second] &= ~(1u << col[e]);
+        }
+        for (int e : path) set(e, col[e] == a ? b : a);
+        set((int)k, a);
     }
     return col;
 }
