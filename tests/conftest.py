@@ -33,10 +33,11 @@ def pytest_collection_modifyitems(config, items):
 def pytest_terminal_summary(terminalreporter):
     """Worst per-element relative CUDA-vs-oracle error of each parity check this session."""
     try:
-        from tests.paritylib import REPORT
+        from tests.paritylib import BOUND, REPORT
     except Exception:
         return
     if REPORT:
-        terminalreporter.write_sep("-", "parity: worst per-element relative error (entries >= 1e-6 max)")
+        terminalreporter.write_sep("-", "parity: worst per-element relative error (entries >= 1e-6 max) | worst "
+                                        "error / allowed bound (<= 1 passes)")
         for k in sorted(REPORT):
-            terminalreporter.write_line("%-48s %.3e" % (k, REPORT[k]))
+            terminalreporter.write_line("%-48s %.3e | %.3f" % (k, REPORT[k], BOUND.get(k, 0.0)))
