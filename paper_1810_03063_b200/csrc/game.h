@@ -16,7 +16,10 @@ namespace egt {
 // private hands per game the gradient kernel handles (256 threads x 5 positions)
 constexpr int EGT_MAX_HANDS = 1280;
 // warps of the treeplex kernel; each level's nodes are scheduled onto them on the host
-constexpr int TREE_WARPS = 8;
+#ifndef TREE_WARPS_DEF
+#define TREE_WARPS_DEF 8
+#endif
+constexpr int TREE_WARPS = TREE_WARPS_DEF;
 // terminals per CTA of the staged river gradient kernel (rows are never split)
 #ifndef EGT_GRAD_CHUNK_TERMS
 #define EGT_GRAD_CHUNK_TERMS 16
