@@ -40,4 +40,4 @@ def pytest_terminal_summary(terminalreporter):
         terminalreporter.write_sep("-", "parity: worst per-element relative error (entries >= 1e-6 max) | worst "
                                         "error / allowed bound (<= 1 passes)")
         for k in sorted(REPORT):
-            terminalreporter.write_line("%-48s %.3e | %.3f" % (k, REPORT[k], BOUND.get(k, 0.0)))
+            terminalreporter.write_line("%-48s %.3e | %.2e" % (k, REPORT[k], BOUND.get(k, 0.0)))

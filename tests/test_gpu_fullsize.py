@@ -297,3 +297,37 @@ def test_bench_workload_longer_runs(bench_pair, solver):
     gaps = G.saddle_gap(which)
     want = br.saddle_gap(sf, want_x, want_y)
     assert_scalar(gaps[g], want, TOL, "bench-batch long-run eps_sad")
+
+
+def _sweep_specs():
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import grad_sweep
+    return grad_sweep.specs()
+
+
+@pytest.mark.parametrize("which", range(5))
+def test_sweep_abstractions_gradient(which):
+    """BASELINE.json configs[4]'s five bet abstractions (tools/grad_sweep.py), from 18 to 348
+    public sequences per player and 23 to 463 terminals -- the largest trees the gradient kernel
+    is timed on, with the most terminals per chunk and the longest sequence indices -- on full
+    52-card river boards with bench-style priors: both gradients per element against the oracle
+    (Gen-CFR lines 29/35)."""
+    name, spec = _sweep_specs()[which]
+    boards = workloads.random_boards(4, seed=700 + which)
+    priors = workloads.random_priors(boards, seed=700 + which)
+    pair = Pair("river", n_games=4, spec=spec, boards=boards, priors=priors, sample=(0, 3), build_sparse=False)
+    G = pair.game
+    for p in (0, 1):
+        blocks, vals = _full_inputs(pair, 1 - p, np.random.default_rng(710 + which + p), (0, 3))
+        dout = torch.full((G.n_games,) + G.vec_shape(p)[1:], np.nan, dtype=torch.float64, device="cuda")
+        G.egt_gradient(p, dev(blocks), dout)
+        out = host(dout).reshape(G.n_games, -1)
+        assert np.isfinite(out).all(), name
+        for g in (0, 3):
+            sf = pair.sf[g]
+            want = sf.Ay(vals[g]) if p == 0 else sf.ATx(vals[g])
+            got = pair.from_product(g, p, out[g])
+            got[0] = out[g][:G.H_pad].sum()
+            assert_parity(got, want, TOL, "sweep-abstraction gradient")
