@@ -313,7 +313,8 @@ def test_sweep_abstractions_gradient(which):
     public sequences per player and 23 to 463 terminals -- the largest trees the gradient kernel
     is timed on, with the most terminals per chunk and the longest sequence indices -- on full
     52-card river boards with bench-style priors: both gradients per element against the oracle
-    (Gen-CFR lines 29/35)."""
+    (Gen-CFR lines 29/35), then the smoothed best response and the best response
+    on the same treeplexes."""
     name, spec = _sweep_specs()[which]
     boards = workloads.random_boards(4, seed=700 + which)
     priors = workloads.random_priors(boards, seed=700 + which)
@@ -331,3 +332,29 @@ def test_sweep_abstractions_gradient(which):
             got = pair.from_product(g, p, out[g])
             got[0] = out[g][:G.H_pad].sum()
             assert_parity(got, want, TOL, "sweep-abstraction gradient")
+    # the treeplex passes on the same trees (nodes of up to 11 actions go through the
+    # kernel's generic in-shared-memory path): smoothed best response and best response
+    rng = np.random.default_rng(720 + which)
+    for p, gsign in ((0, 1.0), (1, -1.0)):
+        gs = np.zeros((G.n_games, G.n_pub[p] * G.H_pad))
+        mus = np.ones(G.n_games)
+        wants = {}
+        for g in (0, 3):
+            v = rng.standard_normal(pair.tp(g, p).n_seq) * 50.0
+            gs[g] = pair.to_product(g, p, v)
+            gs[g][0] = v[0]
+            mus[g] = float(np.exp(rng.uniform(-1, 3)))
+            wants[g] = (dgf.smoothed_best_response(pair.tp(g, p), gsign * v, mus[g]),
+                        br.best_response(pair.tp(g, p), gsign * v, "min")[0])
+        dg = dev(gs.reshape((G.n_games,) + G.vec_shape(p)[1:]))
+        dq = torch.zeros(G.vec_shape(p), dtype=torch.float64, device="cuda")
+        val = torch.zeros(G.n_games, dtype=torch.float64, device="cuda")
+        bval = torch.zeros_like(val)
+        G.egt_smoothed_br(p, dg, gsign, dev(mus), dq, None, val)
+        G.egt_best_response(p, dg, gsign, bval)
+        q, vals, bvals = host(dq).reshape(G.n_games, -1), host(val), host(bval)
+        for g in (0, 3):
+            (wq, wv), wb = wants[g]
+            assert_parity(pair.from_product(g, p, q[g])[1:], wq[1:], TOL, "sweep-abstraction sbr q")
+            assert_scalar(vals[g], wv, TOL, "sweep-abstraction sbr value")
+            assert_scalar(bvals[g], wb, TOL, "sweep-abstraction br value")
