@@ -1525,13 +1525,25 @@ __global__ void __launch_bounds__(TH_NT, (OUTS & TO_LB) ? TREE_MIN_CTAS_LB : TRE
     C.lbo = lbo;
     T* __restrict__ cz = A.center.ok() ? A.center.at<T>(g) : nullptr;
     T* __restrict__ rg = A.regret.ok() ? A.regret.at<T>(g) : nullptr;
+    // the global rows a node's bottom-up work reads (prox centre logs; CFR strategy and
+    // regrets): the next node's are requested into L1 while this one is processed
+    auto prefetch_up = [&](int m2) {
+        if (MODE != TM_PROX && MODE != TM_CFR) return;
+        const int f2 = s_first[m2], n2 = s_nact[m2];
+        for (int a = 0; a < n2; ++a) {
+            if (cz) asm volatile("prefetch.global.L1 [%0];" ::"l"(cz + (size_t)(f2 + a) * Hp + h0 + lane));
+            if (MODE == TM_CFR && rg) asm volatile("prefetch.global.L1 [%0];" ::"l"(rg + (size_t)(f2 + a) * Hp + h0 + lane));
+        }
+    };
     if (has_grad) {
         for (int L = n_lv - 1; L >= 0; --L) {
             const int i0 = s_so[L * TH_WARPS + wid], i1 = s_so[L * TH_WARPS + wid + 1];
+            if (i0 < i1) prefetch_up(s_sn[i0]);
             for (int idx = i0; idx < i1; ++idx) {
                 const int m = s_sn[idx];
                 const int first = s_first[m], n = s_nact[m], par = s_par[m], rs = s_rslot[m];
                 const T logn = s_logn[m];
+                if (idx + 1 < i1) prefetch_up(s_sn[idx + 1]);
 #pragma unroll
                 for (int j = 0; j < TH_HPL; ++j) {
                     const int c = lane + 32 * j, h = h0 + c;
