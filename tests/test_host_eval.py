@@ -36,3 +36,18 @@ def test_card_plan_conflict_free_and_exact(tmp_path):
     out = subprocess.run([str(exe), "48"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout
     assert "violations 0" in out.stdout
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="needs g++")
+def test_edge_colouring_on_random_multigraphs(tmp_path):
+    """The card plan's 16-edge-colouring of bipartite multigraphs (game.cpp colour_edges16: a
+    colour free at both ends when one exists, an alternating-path swap otherwise) is proper on
+    200 random multigraphs of maximum degree 16, most of them 16-regular with repeated edges --
+    the colouring Koenig's theorem guarantees (index work: exact)."""
+    exe = tmp_path / "colour_check"
+    csrc = os.path.join(ROOT, "paper_1810_03063_b200", "csrc")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-pthread", "-I", os.path.join(ROOT, "include"), "-I", csrc,
+                    os.path.join(ROOT, "tests", "cpp", "colour_check.cpp"), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "200"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout
+    assert "violations 0" in out.stdout
