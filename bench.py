@@ -466,6 +466,9 @@ def run_b200(args):
     roof["other_kernel"] = {"kernel": other, "achieved": sum(kt[k][3] for k in ko) / (ms_o / 1e3) / 1e9,
                             "frac": sum(kt[k][3] for k in ko) / (ms_o / 1e3) / 1e9 / peak,
                             "share_of_step": ms_o / tot_ms}
+    lim_o = (ncu_entry("grad" if other.startswith("grad") else "tree", args.workload) or {}).get("limiter")
+    if lim_o:
+        roof["other_kernel"]["limiter"] = lim_o
     kernel_split = {k: {"ms_per_step": v[0] / args.timing_steps, "launches_per_step": v[1] / args.timing_steps,
                         "gbs": (v[3] / (v[0] / 1e3) / 1e9) if v[0] > 0 else None}
                     for k, v in kt.items()}
